@@ -1,0 +1,391 @@
+"""bench.py — pencils/s and FP64 TFLOP/s of the hot path (S_1..S_d + Vandermonde/LS), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--cfg cfg4] [--impl ours|reference]
+
+A step is one whole pencil of the headline workload (BASELINE.json configs[3], "cfg4": d=2,
+n=200, N=40401, m=100, complex-Gaussian noise sigma=1e-6): prony_project over this rank's
+units + prony_vandermonde_ls over its columns (+ the NCCL all-reduce of the packed partials
+and the m x m solve when N > 1). Inputs are resident in HBM; L2 is flushed (a 256 MiB write)
+before every timed step, outside the timed interval. Timing: CUDA events per step on the
+launching stream, barrier + synchronize around the loop, max over ranks.
+
+e2e: the same pencil through the C ABI with HOST buffers (prony_pencil_host: pinned host ->
+device copies of grid, U, V, sigma, z, the device path, device -> host copies of S, G, b, c, t).
+
+--impl reference: the CPU oracle (oracle/, plain C, all host cores) on a bounded sample of the
+same workload per step, extrapolated to pencils/s (this tier has no installable reference).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workload as W  # noqa: E402
+
+METRIC = "pencils/s and FP64 TFLOP/s (% peak) for S_1..S_d+LS, d=2 N=40401 m=100, 1/2/4/8 GPUs"
+UNIT = "pencils/s"
+
+
+def pencil_flops(d, N, m):
+    """Algorithmic flops of one pencil: d(8mN^2 + 8Nm^2) + 8m^2 N + 8mN."""
+    return d * (8.0 * m * N * N + 8.0 * N * m * m) + 8.0 * m * m * N + 8.0 * m * N
+
+
+# ------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s, p in zip(sm, power) if p > 300.0] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------ reference arm
+def run_reference(args, cfg):
+    """The oracle, as it stands, on host cores: each step = a bounded sample of one pencil
+    (rows [0, R) of T_1 V plus U^* for the pencil part; columns [0, C) of A, G, b for LS),
+    extrapolated to a full pencil."""
+    import oracle
+    oracle.build()
+    prob = W.make_problem(cfg)
+    c = prob.cfg
+    d, n, m, N = c.d, c.n, c.m, c.N
+    # calibrate the sample to ~3 s of project work per step
+    R = 8
+    t0 = time.perf_counter()
+    oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, R)
+    per_row = (time.perf_counter() - t0) / R
+    R = int(max(8, min(N, 3.0 / max(per_row, 1e-9))))
+    Cc = min(N, 4096)
+
+    def step():
+        t0 = time.perf_counter()
+        oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, R)
+        t_proj = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        A = oracle.vandermonde(prob.z, d, n, 0, Cc)
+        oracle.ls_products(A, prob.grid, d, n, 0, Cc)
+        t_ls = time.perf_counter() - t0
+        return t_proj * (d * N / R) + t_ls * (N / Cc)
+
+    for _ in range(args.warmup):
+        step()
+    est = [step() for _ in range(args.steps)]
+    sec = statistics.median(est)
+    value = 1.0 / sec
+    sample = (f"per step: oracle_project_rows rows [0,{R}) of T_1 (of d*N={d * N} row-units) + "
+              f"vandermonde+ls_products on columns [0,{Cc}) of N={N}; extrapolated linearly to one pencil")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{c.name}: d={d} n={n} N={N} m={m} noise={c.noise}", "d": d, "n": n, "N": N, "m": m,
+                   "parallelism": "host threads (OpenMP)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "tflops": pencil_flops(d, N, m) * value / 1e12,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(prob, budget_s=12.0):
+    """cpu_baseline leg (rank 0, N=1): the oracle on a bounded sample of the bench workload."""
+    import oracle
+    oracle.build()
+    c = prob.cfg
+    d, n, m, N = c.d, c.n, c.m, c.N
+    R = 8
+    t0 = time.perf_counter()
+    oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, R)
+    per_row = (time.perf_counter() - t0) / R
+    R = int(max(8, min(N, 0.8 * budget_s / max(per_row, 1e-9))))
+    t0 = time.perf_counter()
+    oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, R)
+    t_proj = time.perf_counter() - t0
+    Cc = min(N, 8192)
+    t0 = time.perf_counter()
+    A = oracle.vandermonde(prob.z, d, n, 0, Cc)
+    oracle.ls_products(A, prob.grid, d, n, 0, Cc)
+    t_ls = time.perf_counter() - t0
+    sec = t_proj * (d * N / R) + t_ls * (N / Cc)
+    return {"value": 1.0 / sec, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": (f"oracle_project_rows on rows [0,{R}) of T_1 ({t_proj:.1f} s) + vandermonde/ls_products on "
+                       f"columns [0,{Cc}) ({t_ls:.1f} s), extrapolated to one pencil of {c.name} "
+                       f"({d * N} row-units, {N} columns): {sec:.0f} s per pencil")}
+
+
+# ------------------------------------------------------------------------------------ our arm
+def zgemm_peak_tflops(torch, n=4096, reps=5):
+    """cuBLAS ZGEMM (complex128) throughput measured now: the FP64-tensor roofline denominator."""
+    a = torch.randn(n, n, dtype=torch.complex128, device="cuda")
+    b = torch.randn(n, n, dtype=torch.complex128, device="cuda")
+    c = torch.empty_like(a)
+    for _ in range(2):
+        torch.matmul(a, b, out=c)
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(reps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch.matmul(a, b, out=c)
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del a, b, c
+    return 8.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2012_11430_b200 as pb
+    from paper_2012_11430_b200 import sharding
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    prob = W.make_problem(cfg)
+    c = prob.cfg
+    d, n, m, N = c.d, c.n, c.m, c.N
+    order = sharding.default_unit_order(d, world)
+    u0, u1 = sharding.unit_range(d, n, world, rank)
+    c0, c1 = sharding.column_range(d, n, world, rank)
+
+    tg = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    grid, U, V, sigma, z = tg(prob.grid), tg(prob.U), tg(prob.V), tg(prob.sigma), tg(prob.z)
+    ws_p = pb.alloc_workspace(pb.WS_PROJECT, d, n, m, dev)
+    ws_l = pb.alloc_workspace(pb.WS_LS, d, n, m, dev)
+    S = torch.empty((d, m, m), dtype=torch.complex128, device=dev)
+    G = torch.empty((m, m), dtype=torch.complex128, device=dev)
+    b = torch.empty(m, dtype=torch.complex128, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def new_events(k):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        for e in evs:
+            e.record(stream)  # force creation so .cuda_event is a live handle
+        return evs
+
+    def step(info_p=None, info_l=None):
+        pb.project(grid, U, V, sigma, d, n, m, u0, u1, order, out=S, workspace=ws_p, stream=stream, info=info_p)
+        full = world == 1
+        outs = {"G": G, "b": b}
+        res = pb.vandermonde_ls(z, grid, d, n, m, c0, c1, want_solution=full, out=outs, workspace=ws_l,
+                                dev_status=st, stream=stream, info=info_l)
+        if world > 1:
+            Sr, Gr, br = sharding.allreduce_pencil(S, G, b)
+            cc, tt = pb.ls_solve(Gr.contiguous(), br.contiguous(), z, d, m, dev_status=st, stream=stream)
+            return Sr, cc, tt
+        return S, res["c"], res["t"]
+
+    # warm-up (also validates the device status once)
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0, f"device status {int(st.item())}"
+
+    K = args.steps
+    ev_s, ev_e = new_events(K), new_events(K)
+    ev_ps, ev_pe = new_events(K), new_events(K)
+    ev_ls, ev_le = new_events(K), new_events(K)
+    infos_p = [pb.make_exec_info(ev_ps[i], ev_pe[i]) for i in range(K)]
+    infos_l = [pb.make_exec_info(ev_ls[i], ev_le[i]) for i in range(K)]
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(K):
+        flush.fill_(i & 0xFF)                  # L2 flush outside the timed interval
+        ev_s[i].record(stream)
+        step(infos_p[i], infos_l[i])
+        ev_e[i].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+
+    step_ms = [ev_s[i].elapsed_time(ev_e[i]) for i in range(K)]
+    proj_ms = [ev_ps[i].elapsed_time(ev_pe[i]) for i in range(K)]
+    vls_ms = [ev_ls[i].elapsed_time(ev_le[i]) for i in range(K)]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms, sum(proj_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms_max = float(t[0])
+    launches_per_step = infos_p[0].launches + infos_l[0].launches + (1 if world > 1 else 0)
+
+    # ---- end to end through the host-buffer C-ABI call (N = 1) / host-staged sharded path (N > 1)
+    e2e = None
+    if world == 1:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        hg, hU, hV, hs, hz = pin(prob.grid), pin(prob.U), pin(prob.V), pin(prob.sigma), pin(prob.z)
+        outs = {k: torch.empty(s, dtype=dt).pin_memory() for k, s, dt in
+                [("S", (d, m, m), torch.complex128), ("G", (m, m), torch.complex128), ("b", (m,), torch.complex128),
+                 ("c", (m,), torch.complex128), ("t", (m, d), torch.float64)]}
+        ws_h = pb.alloc_workspace(pb.WS_PENCIL_HOST, d, n, m, dev)
+        for _ in range(2):
+            pb.pencil_host(hg, hU, hV, hs, hz, d, n, m, workspace=ws_h, outputs=outs, stream=stream)
+        Ke = max(2, min(K, 5))
+        e_ms = []
+        for i in range(Ke):
+            flush.fill_(i & 0xFF)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = pb.pencil_host(hg, hU, hV, hs, hz, d, n, m, workspace=ws_h, outputs=outs, stream=stream)
+            e1.record(stream)
+            e1.synchronize()
+            assert r["status"] == 0
+            e_ms.append(e0.elapsed_time(e1))
+        h2d = sum(x.numel() * x.element_size() for x in (hg, hU, hV, hs, hz))
+        d2h = sum(x.numel() * x.element_size() for x in outs.values()) + 4
+        e2e = {"value": Ke / (sum(e_ms) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": sum(e_ms) / Ke, "api": "prony_pencil_host (pinned host buffers)"}
+        del ws_h
+
+    # ---- roofline of the dominant kernel (k_project), measured live above
+    flops_proj = infos_p[0].main_flops
+    proj_avg_s = statistics.mean(proj_ms) * 1e-3
+    peak = zgemm_peak_tflops(torch) if rank == 0 else None
+
+    if rank == 0:
+        value = world * K / (total_ms_max * 1e-3)
+        ms_per_step = total_ms_max / K
+        F = pencil_flops(d, N, m)
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "r01_ncu_project.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            except (OSError, ValueError):
+                traffic = None
+        achieved = flops_proj / proj_avg_s / 1e12
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded planted exponential sum, complex Gaussian noise 1e-6)",
+            "config": {"workload": f"{c.name}: d={d} n={n} N={N} m={m} noise={c.noise} (BASELINE configs[3])",
+                       "d": d, "n": n, "N": N, "m": m, "parallelism": f"dp{world} ({'l-major' if order == 0 else 'row-major'} units)",
+                       "l2": "flushed (256 MiB write) before every timed step, outside the timed interval",
+                       "pencils_per_step": world},
+            "tflops": F * value / 1e12,
+            "pct_peak": (F * value / 1e12) / (peak * world) if peak else None,
+            "roofline": {"bound": "tensor", "kernel": "k_project (complex FP64 DMMA, implicit Toeplitz gather)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                         "traffic": traffic,
+                         "peak_source": "cuBLAS ZGEMM 4096^3 complex128 measured in this run (MEASURED_PEAKS.json has no FP64 entry)",
+                         "flops_per_launch": flops_proj, "avg_launch_ms": proj_avg_s * 1e3,
+                         "share_of_step": sum(proj_ms) / sum(step_ms),
+                         "grid": list(infos_p[0].main_grid), "split_k": infos_p[0].split_k},
+            "kernels_ms": {"k_project": statistics.mean(proj_ms), "k_vls": statistics.mean(vls_ms)},
+            "gpu_launches": launches_per_step * K,
+            "clocks": clk,
+            "e2e": e2e,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_sample(prob)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--cfg", default="cfg4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = W.CONFIGS[args.cfg]
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        run_reference(args, cfg)
+        return
+    from paper_2012_11430_b200 import _build
+    _build.build()
+    run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,230 @@
+/*
+ * prony.h — C ABI of the B200 (sm_100a) hot path of the multivariate matrix-pencil
+ * Prony method (arXiv 2012.11430; citations "P:<line>" are lines of PAPER.md).
+ *
+ * Problem (Algorithm 1): samples f(k) of f(k) = sum_{j=1..m} c_j e^{-2 pi i <t_j,k>}
+ * -> parameters t_j and coefficients c_j. This library implements the
+ * data-parallel steps of that algorithm that the paper puts on the GPU:
+ *
+ *   prony_project        S_l = U* T_l V Sigma^-1,  T_l = [f(k-h+e_l)]_{k,h in I_n}
+ *                        (P:21, P:27-29 eq_generateSl), T_l generated implicitly from the
+ *                        sample grid (never materialized), complex FP64 on the DMMA pipe.
+ *   prony_vandermonde_ls A = [z_j^k]_{j, k in I_n}, the normal-equation products
+ *                        G = A conj(A)^T, b = A conj(f) of argmin_c ||A^T c - f||_2,
+ *                        and, over the full column range, c = conj(G^-1 b) and
+ *                        t_j = (-arg z_j / 2 pi) mod 1 (reading R4).
+ *   prony_pencil_host    both of the above from HOST buffers (copies in, results out).
+ *   prony_build_pencil   reduced SVD of T (Alg. 3) + prony_project:
+ *                        not implemented in this round (returns PRONY_ERR_UNIMPLEMENTED).
+ *
+ * Layout conventions (readings R1, R2):
+ *   - complex numbers are prony_c128 {re, im} (== cuDoubleComplex == torch.complex128).
+ *   - I_n = {0..n}^d in lexicographic order, LAST coordinate fastest;
+ *     N = (n+1)^d. Row r of U, V and column r of A is element r of I_n.
+ *   - grid: f(k) for k in the box {-n..n+1}^d (L = 2n+2 points per axis, L^d values),
+ *     lexicographic, last coordinate fastest: value of k at index sum_i (k_i+n) L^(d-1-i).
+ *     (Algorithm 1's input "f(k), k in I" must cover k-h+e_l, hence the box, R1.)
+ *   - U, V: N x m row-major (leading dimension m); z: m x d row-major; sigma: m doubles.
+ *   - S: d x m x m row-major (S[l-1][i][j]); G: m x m row-major; b, c: m; t: m x d.
+ *
+ * Ownership and execution:
+ *   - Every pointer argument of prony_project / prony_vandermonde_ls is a DEVICE pointer
+ *     owned by the caller (e.g. a torch tensor); the library never allocates, frees or
+ *     retains memory. Scratch comes only from the caller's `workspace` (device, 256-byte
+ *     aligned, size >= prony_workspace_size(...)). No global mutable state: calls are
+ *     reentrant and CUDA-graph capturable.
+ *   - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t; 0 = legacy
+ *     default stream). Argument validation is synchronous, BEFORE any launch.
+ *   - `dev_status` (device int32, caller-owned, nullable) receives numerical failures
+ *     found on the device (first error wins); the caller must zero it beforehand and read
+ *     it after synchronizing. The return value covers validation and launch errors only.
+ *
+ * Error behaviour (return values):
+ *   PRONY_OK                 launched (or nothing to do for an empty range)
+ *   PRONY_ERR_INVALID        null / misaligned pointer, d,n,m out of range, bad unit_order
+ *   PRONY_ERR_RANGE          (2n+2)^d >= 2^31, m > PRONY_MAX_M, m > N, range outside [0, limit]
+ *   PRONY_ERR_SINGULAR       (dev_status) G not Hermitian positive definite in the Cholesky
+ *   PRONY_ERR_CUDA           a CUDA launch / copy failed (cudaGetLastError() is left set)
+ *   PRONY_ERR_UNIMPLEMENTED  prony_build_pencil (round 1)
+ *   PRONY_ERR_WORKSPACE      workspace_bytes smaller than prony_workspace_size(...)
+ *
+ * Implementation limits (this build): 1 <= d <= PRONY_MAX_D, 1 <= m <= PRONY_MAX_M,
+ * m <= N, (2n+2)^d < 2^31.
+ */
+#ifndef PRONY_H
+#define PRONY_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRONY_ABI_VERSION 1
+#define PRONY_MAX_D 8
+#define PRONY_MAX_M 128
+
+typedef struct prony_c128 {
+  double re;
+  double im;
+} prony_c128;
+
+/* cudaStream_t without including the CUDA headers */
+typedef struct CUstream_st* prony_stream_t;
+
+typedef enum prony_status {
+  PRONY_OK = 0,
+  PRONY_ERR_INVALID = 1,
+  PRONY_ERR_RANGE = 2,
+  PRONY_ERR_SINGULAR = 3,
+  PRONY_ERR_RANK = 4,
+  PRONY_ERR_NOT_CONVERGED = 5,
+  PRONY_ERR_CUDA = 6,
+  PRONY_ERR_UNIMPLEMENTED = 7,
+  PRONY_ERR_WORKSPACE = 8
+} prony_status;
+
+/* which workspace (prony_workspace_size) */
+typedef enum prony_workspace_kind {
+  PRONY_WS_PROJECT = 0,      /* prony_project, any unit range */
+  PRONY_WS_LS = 1,           /* prony_vandermonde_ls, any column range */
+  PRONY_WS_PENCIL_HOST = 2,  /* prony_pencil_host: device copies of inputs/outputs + both above */
+  PRONY_WS_BUILD = 3         /* prony_build_pencil (round 1: 0) */
+} prony_workspace_kind;
+
+/* unit orders of prony_project: units u in [0, d*N) */
+typedef enum prony_unit_order {
+  PRONY_UNITS_L_MAJOR = 0,   /* u = (l-1)*N + k  (l-sharding when ranks divide d) */
+  PRONY_UNITS_ROW_MAJOR = 1  /* u = k*d + (l-1)  (row-block sharding, all l per rank) */
+} prony_unit_order;
+
+/*
+ * Optional per-call execution record (the *_ex entry points). Nothing is retained after the
+ * call returns. The events, when non-null, are cudaEvent_t created by the caller; they are
+ * recorded on `stream` immediately before / after the call's dominant kernel (k_project for
+ * prony_project_ex, k_vls for prony_vandermonde_ls_ex), so the caller can time that kernel.
+ */
+typedef struct prony_exec_info {
+  void* ev_main_begin;    /* in, nullable: cudaEvent_t */
+  void* ev_main_end;      /* in, nullable: cudaEvent_t */
+  int32_t launches;       /* out: kernels launched by the call */
+  int32_t main_grid[3];   /* out: grid of the dominant kernel */
+  int32_t main_block;     /* out: threads per CTA of the dominant kernel */
+  int32_t split_k;        /* out: column chunks of T_l (prony_project) / column blocks (LS) */
+  double main_flops;      /* out: algorithmic FP64 flops of the dominant kernel (8 real flops per
+                             complex multiply-add): 8 m N * rows for k_project, 8 m^2 W for k_vls */
+} prony_exec_info;
+
+/* ABI version (== PRONY_ABI_VERSION of the built library). */
+int prony_abi_version(void);
+
+/* Static description of a status code; never NULL. */
+const char* prony_status_string(int status);
+
+/* Number of SMs / compute capability of the current device, for diagnostics.
+   Returns PRONY_ERR_CUDA if no device is usable. */
+int prony_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/*
+ * Workspace bytes for `kind` at (d, n, m) on the current device; an upper bound valid for
+ * every unit / column range. Writes *bytes. Validates (d, n, m) as the calls do.
+ */
+int prony_workspace_size(int kind, int d, int n, int m, size_t* bytes);
+
+/*
+ * prony_project — the pencil S_l = U* T_l V Sigma^-1, partial over a unit range.
+ *
+ *   grid        device, L^d prony_c128: samples on the box {-n..n+1}^d (see layout above).
+ *   U, V        device, N x m prony_c128 row-major: left / right singular vectors of T
+ *               (eq_T_svd); any N x m inputs are accepted (the pencil is linear in
+ *               them); identical inputs give bit-identical outputs (fixed-order reductions).
+ *   sigma       device, m doubles > 0: Sigma^-1 is applied as the column scale 1/sigma_j (R11).
+ *   unit_begin, unit_end, unit_order
+ *               the call contributes the rows k of T_l for the units u in [unit_begin,
+ *               unit_end) of [0, d*N) (order: prony_unit_order). [0, d*N) gives the complete
+ *               S_1..S_d; a partition of [0, d*N) over ranks gives partial pencils whose SUM
+ *               is S (Sigma^-1 already applied), i.e. one all-reduce completes the pencil.
+ *   S           device, d x m x m prony_c128, OVERWRITTEN with this call's partial sum
+ *               (rows of S_l with no unit in range are zero).
+ *   workspace   device scratch of workspace_bytes >= prony_workspace_size(PRONY_WS_PROJECT).
+ *   dev_status  nullable device int32 (no device-side failure modes in this call).
+ *   stream      CUDA stream for all launches.
+ */
+int prony_project(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
+                  const double* sigma, int64_t unit_begin, int64_t unit_end, int unit_order, prony_c128* S,
+                  void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream);
+
+/* prony_project + execution record (info nullable; same semantics otherwise). */
+int prony_project_ex(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
+                     const double* sigma, int64_t unit_begin, int64_t unit_end, int unit_order, prony_c128* S,
+                     void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream,
+                     prony_exec_info* info);
+
+/*
+ * prony_vandermonde_ls — A = [z_j^k], G = A conj(A)^T and b = A conj(f) (P:59,
+ * DESIGN.md R10) over the columns k in [col_begin, col_end) of I_n.
+ *
+ *   z           device, m x d prony_c128 nodes (computed z~ need not have unit modulus);
+ *               powers z^a are formed by repeated multiplication (R9).
+ *   grid        device, the same sample box as prony_project; f(k) is read at k in I_n.
+ *   A           nullable device m x (col_end-col_begin) prony_c128 row-major: if non-null the
+ *               Vandermonde block of the range is written (A[j][k-col_begin]).
+ *   G, b        device m x m / m prony_c128, OVERWRITTEN with the range's partial sums.
+ *   c, t        nullable device m prony_c128 / m x d doubles: written only when the range is
+ *               the full [0, N): c = conj(G^-1 b) via Cholesky (G conj(c) = b, R10) and
+ *               t = (-arg z / 2 pi) mod 1 (R4). If G is not HPD, *dev_status =
+ *               PRONY_ERR_SINGULAR and c is left NaN.
+ *   workspace   >= prony_workspace_size(PRONY_WS_LS).
+ */
+int prony_vandermonde_ls(int d, int n, int m, const prony_c128* z, const prony_c128* grid, int64_t col_begin,
+                         int64_t col_end, prony_c128* A, prony_c128* G, prony_c128* b, prony_c128* c, double* t,
+                         void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream);
+
+/* prony_vandermonde_ls + execution record (info nullable; same semantics otherwise). */
+int prony_vandermonde_ls_ex(int d, int n, int m, const prony_c128* z, const prony_c128* grid, int64_t col_begin,
+                            int64_t col_end, prony_c128* A, prony_c128* G, prony_c128* b, prony_c128* c, double* t,
+                            void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream,
+                            prony_exec_info* info);
+
+/*
+ * prony_ls_solve — c = conj(G^-1 b) by Cholesky (G conj(c) = b, R10) and, if t is
+ * non-null, t = (-arg z / 2 pi) mod 1 (R4), for G, b already summed over all
+ * columns (e.g. after the all-reduce of per-rank prony_vandermonde_ls partials).
+ *   G, b, z     device m x m, m, m x d prony_c128;  c device m prony_c128;  t nullable m x d doubles.
+ *   workspace   >= prony_workspace_size(PRONY_WS_LS).
+ *   dev_status  PRONY_ERR_SINGULAR if G is not Hermitian positive definite (c is then NaN).
+ */
+int prony_ls_solve(int d, int m, const prony_c128* G, const prony_c128* b, const prony_c128* z, prony_c128* c,
+                   double* t, void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream);
+
+/*
+ * prony_pencil_host — one full pencil (prony_project over [0, dN) + prony_vandermonde_ls over
+ * [0, N)) from HOST inputs to HOST outputs: copies grid, U, V, sigma, z host->device, runs the
+ * device path on `stream`, copies S, G, b, c, t device->host and synchronizes `stream`.
+ * Host buffers should be page-locked for full PCIe bandwidth (not required).
+ *   host inputs : grid (L^d), U, V (N x m), sigma (m), z (m x d)
+ *   host outputs: S (d x m x m), G (m x m), b (m), c (m), t (m x d); any output may be NULL
+ *   workspace   : DEVICE scratch >= prony_workspace_size(PRONY_WS_PENCIL_HOST)
+ *   *status_out : (nullable host int32) the device status word after the call
+ * Returns PRONY_OK, a validation error, or PRONY_ERR_CUDA.
+ */
+int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
+                      const double* sigma, const prony_c128* z, prony_c128* S, prony_c128* G, prony_c128* b,
+                      prony_c128* c, double* t, void* workspace, size_t workspace_bytes, int32_t* status_out,
+                      prony_stream_t stream);
+
+/*
+ * prony_build_pencil — reduced rank-m SVD of T on the device (block power method, Alg. 3,
+ * P:179-201, reusing the implicit Toeplitz apply) followed by prony_project.
+ * Round 1: returns PRONY_ERR_UNIMPLEMENTED after validating its arguments.
+ */
+int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t seed, prony_c128* S, prony_c128* U,
+                       prony_c128* V, double* sigma, int32_t* rank_out, void* workspace, size_t workspace_bytes,
+                       int32_t* dev_status, prony_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PRONY_H */

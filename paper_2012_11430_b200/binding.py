@@ -1,0 +1,258 @@
+"""Thin ctypes binding of libprony.so (include/prony.h). Argument marshalling only:
+every step of the hot path runs in the library's CUDA kernels. Tensors are torch tensors
+on a CUDA device (torch supplies device memory and the current stream); there is no CPU
+fallback — without the built library or a CUDA device every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libprony.so")
+
+PRONY_OK = 0
+PRONY_ERR_INVALID = 1
+PRONY_ERR_RANGE = 2
+PRONY_ERR_SINGULAR = 3
+PRONY_ERR_RANK = 4
+PRONY_ERR_NOT_CONVERGED = 5
+PRONY_ERR_CUDA = 6
+PRONY_ERR_UNIMPLEMENTED = 7
+PRONY_ERR_WORKSPACE = 8
+
+WS_PROJECT, WS_LS, WS_PENCIL_HOST, WS_BUILD = 0, 1, 2, 3
+UNITS_L_MAJOR, UNITS_ROW_MAJOR = 0, 1
+MAX_D, MAX_M = 8, 128
+
+# every symbol include/prony.h declares (checked by tests/test_abi.py)
+EXPORTS = ("prony_abi_version", "prony_status_string", "prony_device_info", "prony_workspace_size",
+           "prony_project", "prony_project_ex", "prony_vandermonde_ls", "prony_vandermonde_ls_ex", "prony_ls_solve",
+           "prony_pencil_host", "prony_build_pencil")
+
+
+class ExecInfo(ctypes.Structure):
+    """prony_exec_info (include/prony.h): events around the dominant kernel + launch record."""
+    _fields_ = [("ev_main_begin", ctypes.c_void_p), ("ev_main_end", ctypes.c_void_p), ("launches", ctypes.c_int32),
+                ("main_grid", ctypes.c_int32 * 3), ("main_block", ctypes.c_int32), ("split_k", ctypes.c_int32),
+                ("main_flops", ctypes.c_double)]
+
+
+def make_exec_info(ev_begin=None, ev_end=None) -> ExecInfo:
+    """ev_*: torch.cuda.Event(enable_timing=True) already created (recorded once)."""
+    info = ExecInfo()
+    info.ev_main_begin = ev_begin.cuda_event if ev_begin is not None else None
+    info.ev_main_end = ev_end.cuda_event if ev_end is not None else None
+    return info
+
+
+class PronyError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        self.code = code
+        super().__init__(f"{what}: {status_string(code)} (status {code})")
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libprony.so (built in-tree by __graft_entry__.build()). Raises if missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
+        L.prony_abi_version.restype = i32
+        L.prony_status_string.restype = ctypes.c_char_p
+        L.prony_status_string.argtypes = [i32]
+        L.prony_device_info.argtypes = [vp, vp, vp]
+        L.prony_workspace_size.argtypes = [i32, i32, i32, i32, ctypes.POINTER(sz)]
+        L.prony_project.argtypes = [i32, i32, i32, vp, vp, vp, vp, i64, i64, i32, vp, vp, sz, vp, vp]
+        L.prony_vandermonde_ls.argtypes = [i32, i32, i32, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp, sz, vp, vp]
+        L.prony_project_ex.argtypes = L.prony_project.argtypes + [vp]
+        L.prony_vandermonde_ls_ex.argtypes = L.prony_vandermonde_ls.argtypes + [vp]
+        L.prony_ls_solve.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, sz, vp, vp]
+        L.prony_pencil_host.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp]
+        L.prony_build_pencil.argtypes = [i32, i32, i32, vp, ctypes.c_uint64, vp, vp, vp, vp, vp, vp, sz, vp, vp]
+        for f in ("prony_device_info", "prony_workspace_size", "prony_project", "prony_vandermonde_ls", "prony_ls_solve",
+                  "prony_project_ex", "prony_vandermonde_ls_ex",
+                  "prony_pencil_host", "prony_build_pencil"):
+            getattr(L, f).restype = i32
+        _lib = L
+    return _lib
+
+
+def status_string(code: int) -> str:
+    return lib().prony_status_string(int(code)).decode()
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != PRONY_OK:
+        raise PronyError(rc, what)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev_tensor(t, dtype, name):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA torch tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def device_info():
+    sms, a, b = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _check(lib().prony_device_info(ctypes.byref(sms), ctypes.byref(a), ctypes.byref(b)), "prony_device_info")
+    return sms.value, (a.value, b.value)
+
+
+def workspace_size(kind: int, d: int, n: int, m: int) -> int:
+    out = ctypes.c_size_t()
+    _check(lib().prony_workspace_size(kind, d, n, m, ctypes.byref(out)), "prony_workspace_size")
+    return out.value
+
+
+def alloc_workspace(kind: int, d: int, n: int, m: int, device=None) -> torch.Tensor:
+    nbytes = workspace_size(kind, d, n, m)
+    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device or "cuda")
+
+
+def project(grid, U, V, sigma, d: int, n: int, m: int, unit_begin: int = 0, unit_end: int | None = None,
+            unit_order: int = UNITS_L_MAJOR, out=None, workspace=None, dev_status=None, stream=None, info=None):
+    """S_l = U* T_l V Sigma^-1 over units [unit_begin, unit_end) -> (d, m, m) complex128."""
+    N = (n + 1) ** d
+    _dev_tensor(grid, torch.complex128, "grid")
+    _dev_tensor(U, torch.complex128, "U")
+    _dev_tensor(V, torch.complex128, "V")
+    _dev_tensor(sigma, torch.float64, "sigma")
+    if unit_end is None:
+        unit_end = d * N
+    if out is None:
+        out = torch.empty((d, m, m), dtype=torch.complex128, device=grid.device)
+    _dev_tensor(out, torch.complex128, "out")
+    if workspace is None:
+        workspace = alloc_workspace(WS_PROJECT, d, n, m, grid.device)
+    rc = lib().prony_project_ex(d, n, m, _ptr(grid), _ptr(U), _ptr(V), _ptr(sigma), int(unit_begin),
+                                int(unit_end), int(unit_order), _ptr(out), _ptr(workspace), workspace.numel(),
+                                _ptr(dev_status), _stream(stream), None if info is None else ctypes.byref(info))
+    _check(rc, "prony_project")
+    return out
+
+
+def vandermonde_ls(z, grid, d: int, n: int, m: int, col_begin: int = 0, col_end: int | None = None,
+                   want_A: bool = False, want_solution: bool = True, out=None, workspace=None, dev_status=None,
+                   stream=None, info=None):
+    """A = [z_j^k], G = A conj(A)^T, b = A conj(f) (+ c, t over the full range) -> dict of tensors."""
+    N = (n + 1) ** d
+    _dev_tensor(z, torch.complex128, "z")
+    _dev_tensor(grid, torch.complex128, "grid")
+    if col_end is None:
+        col_end = N
+    dev = grid.device
+    if out is None:
+        out = {}
+    G = out.get("G")
+    if G is None:
+        G = torch.empty((m, m), dtype=torch.complex128, device=dev)
+    b = out.get("b")
+    if b is None:
+        b = torch.empty(m, dtype=torch.complex128, device=dev)
+    A = out.get("A")
+    if want_A and A is None:
+        A = torch.empty((m, col_end - col_begin), dtype=torch.complex128, device=dev)
+    full = col_begin == 0 and col_end == N
+    c = t = None
+    if full and want_solution:
+        c = out.get("c")
+        if c is None:
+            c = torch.empty(m, dtype=torch.complex128, device=dev)
+        t = out.get("t")
+        if t is None:
+            t = torch.empty((m, d), dtype=torch.float64, device=dev)
+    if workspace is None:
+        workspace = alloc_workspace(WS_LS, d, n, m, dev)
+    rc = lib().prony_vandermonde_ls_ex(d, n, m, _ptr(z), _ptr(grid), int(col_begin), int(col_end),
+                                       _ptr(A if want_A else None), _ptr(G), _ptr(b), _ptr(c), _ptr(t),
+                                       _ptr(workspace), workspace.numel(), _ptr(dev_status), _stream(stream),
+                                       None if info is None else ctypes.byref(info))
+    _check(rc, "prony_vandermonde_ls")
+    res = {"G": G, "b": b}
+    if want_A:
+        res["A"] = A
+    if c is not None:
+        res["c"] = c
+        res["t"] = t
+    return res
+
+
+def ls_solve(G, b, z, d: int, m: int, want_t: bool = True, workspace=None, dev_status=None, stream=None):
+    """c = conj(G^-1 b) (Cholesky) and t = (-arg z/2pi) mod 1 for already-reduced G, b."""
+    _dev_tensor(G, torch.complex128, "G")
+    _dev_tensor(b, torch.complex128, "b")
+    _dev_tensor(z, torch.complex128, "z")
+    dev = G.device
+    c = torch.empty(m, dtype=torch.complex128, device=dev)
+    t = torch.empty((m, d), dtype=torch.float64, device=dev) if want_t else None
+    if workspace is None:
+        workspace = torch.empty(m * m * 16 + m * 16 + 512, dtype=torch.uint8, device=dev)
+    rc = lib().prony_ls_solve(d, m, _ptr(G), _ptr(b), _ptr(z), _ptr(c), _ptr(t), _ptr(workspace), workspace.numel(),
+                              _ptr(dev_status), _stream(stream))
+    _check(rc, "prony_ls_solve")
+    return c, t
+
+
+def pencil_host(grid, U, V, sigma, z, d: int, n: int, m: int, workspace=None, outputs=None, stream=None):
+    """Full pencil from HOST (numpy or pinned CPU torch) buffers: H2D copies, prony_project over
+    [0, dN), prony_vandermonde_ls over [0, N), D2H copies, stream sync. Returns dict of host arrays."""
+    import numpy as np
+
+    def host_ptr(a):
+        if isinstance(a, torch.Tensor):
+            assert not a.is_cuda and a.is_contiguous()
+            return ctypes.c_void_p(a.data_ptr())
+        return a.ctypes.data_as(ctypes.c_void_p)
+
+    if outputs is None:
+        outputs = {
+            "S": np.empty((d, m, m), np.complex128), "G": np.empty((m, m), np.complex128),
+            "b": np.empty(m, np.complex128), "c": np.empty(m, np.complex128), "t": np.empty((m, d), np.float64),
+        }
+    if workspace is None:
+        workspace = alloc_workspace(WS_PENCIL_HOST, d, n, m)
+    st = ctypes.c_int32(0)
+    rc = lib().prony_pencil_host(d, n, m, host_ptr(grid), host_ptr(U), host_ptr(V), host_ptr(sigma), host_ptr(z),
+                                 host_ptr(outputs["S"]), host_ptr(outputs["G"]), host_ptr(outputs["b"]),
+                                 host_ptr(outputs["c"]), host_ptr(outputs["t"]), _ptr(workspace), workspace.numel(),
+                                 ctypes.byref(st), _stream(stream))
+    _check(rc, "prony_pencil_host")
+    outputs["status"] = st.value
+    return outputs
+
+
+def build_pencil(grid, d: int, n: int, m: int, seed: int = 0):
+    """Device SVD + projection (NEXT-1): not in this round; raises PronyError(UNIMPLEMENTED)."""
+    N = (n + 1) ** d
+    dev = grid.device
+    S = torch.empty((d, m, m), dtype=torch.complex128, device=dev)
+    U = torch.empty((N, m), dtype=torch.complex128, device=dev)
+    V = torch.empty((N, m), dtype=torch.complex128, device=dev)
+    s = torch.empty(m, dtype=torch.float64, device=dev)
+    r = torch.empty(1, dtype=torch.int32, device=dev)
+    rc = lib().prony_build_pencil(d, n, m, _ptr(grid), int(seed), _ptr(S), _ptr(U), _ptr(V), _ptr(s), _ptr(r),
+                                  None, 0, None, _stream(None))
+    _check(rc, "prony_build_pencil")
+    return S, U, V, s, r

@@ -1,0 +1,275 @@
+// api.cu — the C ABI of libprony (include/prony.h): synchronous validation, workspace
+// planning, and stream-ordered launches of the kernels in project.cu / vandermonde_ls.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/prony.h"
+#include "common.cuh"
+#include "project.cuh"
+#include "vandermonde_ls.cuh"
+
+using namespace prony;
+
+namespace {
+
+int sm_count_current() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return sms;
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// d, n, m validation shared by every entry point. On success writes N and the box size.
+int validate_dnm(int d, int n, int m, int64_t* N_out) {
+  if (d < 1 || d > PRONY_MAX_D || n < 1 || m < 1) return PRONY_ERR_INVALID;
+  if (m > PRONY_MAX_M) return PRONY_ERR_RANGE;
+  int64_t N = 1, box = 1;
+  for (int i = 0; i < d; ++i) {
+    N *= (n + 1);
+    box *= (2 * (int64_t)n + 2);
+    if (box >= (int64_t(1) << 31)) return PRONY_ERR_RANGE;
+  }
+  if (m > N) return PRONY_ERR_RANGE;
+  if (N * (int64_t)m >= (int64_t(1) << 40)) return PRONY_ERR_RANGE;
+  *N_out = N;
+  return PRONY_OK;
+}
+
+// rows of T_l covered by units [u0, u1) in the given order
+void unit_rows(int d, int64_t N, int64_t u0, int64_t u1, int order, ProjGeom* g) {
+  for (int l = 0; l < d; ++l) {
+    int64_t kb, ke;
+    if (order == PRONY_UNITS_L_MAJOR) {
+      kb = std::min(std::max(u0 - l * N, (int64_t)0), N);
+      ke = std::min(std::max(u1 - l * N, (int64_t)0), N);
+    } else {  // u = k*d + l  ->  k in [ceil((u0-l)/d), ceil((u1-l)/d))
+      auto cdiv = [](int64_t a, int64_t b) { return a >= 0 ? (a + b - 1) / b : -((-a) / b); };
+      kb = std::min(std::max(cdiv(u0 - l, d), (int64_t)0), N);
+      ke = std::min(std::max(cdiv(u1 - l, d), (int64_t)0), N);
+    }
+    g->kb[l] = (int)kb;
+    g->rows[l] = (int)std::max<int64_t>(ke - kb, 0);
+  }
+}
+
+size_t ws_project(int d, int64_t N, int m, int sms) { return project_workspace_bytes(d, (int)N, m, sms); }
+size_t ws_ls(int d, int n, int m, int sms) { return ls_workspace_bytes(d, n, m, sms); }
+
+// device copies used by prony_pencil_host, carved from the front of its workspace
+struct HostLayout {
+  size_t grid, U, V, sigma, z, S, G, b, c, t, status, inner, total;
+};
+
+HostLayout host_layout(int d, int n, int m, int64_t N, int sms) {
+  HostLayout h{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align_up(bytes, 256);
+    return o;
+  };
+  int64_t box = 1;
+  for (int i = 0; i < d; ++i) box *= (2 * (int64_t)n + 2);
+  h.grid = take(box * sizeof(double2));
+  h.U = take(N * m * sizeof(double2));
+  h.V = take(N * m * sizeof(double2));
+  h.sigma = take(m * sizeof(double));
+  h.z = take((size_t)m * d * sizeof(double2));
+  h.S = take((size_t)d * m * m * sizeof(double2));
+  h.G = take((size_t)m * m * sizeof(double2));
+  h.b = take(m * sizeof(double2));
+  h.c = take(m * sizeof(double2));
+  h.t = take((size_t)m * d * sizeof(double));
+  h.status = take(sizeof(int32_t));
+  h.inner = off;
+  off += std::max(ws_project(d, N, m, sms), ws_ls(d, n, m, sms));
+  h.total = off;
+  return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+int prony_abi_version(void) { return PRONY_ABI_VERSION; }
+
+const char* prony_status_string(int status) {
+  switch (status) {
+    case PRONY_OK: return "ok";
+    case PRONY_ERR_INVALID: return "invalid argument (null/misaligned pointer, d/n/m out of range, bad order)";
+    case PRONY_ERR_RANGE: return "size out of range ((2n+2)^d >= 2^31, m > max, m > N, range outside limits)";
+    case PRONY_ERR_SINGULAR: return "numerically singular (G not Hermitian positive definite)";
+    case PRONY_ERR_RANK: return "detected rank below m";
+    case PRONY_ERR_NOT_CONVERGED: return "iteration did not converge";
+    case PRONY_ERR_CUDA: return "CUDA error";
+    case PRONY_ERR_UNIMPLEMENTED: return "not implemented in this build";
+    case PRONY_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+int prony_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return PRONY_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return PRONY_ERR_CUDA;
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  return PRONY_OK;
+}
+
+int prony_workspace_size(int kind, int d, int n, int m, size_t* bytes) {
+  if (!bytes) return PRONY_ERR_INVALID;
+  int64_t N = 0;
+  int rc = validate_dnm(d, n, m, &N);
+  if (rc) return rc;
+  const int sms = sm_count_current();
+  if (sms <= 0) return PRONY_ERR_CUDA;
+  switch (kind) {
+    case PRONY_WS_PROJECT: *bytes = ws_project(d, N, m, sms); return PRONY_OK;
+    case PRONY_WS_LS: *bytes = ws_ls(d, n, m, sms); return PRONY_OK;
+    case PRONY_WS_PENCIL_HOST: *bytes = host_layout(d, n, m, N, sms).total; return PRONY_OK;
+    case PRONY_WS_BUILD: *bytes = 0; return PRONY_OK;
+    default: return PRONY_ERR_INVALID;
+  }
+}
+
+int prony_project(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
+                  const double* sigma, int64_t unit_begin, int64_t unit_end, int unit_order, prony_c128* S,
+                  void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream) {
+  return prony_project_ex(d, n, m, grid, U, V, sigma, unit_begin, unit_end, unit_order, S, workspace,
+                          workspace_bytes, dev_status, stream, nullptr);
+}
+
+int prony_project_ex(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
+                     const double* sigma, int64_t unit_begin, int64_t unit_end, int unit_order, prony_c128* S,
+                     void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream,
+                     prony_exec_info* info) {
+  (void)dev_status;
+  int64_t N = 0;
+  int rc = validate_dnm(d, n, m, &N);
+  if (rc) return rc;
+  if (!grid || !U || !V || !sigma || !S || !workspace) return PRONY_ERR_INVALID;
+  if (!aligned16(grid) || !aligned16(U) || !aligned16(V) || !aligned16(S) || ((uintptr_t)sigma & 7u) ||
+      ((uintptr_t)workspace & 255u))
+    return PRONY_ERR_INVALID;
+  if (unit_order != PRONY_UNITS_L_MAJOR && unit_order != PRONY_UNITS_ROW_MAJOR) return PRONY_ERR_INVALID;
+  if (unit_begin < 0 || unit_end < unit_begin || unit_end > (int64_t)d * N) return PRONY_ERR_RANGE;
+  const int sms = sm_count_current();
+  if (sms <= 0) return PRONY_ERR_CUDA;
+  if (workspace_bytes < ws_project(d, N, m, sms)) return PRONY_ERR_WORKSPACE;
+  ProjGeom g{};
+  g.d = d;
+  g.n = n;
+  g.m = m;
+  g.N = (int)N;
+  unit_rows(d, N, unit_begin, unit_end, unit_order, &g);
+  ProjPlan pl{};
+  project_plan(g, sms, &pl);
+  return project_launch(g, pl, (const double2*)grid, (const double2*)U, (const double2*)V, sigma, (double2*)S,
+                        workspace, (cudaStream_t)stream, info);
+}
+
+int prony_vandermonde_ls(int d, int n, int m, const prony_c128* z, const prony_c128* grid, int64_t col_begin,
+                         int64_t col_end, prony_c128* A, prony_c128* G, prony_c128* b, prony_c128* c, double* t,
+                         void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream) {
+  return prony_vandermonde_ls_ex(d, n, m, z, grid, col_begin, col_end, A, G, b, c, t, workspace, workspace_bytes,
+                                 dev_status, stream, nullptr);
+}
+
+int prony_vandermonde_ls_ex(int d, int n, int m, const prony_c128* z, const prony_c128* grid, int64_t col_begin,
+                            int64_t col_end, prony_c128* A, prony_c128* G, prony_c128* b, prony_c128* c, double* t,
+                            void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream,
+                            prony_exec_info* info) {
+  int64_t N = 0;
+  int rc = validate_dnm(d, n, m, &N);
+  if (rc) return rc;
+  if (!z || !grid || !G || !b || !workspace) return PRONY_ERR_INVALID;
+  if (!aligned16(z) || !aligned16(grid) || !aligned16(G) || !aligned16(b) || (A && !aligned16(A)) ||
+      (c && !aligned16(c)) || (t && ((uintptr_t)t & 7u)) || ((uintptr_t)workspace & 255u))
+    return PRONY_ERR_INVALID;
+  if (col_begin < 0 || col_end < col_begin || col_end > N) return PRONY_ERR_RANGE;
+  const int sms = sm_count_current();
+  if (sms <= 0) return PRONY_ERR_CUDA;
+  if (workspace_bytes < ws_ls(d, n, m, sms)) return PRONY_ERR_WORKSPACE;
+  return ls_launch(d, n, m, (int)N, (const double2*)z, (const double2*)grid, col_begin, col_end, (double2*)A,
+                   (double2*)G, (double2*)b, (double2*)c, t, workspace, dev_status, sms, (cudaStream_t)stream, info);
+}
+
+int prony_ls_solve(int d, int m, const prony_c128* G, const prony_c128* b, const prony_c128* z, prony_c128* c,
+                   double* t, void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream) {
+  if (d < 1 || d > PRONY_MAX_D || m < 1) return PRONY_ERR_INVALID;
+  if (m > PRONY_MAX_M) return PRONY_ERR_RANGE;
+  if (!G || !b || !z || !c || !workspace) return PRONY_ERR_INVALID;
+  if (!aligned16(G) || !aligned16(b) || !aligned16(z) || !aligned16(c) || (t && ((uintptr_t)t & 7u)) ||
+      ((uintptr_t)workspace & 255u))
+    return PRONY_ERR_INVALID;
+  if (workspace_bytes < (size_t)m * m * sizeof(double2) + 256 + (size_t)m * sizeof(double2)) return PRONY_ERR_WORKSPACE;
+  return ls_solve_launch(d, m, (const double2*)G, (const double2*)b, (const double2*)z, (double2*)c, t, workspace,
+                         dev_status, (cudaStream_t)stream);
+}
+
+int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
+                      const double* sigma, const prony_c128* z, prony_c128* S, prony_c128* G, prony_c128* b,
+                      prony_c128* c, double* t, void* workspace, size_t workspace_bytes, int32_t* status_out,
+                      prony_stream_t stream) {
+  int64_t N = 0;
+  int rc = validate_dnm(d, n, m, &N);
+  if (rc) return rc;
+  if (!grid || !U || !V || !sigma || !z || !workspace) return PRONY_ERR_INVALID;
+  if ((uintptr_t)workspace & 255u) return PRONY_ERR_INVALID;
+  const int sms = sm_count_current();
+  if (sms <= 0) return PRONY_ERR_CUDA;
+  const HostLayout h = host_layout(d, n, m, N, sms);
+  if (workspace_bytes < h.total) return PRONY_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)workspace;
+  int64_t box = 1;
+  for (int i = 0; i < d; ++i) box *= (2 * (int64_t)n + 2);
+  auto h2d = [&](size_t off, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(w + off, src, bytes, cudaMemcpyHostToDevice, st) == cudaSuccess;
+  };
+  auto d2h = [&](void* dst, size_t off, size_t bytes) {
+    return dst == nullptr || cudaMemcpyAsync(dst, w + off, bytes, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+  };
+  if (!h2d(h.grid, grid, box * sizeof(double2)) || !h2d(h.U, U, N * m * sizeof(double2)) ||
+      !h2d(h.V, V, N * m * sizeof(double2)) || !h2d(h.sigma, sigma, m * sizeof(double)) ||
+      !h2d(h.z, z, (size_t)m * d * sizeof(double2)))
+    return PRONY_ERR_CUDA;
+  if (cudaMemsetAsync(w + h.status, 0, sizeof(int32_t), st) != cudaSuccess) return PRONY_ERR_CUDA;
+  int32_t* dst = (int32_t*)(w + h.status);
+  rc = prony_project(d, n, m, (const prony_c128*)(w + h.grid), (const prony_c128*)(w + h.U),
+                     (const prony_c128*)(w + h.V), (const double*)(w + h.sigma), 0, (int64_t)d * N,
+                     PRONY_UNITS_L_MAJOR, (prony_c128*)(w + h.S), w + h.inner, h.total - h.inner, dst, stream);
+  if (rc) return rc;
+  rc = prony_vandermonde_ls(d, n, m, (const prony_c128*)(w + h.z), (const prony_c128*)(w + h.grid), 0, N, nullptr,
+                            (prony_c128*)(w + h.G), (prony_c128*)(w + h.b), (prony_c128*)(w + h.c),
+                            (double*)(w + h.t), w + h.inner, h.total - h.inner, dst, stream);
+  if (rc) return rc;
+  if (!d2h(S, h.S, (size_t)d * m * m * sizeof(double2)) || !d2h(G, h.G, (size_t)m * m * sizeof(double2)) ||
+      !d2h(b, h.b, m * sizeof(double2)) || !d2h(c, h.c, m * sizeof(double2)) ||
+      !d2h(t, h.t, (size_t)m * d * sizeof(double)) || !d2h(status_out, h.status, sizeof(int32_t)))
+    return PRONY_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return PRONY_ERR_CUDA;
+  return PRONY_OK;
+}
+
+int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t seed, prony_c128* S, prony_c128* U,
+                       prony_c128* V, double* sigma, int32_t* rank_out, void* workspace, size_t workspace_bytes,
+                       int32_t* dev_status, prony_stream_t stream) {
+  (void)seed; (void)workspace_bytes; (void)dev_status; (void)stream;
+  int64_t N = 0;
+  int rc = validate_dnm(d, n, m, &N);
+  if (rc) return rc;
+  if (!grid || !S || !U || !V || !sigma || !rank_out) return PRONY_ERR_INVALID;
+  (void)workspace;
+  return PRONY_ERR_UNIMPLEMENTED;
+}
+
+}  // extern "C"

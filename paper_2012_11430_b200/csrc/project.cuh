@@ -1,0 +1,56 @@
+// project.cuh — host/device interface of the projection kernels (project.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace prony {
+
+constexpr int kPtabPad = 4;   // P table padded so the last k-step may read P(h) for h < N+4
+constexpr int kMaxNP = 128;   // padded width of Y rows handled by k_reduce
+
+struct ProjShape {
+  int NT, WN, WM, BM, NP;
+};
+
+// rows of T_l covered by a call: for l = 1..d (index l-1), rows [kb, kb+rows) of I_n
+struct ProjGeom {
+  int d, n, m, N;
+  int kb[PRONY_MAX_D];
+  int rows[PRONY_MAX_D];
+};
+
+struct ProjPlan {
+  ProjShape shape;
+  int yoff[PRONY_MAX_D];
+  int R_tot, max_rows;
+  int chunk_w, KC;  // split-K: KC chunks of chunk_w columns of T_l
+  int RP;           // reduce partitions per l
+};
+
+struct ProjParams {
+  const double2* grid;
+  const double2* V;
+  const int32_t* ptab;
+  double2* Y;
+  int N, m, NP, chunk_w, R_tot;
+  int kb[PRONY_MAX_D], rows[PRONY_MAX_D], yoff[PRONY_MAX_D], shift[PRONY_MAX_D];
+};
+
+struct RedParams {
+  const double2* Y;
+  const double2* U;
+  double2* Spart;
+  int m, NP, KC, R_tot, RP;
+  int kb[PRONY_MAX_D], rows[PRONY_MAX_D], yoff[PRONY_MAX_D];
+};
+
+ProjShape proj_shape(int m);
+int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl);
+size_t project_workspace_bytes(int d, int N, int m, int sm_count);
+int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
+                   const double* sigma, double2* S, void* ws, cudaStream_t st, prony_exec_info* info);
+
+}  // namespace prony

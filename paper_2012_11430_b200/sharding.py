@@ -1,0 +1,58 @@
+"""Multi-GPU sharding of the pencil.
+
+S_l = sum_g U[R_g]^* T_l[R_g, :] V Sigma^-1 is linear in any partition of the rows k of T_l
+and of l, and G = sum_g A[:, K_g] A[:, K_g]^H, b likewise over the columns k. So each rank
+takes a contiguous, equal slice of the unit space [0, dN) (l-major or row-major order, see
+prony_unit_order) and of the columns [0, N), computes partial S (Sigma^-1 already applied),
+G and b with its own GPU, and ONE all_reduce(SUM) of the packed [S_1..S_d, G, b]
+((d+1) m^2 + m complex128, 470 KB at d=2, m=100) over NCCL completes the pencil on every
+rank; the m x m Cholesky solve for c then runs locally (prony_ls_solve).
+
+This module is host logic only (ranges, packing, the collective); the arithmetic is in the
+CUDA library. It is exercised on CPU with gloo (tests/test_sharding.py).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def split_range(total: int, parts: int, idx: int) -> tuple[int, int]:
+    """Contiguous near-equal split of [0, total) into `parts`; slice `idx`."""
+    return total * idx // parts, total * (idx + 1) // parts
+
+
+def unit_range(d: int, n: int, world: int, rank: int) -> tuple[int, int]:
+    N = (n + 1) ** d
+    return split_range(d * N, world, rank)
+
+
+def column_range(d: int, n: int, world: int, rank: int) -> tuple[int, int]:
+    N = (n + 1) ** d
+    return split_range(N, world, rank)
+
+
+def default_unit_order(d: int, world: int) -> int:
+    """l-major when the ranks divide d (pure l-sharding, e.g. cfg3 on 3 GPUs), else row-major
+    (every rank touches all l: V tiles and grid windows shared across l, balanced rows)."""
+    return 0 if world > 1 and d % world == 0 else 1
+
+
+def pack(S: torch.Tensor, G: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """[S_1..S_d, G, b] flattened into one complex128 buffer (one collective)."""
+    return torch.cat([S.reshape(-1), G.reshape(-1), b.reshape(-1)])
+
+
+def unpack(buf: torch.Tensor, d: int, m: int):
+    s = d * m * m
+    return buf[:s].view(d, m, m), buf[s:s + m * m].view(m, m), buf[s + m * m:s + m * m + m]
+
+
+def allreduce_pencil(S: torch.Tensor, G: torch.Tensor, b: torch.Tensor, group=None):
+    """Sum the per-rank partial pencils: one all_reduce(SUM) of the packed buffer.
+    complex128 is reduced as its float64 view (sum of complex = sum of re and im parts)."""
+    d, m, _ = S.shape
+    buf = pack(S, G, b)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(torch.view_as_real(buf), op=dist.ReduceOp.SUM, group=group)
+    return unpack(buf, d, m)

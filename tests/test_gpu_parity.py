@@ -1,0 +1,270 @@
+"""CUDA path (libprony.so through the C ABI) vs the CPU oracle, element by element.
+
+Tolerances (north_star / DESIGN.md §4): relative Frobenius <= 1e-10 on S_l, G and b (2-norm
+for b); |t - t_planted| <= 1e-8 on noise-free data. Observed errors are ~1e-15.
+"""
+import numpy as np
+import pytest
+import torch
+
+import workload as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2012_11430_b200 as pb
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return pb
+
+
+@pytest.fixture(scope="module")
+def orc():
+    import oracle
+    oracle.build()
+    return oracle
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else a
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def problem(d, n, m, seed, noise=0.0, random_uv=False):
+    cfg = W.custom_config(d, n, m, noise, seed)
+    prob = W.make_problem(cfg, with_svd=not random_uv)
+    if random_uv:
+        rng = np.random.default_rng(seed + 1)
+        N = cfg.N
+        prob.U = W.random_orthonormal(N, m, rng)
+        prob.V = W.random_orthonormal(N, m, rng)
+        prob.sigma = np.sort(rng.random(m) + 0.5)[::-1].copy()
+    return prob
+
+
+def run_project(pb, prob, **kw):
+    c = prob.cfg
+    return pb.project(dev(prob.grid), dev(prob.U), dev(prob.V), dev(prob.sigma), c.d, c.n, c.m, **kw)
+
+
+# ------------------------------------------------------------------ projection parity
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_project_configs_full_oracle(pb, orc, name):
+    prob = W.make_problem(name)
+    c = prob.cfg
+    S = run_project(pb, prob)
+    torch.cuda.synchronize()
+    S_or = orc.project(prob.grid, prob.U, prob.V, prob.sigma, c.d, c.n)
+    for l in range(c.d):
+        assert rel(S[l], S_or[l]) <= TOL
+
+
+@pytest.mark.parametrize("d,n,m,noise", [
+    (1, 40, 7, 1e-6),      # d = 1
+    (2, 6, 1, 0.0),        # m = 1
+    (2, 7, 9, 1e-3),       # ragged: N = 64, m = 9 (two n-tiles, pad 7)
+    (2, 13, 33, 1e-6),     # N = 196 (ragged row block), m = 33
+    (3, 4, 17, 0.0),       # d = 3, N = 125
+    (4, 3, 12, 1e-6),      # d = 4
+    (5, 2, 8, 0.0),        # d = 5, N = 243
+    (2, 11, 64, 0.0),      # m = 64 (WN = 1, NT = 8 -> WN = 2 path)
+    (2, 12, 100, 1e-6),    # m = 100 (WN = 2, NT = 7), N = 169
+    (2, 11, 128, 0.0),     # m = 128 = PRONY_MAX_M (NT = 8, WN = 2)
+])
+def test_project_edge_shapes(pb, orc, d, n, m, noise):
+    prob = problem(d, n, m, 1000 + d * 100 + n + m, noise, random_uv=True)
+    S = run_project(pb, prob)
+    torch.cuda.synchronize()
+    S_or = orc.project(prob.grid, prob.U, prob.V, prob.sigma, d, n)
+    for l in range(d):
+        assert rel(S[l], S_or[l]) <= TOL
+
+
+@pytest.mark.parametrize("order", [0, 1])
+def test_project_unit_ranges_partition(pb, orc, order):
+    """Partial pencils over unit sub-ranges match the oracle and sum to the full pencil."""
+    prob = problem(3, 6, 10, 77, 1e-6, random_uv=True)
+    c = prob.cfg
+    N = c.N
+    cuts = [0, 5, 343, 344, 700, 3 * N - 1, 3 * N]
+    acc = torch.zeros((c.d, c.m, c.m), dtype=torch.complex128, device="cuda")
+    for a, b in zip(cuts, cuts[1:]):
+        S = run_project(pb, prob, unit_begin=a, unit_end=b, unit_order=order)
+        torch.cuda.synchronize()
+        S_or = orc.project_units(prob.grid, prob.U, prob.V, prob.sigma, c.d, c.n, a, b, order)
+        for l in range(c.d):
+            if np.linalg.norm(S_or[l]) == 0:
+                assert float(S[l].abs().max()) == 0.0
+            else:
+                assert rel(S[l], S_or[l]) <= TOL
+        acc += S
+    full = orc.project(prob.grid, prob.U, prob.V, prob.sigma, c.d, c.n)
+    for l in range(c.d):
+        assert rel(acc[l], full[l]) <= TOL
+
+
+def test_project_empty_range_is_zero(pb):
+    prob = problem(2, 5, 4, 5, random_uv=True)
+    S = run_project(pb, prob, unit_begin=7, unit_end=7)
+    torch.cuda.synchronize()
+    assert float(S.abs().max()) == 0.0
+
+
+def test_project_deterministic(pb):
+    prob = W.make_problem("cfg2")
+    S1 = run_project(pb, prob)
+    S2 = run_project(pb, prob)
+    torch.cuda.synchronize()
+    assert torch.equal(S1, S2)
+
+
+def test_project_spectrum_recovers_nodes(pb):
+    """F2 on the GPU result: eig(S_l) = {z_j(l)} with the planted SVD (noise-free cfg3)."""
+    prob = W.make_problem("cfg3")
+    S = run_project(pb, prob).cpu().numpy()
+    for l in range(prob.cfg.d):
+        ev = np.linalg.eigvals(S[l])
+        for zj in prob.z[:, l]:
+            assert np.min(np.abs(ev - zj)) < 1e-10
+
+
+# ------------------------------------------------------------------ full-size configs
+def _closed_form_S(prob):
+    """F1 (noise-free, any U V sigma): S_l = (U* B) diag(c z_l) (B^H V) Sigma^-1."""
+    c = prob.cfg
+    k = W.index_set(c.d, c.n).astype(np.float64)
+    ph = k @ prob.t.T
+    B = np.exp(-2j * np.pi * (ph - np.floor(ph)))
+    UB = prob.U.conj().T @ B
+    BV = B.conj().T @ prob.V
+    return np.stack([(UB * (prob.c * prob.z[:, l])) @ BV / prob.sigma[None, :] for l in range(c.d)])
+
+
+def test_cfg5_full_size_closed_form(pb):
+    prob = W.make_problem("cfg5")
+    S = run_project(pb, prob)
+    torch.cuda.synchronize()
+    want = _closed_form_S(prob)
+    for l in range(prob.cfg.d):
+        assert rel(S[l], want[l]) <= TOL
+
+
+@pytest.mark.parametrize("name,cols", [("cfg4", [0, 57, 99]), ("cfg5", [3, 29])])
+def test_full_size_sampled_columns_oracle(pb, orc, name, cols):
+    """Full BASELINE sizes, the launch configuration bench.py times: sampled columns of S_l
+    computed one by one by the oracle (T_l v_j in full, then U^*)."""
+    prob = W.make_problem(name)
+    c = prob.cfg
+    S = run_project(pb, prob).cpu().numpy()
+    ells = [1, c.d] if c.d > 1 else [1]
+    for ell in ells:
+        want = orc.project_columns(prob.grid, prob.U, prob.V, prob.sigma, c.d, c.n, ell, cols)
+        assert rel(S[ell - 1][:, cols], want) <= TOL
+
+
+# ------------------------------------------------------------------ Vandermonde / LS parity
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5"])
+def test_vandermonde_ls_configs(pb, orc, name):
+    prob = W.make_problem(name, with_svd=False)
+    c = prob.cfg
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = pb.vandermonde_ls(dev(prob.z), dev(prob.grid), c.d, c.n, c.m, want_A=True, dev_status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    A_or = orc.vandermonde(prob.z, c.d, c.n)
+    G_or, b_or = orc.ls_products(A_or, prob.grid, c.d, c.n)
+    assert rel(out["A"], A_or) <= TOL
+    assert rel(out["G"], G_or) <= TOL
+    assert rel(out["b"], b_or) <= TOL
+    c_or = orc.cholesky_solve(G_or, b_or)
+    assert rel(out["c"], c_or) <= 1e-9
+    t = out["t"].cpu().numpy()
+    assert W.torus_dist_inf(t, prob.t).max() <= 1e-8
+    if c.noise == 0.0:
+        assert rel(out["c"], prob.c) <= 1e-9
+
+
+def test_vandermonde_ls_cfg4_full_size(pb, orc):
+    prob = W.make_problem("cfg4", with_svd=False)
+    c = prob.cfg
+    out = pb.vandermonde_ls(dev(prob.z), dev(prob.grid), c.d, c.n, c.m, want_A=True)
+    torch.cuda.synchronize()
+    A_or = orc.vandermonde(prob.z, c.d, c.n)
+    G_or, b_or = orc.ls_products(A_or, prob.grid, c.d, c.n)
+    assert rel(out["A"], A_or) <= TOL
+    assert rel(out["G"], G_or) <= TOL
+    assert rel(out["b"], b_or) <= TOL
+    assert W.torus_dist_inf(out["t"].cpu().numpy(), prob.t).max() <= 1e-8
+    assert rel(out["c"], prob.c) <= 1e-5          # noisy sigma = 1e-6 data: c error ~ eps
+
+
+@pytest.mark.parametrize("d,n,m", [(1, 30, 5), (2, 9, 1), (3, 5, 70), (4, 3, 9), (2, 11, 128)])
+def test_vandermonde_ls_edges_and_ranges(pb, orc, d, n, m):
+    rng = np.random.default_rng(d * 1000 + n * 10 + m)
+    z = W.node_vectors(rng.random((m, d))) * (1.0 + 0.01 * (rng.random((m, d)) - 0.5))   # non-unit nodes
+    grid = W.sample_grid(rng.random((3, d)), np.array([1.0, 0.5j, -2.0]), n, 1e-6, 3)
+    N = (n + 1) ** d
+    for a, e in [(0, N), (0, 1), (3, N - 2), (N // 2, N)]:
+        out = pb.vandermonde_ls(dev(z), dev(grid), d, n, m, a, e, want_A=True)
+        torch.cuda.synchronize()
+        A_or = orc.vandermonde(z, d, n, a, e)
+        G_or, b_or = orc.ls_products(A_or, grid, d, n, a, e)
+        assert rel(out["A"], A_or) <= TOL
+        assert rel(out["G"], G_or) <= TOL
+        assert rel(out["b"], b_or) <= TOL
+
+
+def test_ls_solve_singular_status(pb):
+    m, d = 3, 2
+    G = torch.tensor([[1, 2, 0], [2, 1, 0], [0, 0, 1]], dtype=torch.complex128, device="cuda")
+    b = torch.ones(m, dtype=torch.complex128, device="cuda")
+    z = torch.ones((m, d), dtype=torch.complex128, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    c, _ = pb.ls_solve(G, b, z, d, m, dev_status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == pb.PRONY_ERR_SINGULAR
+    assert torch.isnan(c.real).all()
+
+
+# ------------------------------------------------------------------ end to end from host buffers
+def test_pencil_host_matches_device_path(pb, orc):
+    prob = W.make_problem("cfg2")
+    c = prob.cfg
+    out = pb.pencil_host(prob.grid, prob.U, prob.V, prob.sigma, prob.z, c.d, c.n, c.m)
+    assert out["status"] == 0
+    S_or = orc.project(prob.grid, prob.U, prob.V, prob.sigma, c.d, c.n)
+    for l in range(c.d):
+        assert rel(out["S"][l], S_or[l]) <= TOL
+    A_or = orc.vandermonde(prob.z, c.d, c.n)
+    G_or, b_or = orc.ls_products(A_or, prob.grid, c.d, c.n)
+    assert rel(out["G"], G_or) <= TOL and rel(out["b"], b_or) <= TOL
+    assert W.torus_dist_inf(out["t"], prob.t).max() <= 1e-8
+
+
+def test_end_to_end_recovery_with_oracle_tail(pb, orc):
+    """Algorithm 1 with the GPU pencil: S from the device, then the oracle's eig / diagonalization
+    (NEXT-1 runs those on the device); t within 1e-8 of planted (noise-free cfg3)."""
+    prob = W.make_problem("cfg3")
+    S = run_project(pb, prob).cpu().numpy()
+    z, _, off = orc.diagonalize(S, orc.random_mu(prob.cfg.d, 1))
+    t = orc.t_from_z(z)
+    perm = orc.match_nodes(t, prob.t)
+    assert W.torus_dist_inf(t[perm], prob.t).max() <= 1e-8
+    out = pb.vandermonde_ls(dev(z), dev(prob.grid), prob.cfg.d, prob.cfg.n, prob.cfg.m)
+    assert rel(out["c"].cpu().numpy()[perm], prob.c) <= 1e-8
+
+
+def test_build_pencil_unimplemented(pb):
+    prob = problem(2, 4, 2, 3, random_uv=True)
+    with pytest.raises(pb.PronyError) as e:
+        pb.build_pencil(dev(prob.grid), 2, 4, 2)
+    assert e.value.code == pb.PRONY_ERR_UNIMPLEMENTED
