@@ -313,7 +313,7 @@ def run_ours(args, cfg):
             assert r["status"] == 0
             e_ms.append(e0.elapsed_time(e1))
         h2d = sum(x.numel() * x.element_size() for x in (hg, hU, hV, hs, hz))
-        d2h = sum(x.numel() * x.element_size() for x in outs.values()) + 4
+        d2h = sum(x.numel() * x.element_size() for x in outs.values() if isinstance(x, torch.Tensor)) + 4
         e2e = {"value": Ke / (sum(e_ms) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": sum(e_ms) / Ke, "api": "prony_pencil_host (pinned host buffers)"}
         del ws_h

@@ -10,12 +10,20 @@
 //   k_reduce    S_part[p] = U[rows_p]^* (sum_c Y_c[rows_p]) (fixed-order), then
 //   k_finalize  S_l = (sum_p S_part[p]) diag(1/sigma) (fixed order -> deterministic).
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "project.cuh"
 
 namespace prony {
+
+// complex product formulation of k_project: 3 (Gauss/3M, default) or 4 (4M); env PRONY_CMUL=4m
+static int cmul_mode() {
+  const char* e = getenv("PRONY_CMUL");
+  return (e && (e[0] == '4')) ? 4 : 3;
+}
 
 // ---------------------------------------------------------------------------- P table
 __global__ void k_ptab(int d, int n, int N, int32_t* __restrict__ ptab) {
@@ -36,17 +44,65 @@ __global__ void k_ptab(int d, int n, int N, int32_t* __restrict__ ptab) {
 }
 
 // ---------------------------------------------------------------------------- projection
-// CTA = 8 warps = WM (row) x WN (col) warps; warp tile 16 rows x (8*NT) columns of Y.
-// Lane (g = lane>>2, q = lane&3) owns rows g, g+8 of its warp tile for the A fragment and
-// column g of each n-tile for the B fragment; per k-step of 4 columns h of T_l it loads
-//   A: T_l[k_g][h0+q], T_l[k_{g+8}][h0+q]   = grid[P0 - P(h)], grid[P1 - P(h)]   (2 x LDG.128)
-//   B: V[h0+q][col0 + 8j], j < NT                                                 (NT x LDG.128)
-// one step ahead (register double buffer) and issues 4*NT DMMA m16n8k4.
+// CTA = 8 warps = WM (row) x WN (col) warps; CTA tile BM = 16*WM rows of T_l x NP = 8*NT*WN
+// columns of V; warp tile 16 rows x 8*NT columns. The K loop (columns h of T_l, rows of V) runs
+// in stages of BK = 16 through a kStages-deep cp.async ring in shared memory:
+//   A tile  As[kc][r] = T_l[k_r][h0+kc] = grid[P(k_r) + s_l + C0 - P(h0+kc)]   (implicit Toeplitz
+//           gather: one 16-byte cp.async per element straight from the L2/L1-resident grid)
+//   B tile  Bs[kc][c] = V[h0+kc][c]  (zero-filled for c >= m and h >= h_end)
+// Consumers read the DMMA fragments with conflict-free LDS.128 (row strides BM+2, NP+2 double2).
+// Lane (g = lane>>2, q = lane&3): A frag rows g, g+8 at column q; B frag row q, column g.
+// MODE 4: 4M  Re += Ar Br - Ai Bi, Im += Ar Bi + Ai Br              (4 DMMA m16n8k4 / n-tile)
+// MODE 3: 3M  P1 += Ar Br, P2 += Ai Bi, P3 += (Ar+Ai)(Br+Bi);
+//             Re = P1 - P2, Im = P3 - P1 - P2                       (3 DMMA m16n8k4 / n-tile)
+constexpr int kBK = 16;
+constexpr int kStages = 4;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async16_cg(void* smem_dst, const void* gsrc, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// non-volatile so ptxas may interleave independent MMAs
+__device__ __forceinline__ void mma16x8x4(double (&c)[4], double a0, double a1, double b) {
+  asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b));
+}
+
 template <int NT, int WN>
+struct ProjTile {
+  static constexpr int WM = 8 / WN;
+  static constexpr int BM = 16 * WM;
+  static constexpr int NP = 8 * NT * WN;
+  static constexpr int AS = BM + 2;
+  static constexpr int BS = NP + 2;
+  static constexpr int STAGE = kBK * (AS + BS);  // double2 per stage
+  static constexpr size_t SMEM = (size_t)kStages * STAGE * sizeof(double2);
+  static constexpr int GA = kBK * BM / 256;      // A elements gathered per thread per stage
+  static constexpr int KSTEP = 256 / BM;         // column stride between a thread's A elements
+  static constexpr int GB = (kBK * NP + 255) / 256;
+};
+
+template <int NT, int WN, int MODE>
 __global__ void __launch_bounds__(256, 1) k_project(ProjParams p) {
-  constexpr int WM = 8 / WN;
-  constexpr int BM = 16 * WM;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  using T = ProjTile<NT, WN>;
+  constexpr int WM = T::WM, BM = T::BM, NP = T::NP, AS = T::AS, BS = T::BS, GA = T::GA, KSTEP = T::KSTEP,
+                GB = T::GB;
+  constexpr int NACC = MODE == 3 ? 3 : 2;
+  extern __shared__ __align__(16) double2 smem[];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int wm = warp % WM, wn = warp / WM;
   const int g = lane >> 2, q = lane & 3;
   const int l = blockIdx.z;
@@ -56,71 +112,130 @@ __global__ void __launch_bounds__(256, 1) k_project(ProjParams p) {
   const int chunk = blockIdx.y;
   const int h_begin = chunk * p.chunk_w;
   const int h_end = min(h_begin + p.chunk_w, p.N);
-
-  const int r0 = rb0 + wm * 16 + g, r1 = r0 + 8;
-  const bool v0 = r0 < rows, v1 = r1 < rows;
+  const int KT = (h_end - h_begin + kBK - 1) / kBK;
   const int32_t* __restrict__ ptab = p.ptab;
-  const int P0 = ptab[p.kb[l] + (v0 ? r0 : 0)] + p.shift[l];
-  const int P1 = ptab[p.kb[l] + (v1 ? r1 : 0)] + p.shift[l];
-  const int colw = wn * NT * 8;
   const double2* __restrict__ grid = p.grid;
   const double2* __restrict__ V = p.V;
-  const int m = p.m;
-  const double2 zero = make_double2(0.0, 0.0);
+  const int m = p.m, N = p.N;
 
-  double acc_re[NT][4], acc_im[NT][4];
-#pragma unroll
-  for (int j = 0; j < NT; ++j)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) acc_re[j][e] = acc_im[j][e] = 0.0;
+  // gather role: row ra of the tile, columns kc0 + KSTEP*x
+  const int ra = tid % BM, kc0 = tid / BM;
+  const bool va = rb0 + ra < rows;
+  const int PA = va ? ptab[p.kb[l] + rb0 + ra] + p.shift[l] : 0;
 
-  double2 a0, a1, b[NT];
-  auto load = [&](int h0, double2& x0, double2& x1, double2 (&y)[NT]) {
-    const int h = h0 + q;
-    const bool vh = h < h_end;
-    const int Ph = ptab[h];  // padded table: h < N + kPtabPad always
-    x0 = (v0 && vh) ? ldg2(grid + (P0 - Ph)) : zero;
-    x1 = (v1 && vh) ? ldg2(grid + (P1 - Ph)) : zero;
-    const double2* vrow = V + (size_t)h * m;
+  auto load_ph = [&](int h0, int (&ph)[GA]) {
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const int col = colw + 8 * j + g;
-      y[j] = (vh && col < m) ? ldg2(vrow + col) : zero;
+    for (int x = 0; x < GA; ++x) {
+      const int h = h0 + kc0 + KSTEP * x;
+      ph[x] = h < N ? __ldg(ptab + h) : 0;
+    }
+  };
+  auto load_stage = [&](int slot, int h0, const int (&ph)[GA]) {
+    double2* As = smem + slot * T::STAGE;
+    double2* Bs = As + kBK * AS;
+#pragma unroll
+    for (int x = 0; x < GA; ++x) {
+      const int kc = kc0 + KSTEP * x;
+      const bool ok = va && (h0 + kc < h_end);
+      cp_async16(As + kc * AS + ra, grid + (ok ? PA - ph[x] : 0), ok ? 16 : 0);
+    }
+#pragma unroll
+    for (int y = 0; y < GB; ++y) {
+      const int e = tid + 256 * y;
+      if (e < kBK * NP) {
+        const int kr = e / NP, col = e % NP;
+        const int h = h0 + kr;
+        const bool ok = (h < h_end) && (col < m);
+        cp_async16_cg(Bs + kr * BS + col, V + (ok ? (size_t)h * m + col : 0), ok ? 16 : 0);
+      }
     }
   };
 
-  load(h_begin, a0, a1, b);
-  for (int h0 = h_begin; h0 < h_end; h0 += 4) {
-    double2 na0, na1, nb[NT];
-    if (h0 + 4 < h_end) {
-      load(h0 + 4, na0, na1, nb);
-    } else {
-      na0 = na1 = zero;
+  double acc[NACC][NT][4];
 #pragma unroll
-      for (int j = 0; j < NT; ++j) nb[j] = zero;
+  for (int a = 0; a < NACC; ++a)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[a][j][e] = 0.0;
+
+  int ph[GA];
+  load_ph(h_begin, ph);
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < KT) {
+      load_stage(s, h_begin + s * kBK, ph);
+      load_ph(h_begin + (s + 1) * kBK, ph);
     }
-#pragma unroll
-    for (int j = 0; j < NT; ++j) cmma16x8x4_4m(acc_re[j], acc_im[j], a0, a1, b[j]);
-    a0 = na0;
-    a1 = na1;
-#pragma unroll
-    for (int j = 0; j < NT; ++j) b[j] = nb[j];
+    cp_async_commit();
   }
 
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    const int nk = kt + kStages - 1;
+    if (nk < KT) {
+      load_stage(nk % kStages, h_begin + nk * kBK, ph);
+      load_ph(h_begin + (nk + 1) * kBK, ph);
+    }
+    cp_async_commit();
+
+    const double2* As = smem + (kt % kStages) * T::STAGE;
+    const double2* Bs = As + kBK * AS;
+#pragma unroll
+    for (int kk = 0; kk < kBK / 4; ++kk) {
+      const double2 a0 = As[(kk * 4 + q) * AS + wm * 16 + g];
+      const double2 a1 = As[(kk * 4 + q) * AS + wm * 16 + g + 8];
+      const double2* brow = Bs + (kk * 4 + q) * BS + wn * NT * 8 + g;
+      if constexpr (MODE == 3) {
+        const double s0 = a0.x + a0.y, s1 = a1.x + a1.y;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const double2 b = brow[8 * j];
+          mma16x8x4(acc[0][j], a0.x, a1.x, b.x);
+          mma16x8x4(acc[1][j], a0.y, a1.y, b.y);
+          mma16x8x4(acc[2][j], s0, s1, b.x + b.y);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const double2 b = brow[8 * j];
+          mma16x8x4(acc[0][j], a0.x, a1.x, b.x);
+          mma16x8x4(acc[1][j], a0.x, a1.x, b.y);
+          mma16x8x4(acc[0][j], -a0.y, -a1.y, b.y);
+          mma16x8x4(acc[1][j], a0.y, a1.y, b.x);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+
   // epilogue: Y[chunk][yoff_l + r][col], NP-wide rows (all NP columns written)
+  const int r0 = rb0 + wm * 16 + g, r1 = r0 + 8;
   const size_t ybase = (size_t)chunk * p.R_tot + p.yoff[l];
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
-    const int col = colw + 8 * j + 2 * q;
-    if (v0) {
-      double2* y = p.Y + (ybase + r0) * p.NP + col;
-      y[0] = make_double2(acc_re[j][0], acc_im[j][0]);
-      y[1] = make_double2(acc_re[j][1], acc_im[j][1]);
+    double re[4], im[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if constexpr (MODE == 3) {
+        re[e] = acc[0][j][e] - acc[1][j][e];
+        im[e] = acc[2][j][e] - acc[0][j][e] - acc[1][j][e];
+      } else {
+        re[e] = acc[0][j][e];
+        im[e] = acc[1][j][e];
+      }
     }
-    if (v1) {
-      double2* y = p.Y + (ybase + r1) * p.NP + col;
-      y[0] = make_double2(acc_re[j][2], acc_im[j][2]);
-      y[1] = make_double2(acc_re[j][3], acc_im[j][3]);
+    const int col = wn * NT * 8 + 8 * j + 2 * q;
+    if (r0 < rows) {
+      double2* y = p.Y + (ybase + r0) * NP + col;
+      y[0] = make_double2(re[0], im[0]);
+      y[1] = make_double2(re[1], im[1]);
+    }
+    if (r1 < rows) {
+      double2* y = p.Y + (ybase + r1) * NP + col;
+      y[0] = make_double2(re[2], im[2]);
+      y[1] = make_double2(re[3], im[3]);
     }
   }
 }
@@ -245,7 +360,7 @@ int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl) {
   pl->max_rows = max_rows;
   // split-K: chunk count KC minimizing ceil(waves)/KC (time per CTA ~ 1/KC), subject to
   // KC * R_tot <= 2 d N (workspace bound) and chunks of >= 64 columns.
-  const int64_t cap_rows = 2LL * g.d * g.N;
+  const int64_t cap_rows = (int64_t)kYCap * g.d * g.N;
   int kc_max = (int)std::min<int64_t>(64, std::max<int64_t>(1, cap_rows / std::max(R_tot, 1)));
   kc_max = std::max(1, std::min(kc_max, std::max(1, g.N / 64)));
   double best = 1e30;
@@ -253,7 +368,8 @@ int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl) {
   for (int kc = 1; kc <= kc_max; ++kc) {
     const double ctas = (double)row_blocks * kc;
     const double waves = std::ceil(ctas / sm_count);
-    const double cost = waves / kc * (1.0 + 0.002 * kc);  // small per-chunk overhead (Y traffic)
+    // time ~ waves x (chunk columns + pipeline fill/drain of ~4 stages)
+    const double cost = waves * ((double)g.N / kc + 4.0 * kBK);
     if (cost < best - 1e-12) {
       best = cost;
       best_kc = kc;
@@ -274,7 +390,7 @@ int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl) {
 size_t project_workspace_bytes(int d, int N, int m, int sm_count) {
   const ProjShape sh = proj_shape(m);
   size_t bytes = align_up((size_t)(N + kPtabPad) * sizeof(int32_t), 256);
-  bytes += align_up((size_t)2 * d * N * sh.NP * sizeof(double2), 256);  // Y partials (KC*R_tot <= 2dN)
+  bytes += align_up((size_t)kYCap * d * N * sh.NP * sizeof(double2), 256);  // Y partials (KC*R_tot <= kYCap*dN)
   const int ib = (m + 63) / 64;
   int RP = std::max(1, (2 * sm_count) / std::max(1, d * ib));
   bytes += align_up((size_t)d * RP * m * m * sizeof(double2), 256);
@@ -282,8 +398,20 @@ size_t project_workspace_bytes(int d, int N, int m, int sm_count) {
 }
 
 template <int NT, int WN>
-static void launch_project_t(const ProjParams& p, dim3 grid, cudaStream_t st) {
-  k_project<NT, WN><<<grid, 256, 0, st>>>(p);
+static int launch_project_t(const ProjParams& p, dim3 grid, cudaStream_t st, int mode) {
+  const size_t smem = ProjTile<NT, WN>::SMEM;
+  if (mode == 4) {
+    if (cudaFuncSetAttribute(k_project<NT, WN, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return PRONY_ERR_CUDA;
+    k_project<NT, WN, 4><<<grid, 256, smem, st>>>(p);
+  } else {
+    if (cudaFuncSetAttribute(k_project<NT, WN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return PRONY_ERR_CUDA;
+    k_project<NT, WN, 3><<<grid, 256, smem, st>>>(p);
+  }
+  return PRONY_OK;
 }
 
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
@@ -292,7 +420,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   int32_t* ptab = (int32_t*)w;
   w += align_up((size_t)(g.N + kPtabPad) * sizeof(int32_t), 256);
   double2* Y = (double2*)w;
-  w += align_up((size_t)2 * g.d * g.N * pl.shape.NP * sizeof(double2), 256);
+  w += align_up((size_t)kYCap * g.d * g.N * pl.shape.NP * sizeof(double2), 256);
   double2* Spart = (double2*)w;
 
   if (info) {
@@ -333,10 +461,12 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   dim3 grd((pl.max_rows + pl.shape.BM - 1) / pl.shape.BM, pl.KC, g.d);
   const int NT = pl.shape.NT, WN = pl.shape.WN;
   if (info && info->ev_main_begin) cudaEventRecord((cudaEvent_t)info->ev_main_begin, st);
+  const int mode = cmul_mode();
+  int lrc = PRONY_OK;
   switch (WN * 16 + NT) {
 #define PRONY_CASE(nt, wn) \
   case wn * 16 + nt:       \
-    launch_project_t<nt, wn>(p, grd, st); \
+    lrc = launch_project_t<nt, wn>(p, grd, st, mode); \
     break;
     PRONY_CASE(1, 1) PRONY_CASE(2, 1) PRONY_CASE(3, 1) PRONY_CASE(4, 1) PRONY_CASE(5, 1) PRONY_CASE(6, 1)
     PRONY_CASE(7, 1) PRONY_CASE(4, 2) PRONY_CASE(5, 2) PRONY_CASE(6, 2) PRONY_CASE(7, 2) PRONY_CASE(8, 2)
@@ -344,6 +474,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
     default:
       return PRONY_ERR_RANGE;
   }
+  if (lrc != PRONY_OK) return lrc;
   if (info && info->ev_main_end) cudaEventRecord((cudaEvent_t)info->ev_main_end, st);
 
   RedParams r{};

@@ -10,6 +10,7 @@ namespace prony {
 
 constexpr int kPtabPad = 4;   // P table padded so the last k-step may read P(h) for h < N+4
 constexpr int kMaxNP = 128;   // padded width of Y rows handled by k_reduce
+constexpr int kYCap = 4;      // split-K bound: KC * (rows in range) <= kYCap * d * N
 
 struct ProjShape {
   int NT, WN, WM, BM, NP;

@@ -112,6 +112,19 @@ def test_project_unit_ranges_partition(pb, orc, order):
         assert rel(acc[l], full[l]) <= TOL
 
 
+@pytest.mark.parametrize("mode", ["4m", "3m"])
+@pytest.mark.parametrize("d,n,m", [(2, 12, 100), (3, 5, 20)])
+def test_project_cmul_modes(pb, orc, mode, d, n, m, monkeypatch):
+    """Both complex-product formulations of k_project (3M default, 4M via PRONY_CMUL=4m)."""
+    monkeypatch.setenv("PRONY_CMUL", mode)
+    prob = problem(d, n, m, 4242, 1e-6, random_uv=True)
+    S = run_project(pb, prob)
+    torch.cuda.synchronize()
+    S_or = orc.project(prob.grid, prob.U, prob.V, prob.sigma, d, n)
+    for l in range(d):
+        assert rel(S[l], S_or[l]) <= 1e-13
+
+
 def test_project_empty_range_is_zero(pb):
     prob = problem(2, 5, 4, 5, random_uv=True)
     S = run_project(pb, prob, unit_begin=7, unit_end=7)
