@@ -35,7 +35,7 @@ int validate_dnm(int d, int n, int m, int64_t* N_out) {
     if (box >= (int64_t(1) << 31)) return PRONY_ERR_RANGE;
   }
   if (m > N) return PRONY_ERR_RANGE;
-  if (N * (int64_t)m >= (int64_t(1) << 40)) return PRONY_ERR_RANGE;
+  if (N * (int64_t)((m + 7) / 8 * 8) >= (int64_t(1) << 31)) return PRONY_ERR_RANGE;  // int32 offsets into V / Vsum
   *N_out = N;
   return PRONY_OK;
 }
@@ -57,7 +57,7 @@ void unit_rows(int d, int64_t N, int64_t u0, int64_t u1, int order, ProjGeom* g)
   }
 }
 
-size_t ws_project(int d, int64_t N, int m, int sms) { return project_workspace_bytes(d, (int)N, m, sms); }
+size_t ws_project(int d, int n, int64_t N, int m, int sms) { return project_workspace_bytes(d, n, (int)N, m, sms); }
 size_t ws_ls(int d, int n, int m, int sms) { return ls_workspace_bytes(d, n, m, sms); }
 
 // device copies used by prony_pencil_host, carved from the front of its workspace
@@ -87,7 +87,7 @@ HostLayout host_layout(int d, int n, int m, int64_t N, int sms) {
   h.t = take((size_t)m * d * sizeof(double));
   h.status = take(sizeof(int32_t));
   h.inner = off;
-  off += std::max(ws_project(d, N, m, sms), ws_ls(d, n, m, sms));
+  off += std::max(ws_project(d, n, N, m, sms), ws_ls(d, n, m, sms));
   h.total = off;
   return h;
 }
@@ -132,7 +132,7 @@ int prony_workspace_size(int kind, int d, int n, int m, size_t* bytes) {
   const int sms = sm_count_current();
   if (sms <= 0) return PRONY_ERR_CUDA;
   switch (kind) {
-    case PRONY_WS_PROJECT: *bytes = ws_project(d, N, m, sms); return PRONY_OK;
+    case PRONY_WS_PROJECT: *bytes = ws_project(d, n, N, m, sms); return PRONY_OK;
     case PRONY_WS_LS: *bytes = ws_ls(d, n, m, sms); return PRONY_OK;
     case PRONY_WS_PENCIL_HOST: *bytes = host_layout(d, n, m, N, sms).total; return PRONY_OK;
     case PRONY_WS_BUILD: *bytes = 0; return PRONY_OK;
@@ -163,7 +163,7 @@ int prony_project_ex(int d, int n, int m, const prony_c128* grid, const prony_c1
   if (unit_begin < 0 || unit_end < unit_begin || unit_end > (int64_t)d * N) return PRONY_ERR_RANGE;
   const int sms = sm_count_current();
   if (sms <= 0) return PRONY_ERR_CUDA;
-  if (workspace_bytes < ws_project(d, N, m, sms)) return PRONY_ERR_WORKSPACE;
+  if (workspace_bytes < ws_project(d, n, N, m, sms)) return PRONY_ERR_WORKSPACE;
   ProjGeom g{};
   g.d = d;
   g.n = n;
@@ -173,7 +173,7 @@ int prony_project_ex(int d, int n, int m, const prony_c128* grid, const prony_c1
   ProjPlan pl{};
   project_plan(g, sms, &pl);
   return project_launch(g, pl, (const double2*)grid, (const double2*)U, (const double2*)V, sigma, (double2*)S,
-                        workspace, (cudaStream_t)stream, info);
+                        workspace, sms, (cudaStream_t)stream, info);
 }
 
 int prony_vandermonde_ls(int d, int n, int m, const prony_c128* z, const prony_c128* grid, int64_t col_begin,

@@ -1,14 +1,14 @@
 // project.cu — S_l = U* T_l V Sigma^-1 (eq_generateSl) on sm_100a.
 //
-// Three launches per call:
-//   k_ptab      P(k) = sum_i k_i L^(d-1-i) for k in I_n (the linear box offset of k, so that
-//               T_l[k,h] = grid[P(k) - P(h) + L^(d-l) + C0], C0 = n sum_i L^i; F5)
-//   k_project   Y_c = T_l[rows, chunk c] * V[chunk c, :] — implicit-Toeplitz gather of T_l
-//               straight from the L2-resident sample grid into DMMA fragments (T_l is never
-//               written anywhere), complex FP64 4M on the FP64 tensor pipe (DMMA), split-K
-//               over column chunks c for wave balance; writes Y partials (N x NP per chunk).
-//   k_reduce    S_part[p] = U[rows_p]^* (sum_c Y_c[rows_p]) (fixed-order), then
-//   k_finalize  S_l = (sum_p S_part[p]) diag(1/sigma) (fixed order -> deterministic).
+// Launches per call:
+//   k_prep      P(k) = sum_i k_i L^(d-1-i) for k in I_n (linear box offset of k, so that
+//               T_l[k,h] = grid[P(k) - P(h) + L^(d-l) + C0], C0 = n sum_i L^i; F5),
+//               gsum = Re+Im of the grid and Vsum = Re+Im of V (3M operand planes)
+//   k_project   Y_c = T_l[rows, chunk c] V[chunk c, :] — implicit-Toeplitz gather of T_l straight
+//               from the L2-resident sample grid into shared memory (T_l is never written
+//               anywhere), complex FP64 on the DMMA pipe, split-K over column chunks c
+//   k_reduce    S_part[p] = U[rows_p]^* (sum_c Y_c[rows_p])   (same DMMA warp engine)
+//   k_finalize  S_l = (sum_p S_part[p]) diag(1/sigma)          (fixed order -> deterministic)
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -19,21 +19,25 @@
 
 namespace prony {
 
-// complex product formulation of k_project: 3 (Gauss/3M, default) or 4 (4M); env PRONY_CMUL=4m
+// complex product formulation: 3 (Gauss/3M, default) or 4 (4M); env PRONY_CMUL=4m selects 4M
 static int cmul_mode() {
   const char* e = getenv("PRONY_CMUL");
   return (e && (e[0] == '4')) ? 4 : 3;
 }
 
-// ---------------------------------------------------------------------------- P table
-__global__ void k_ptab(int d, int n, int N, int32_t* __restrict__ ptab) {
+// ---------------------------------------------------------------------------- prep
+__global__ void k_prep(int d, int n, int N, int m, int NP, int64_t box, const double2* __restrict__ grid,
+                       const double2* __restrict__ V, int32_t* __restrict__ ptab, double* __restrict__ gsum,
+                       double* __restrict__ vsum) {
   const int L = 2 * n + 2;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N + kPtabPad; k += gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int64_t k = t0; k < N + kPtabPad; k += stride) {
     if (k >= N) {
       ptab[k] = 0;
       continue;
     }
-    int r = k, P = 0, s = 1;
+    int r = (int)k, P = 0, s = 1;
     for (int i = d - 1; i >= 0; --i) {  // last coordinate fastest, stride 1
       P += (r % (n + 1)) * s;
       r /= (n + 1);
@@ -41,37 +45,24 @@ __global__ void k_ptab(int d, int n, int N, int32_t* __restrict__ ptab) {
     }
     ptab[k] = P;
   }
+  for (int64_t e = t0; e < box; e += stride) {
+    const double2 v = grid[e];
+    gsum[e] = v.x + v.y;
+  }
+  const int64_t nv = (int64_t)N * NP;
+  for (int64_t e = t0; e < nv; e += stride) {
+    const int64_t h = e / NP;
+    const int c = (int)(e % NP);
+    double s = 0.0;
+    if (c < m) {
+      const double2 v = V[h * m + c];
+      s = v.x + v.y;
+    }
+    vsum[e] = s;
+  }
 }
 
-// ---------------------------------------------------------------------------- projection
-// CTA = 8 warps = WM (row) x WN (col) warps; CTA tile BM = 16*WM rows of T_l x NP = 8*NT*WN
-// columns of V; warp tile 16 rows x 8*NT columns. The K loop (columns h of T_l, rows of V) runs
-// in stages of BK = 16 through a kStages-deep cp.async ring in shared memory:
-//   A tile  As[kc][r] = T_l[k_r][h0+kc] = grid[P(k_r) + s_l + C0 - P(h0+kc)]   (implicit Toeplitz
-//           gather: one 16-byte cp.async per element straight from the L2/L1-resident grid)
-//   B tile  Bs[kc][c] = V[h0+kc][c]  (zero-filled for c >= m and h >= h_end)
-// Consumers read the DMMA fragments with conflict-free LDS.128 (row strides BM+2, NP+2 double2).
-// Lane (g = lane>>2, q = lane&3): A frag rows g, g+8 at column q; B frag row q, column g.
-// MODE 4: 4M  Re += Ar Br - Ai Bi, Im += Ar Bi + Ai Br              (4 DMMA m16n8k4 / n-tile)
-// MODE 3: 3M  P1 += Ar Br, P2 += Ai Bi, P3 += (Ar+Ai)(Br+Bi);
-//             Re = P1 - P2, Im = P3 - P1 - P2                       (3 DMMA m16n8k4 / n-tile)
-constexpr int kBK = 16;
-constexpr int kStages = 4;
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int src_bytes) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async16_cg(void* smem_dst, const void* gsrc, int src_bytes) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
+// ---------------------------------------------------------------------------- warp engine
 // non-volatile so ptxas may interleave independent MMAs
 __device__ __forceinline__ void mma16x8x4(double (&c)[4], double a0, double a1, double b) {
   asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
@@ -79,27 +70,133 @@ __device__ __forceinline__ void mma16x8x4(double (&c)[4], double a0, double a1, 
       : "d"(a0), "d"(a1), "d"(b));
 }
 
+// Complex warp tile C(16 x 8*NA) += A(16 x 4) B(4 x 8*NA) for one k-step of 4, operands in shared
+// memory in k-major planes: Ac[k*lda + row] (re, im), As[k*ldas + row] (re+im), Bc[k*ldb + col],
+// Bs[k*ldbs + col]. Lane (g = lane>>2, q = lane&3) reads A rows g, g+8 at k = q and B column g at
+// k = q (conflict-free LDS: strides are = 2 (double2) / 4 (double) mod 16 x 8 bytes).
+// MODE 3 (3M): acc0 += Ar Br, acc1 += Ai Bi, acc2 += (Ar+Ai)(Br+Bi)
+// MODE 4 (4M): acc0 += Ar Br - Ai Bi, acc1 += Ar Bi + Ai Br
+// NA <= NT n-tiles are active (compile-time, so no predicated MMAs).
+template <int NT, int NA, int MODE>
+__device__ __forceinline__ void warp_cmma_k4(double (&acc)[3][NT][4], const double2* __restrict__ Ac,
+                                             const double* __restrict__ As, int lda, int ldas,
+                                             const double2* __restrict__ Bc, const double* __restrict__ Bs,
+                                             int ldb, int ldbs, int g, int q) {
+  const double2 a0 = Ac[q * lda + g];
+  const double2 a1 = Ac[q * lda + g + 8];
+  double s0 = 0.0, s1 = 0.0;
+  if constexpr (MODE == 3) {
+    s0 = As[q * ldas + g];
+    s1 = As[q * ldas + g + 8];
+  }
+  const double2* brow = Bc + q * ldb + g;
+  const double* bsrow = Bs + q * ldbs + g;
+#pragma unroll
+  for (int j = 0; j < NA; ++j) {
+    const double2 b = brow[8 * j];
+    if constexpr (MODE == 3) {
+      const double bs = bsrow[8 * j];
+      mma16x8x4(acc[0][j], a0.x, a1.x, b.x);
+      mma16x8x4(acc[1][j], a0.y, a1.y, b.y);
+      mma16x8x4(acc[2][j], s0, s1, bs);
+    } else {
+      mma16x8x4(acc[0][j], a0.x, a1.x, b.x);
+      mma16x8x4(acc[1][j], a0.x, a1.x, b.y);
+      mma16x8x4(acc[0][j], -a0.y, -a1.y, b.y);
+      mma16x8x4(acc[1][j], a0.y, a1.y, b.x);
+    }
+  }
+}
+
+// dispatch on the warp's active n-tile count (warp-uniform) so each variant is fully unrolled
+template <int NT, int MODE>
+__device__ __forceinline__ void warp_cmma_k4_n(int nt_active, double (&acc)[3][NT][4], const double2* Ac,
+                                               const double* As, int lda, int ldas, const double2* Bc,
+                                               const double* Bs, int ldb, int ldbs, int g, int q) {
+  if (nt_active == NT) {
+    warp_cmma_k4<NT, NT, MODE>(acc, Ac, As, lda, ldas, Bc, Bs, ldb, ldbs, g, q);
+  } else if constexpr (NT > 1) {
+    if (nt_active == NT - 1) {
+      warp_cmma_k4<NT, NT - 1, MODE>(acc, Ac, As, lda, ldas, Bc, Bs, ldb, ldbs, g, q);
+    } else if constexpr (NT > 2) {
+      if (nt_active == NT - 2) {
+        warp_cmma_k4<NT, NT - 2, MODE>(acc, Ac, As, lda, ldas, Bc, Bs, ldb, ldbs, g, q);
+      } else if constexpr (NT > 3) {
+        if (nt_active == NT - 3) warp_cmma_k4<NT, NT - 3, MODE>(acc, Ac, As, lda, ldas, Bc, Bs, ldb, ldbs, g, q);
+      }
+    }
+  }
+}
+
+template <int NT, int MODE>
+__device__ __forceinline__ void acc_to_complex(const double (&acc)[3][NT][4], int j, double (&re)[4],
+                                               double (&im)[4]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if constexpr (MODE == 3) {
+      re[e] = acc[0][j][e] - acc[1][j][e];
+      im[e] = acc[2][j][e] - acc[0][j][e] - acc[1][j][e];
+    } else {
+      re[e] = acc[0][j][e];
+      im[e] = acc[1][j][e];
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t sdst, const void* gsrc, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(uint32_t sdst, const void* gsrc, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async16_cg(uint32_t sdst, const void* gsrc, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ---------------------------------------------------------------------------- projection
+// CTA = 16 warps = WM (row) x WN (col) warps; CTA tile BM = 16*WM rows of T_l x NP = 8*ntot
+// columns of V (ntot = ceil(m/8) n-tiles split near-evenly over the WN column warps, <= NT each);
+// warp tile 16 rows x 8*nt_active columns. The K loop (columns h of T_l = rows of V) runs in
+// stages of kBK = 16 through a kStages-deep cp.async ring in shared memory:
+//   A planes  Ac[kc][r] = T_l[k_r][h0+kc] = grid[P(k_r) + s_l + C0 - P(h0+kc)],  As = gsum[same]
+//             (implicit Toeplitz gather: one 16-byte + one 8-byte cp.async per element straight
+//             from the L2/L1-resident grid; zero-filled outside the tile)
+//   B planes  Bc[kc][c] = V[h0+kc][c], Bs[kc][c] = Vsum[h0+kc][c] (zero-filled for c >= m, h >= h_end)
+// The next stage's copies are issued in kBK/4 slices interleaved with the current stage's k-steps.
+constexpr int kThreads = 512;
+
 template <int NT, int WN>
 struct ProjTile {
-  static constexpr int WM = 8 / WN;
+  static constexpr int WM = 16 / WN;
   static constexpr int BM = 16 * WM;
-  static constexpr int NP = 8 * NT * WN;
-  static constexpr int AS = BM + 2;
-  static constexpr int BS = NP + 2;
-  static constexpr int STAGE = kBK * (AS + BS);  // double2 per stage
-  static constexpr size_t SMEM = (size_t)kStages * STAGE * sizeof(double2);
-  static constexpr int GA = kBK * BM / 256;      // A elements gathered per thread per stage
-  static constexpr int KSTEP = 256 / BM;         // column stride between a thread's A elements
-  static constexpr int GB = (kBK * NP + 255) / 256;
+  static constexpr int NPMAX = 8 * NT * WN;          // smem capacity (NP <= NPMAX)
+  static constexpr int LDA = BM + 2, LDAS = BM + 4;  // double2 / double strides (conflict-free)
+  static constexpr int LDB = NPMAX + 2, LDBS = NPMAX + 4;
+  static constexpr int A_C = 0;                      // offsets in doubles within a stage
+  static constexpr int A_S = A_C + kBK * LDA * 2;
+  static constexpr int B_C = A_S + kBK * LDAS;
+  static constexpr int B_S = B_C + kBK * LDB * 2;
+  static constexpr int STAGE = B_S + kBK * LDBS;
+  static constexpr size_t SMEM = (size_t)kStages * STAGE * sizeof(double);
+  static constexpr int GA = kBK * BM / kThreads;           // A elements gathered per thread per stage
+  static constexpr int KSTEP = kThreads / BM;              // column stride between a thread's A elements
+  static constexpr int GB = (kBK * NPMAX + kThreads - 1) / kThreads;  // B elements per thread per stage
+  static_assert(STAGE % 2 == 0, "stage must keep 16-byte alignment");
+  static_assert(GA * KSTEP == kBK, "A gather covers the stage");
 };
 
 template <int NT, int WN, int MODE>
-__global__ void __launch_bounds__(256, 1) k_project(ProjParams p) {
+__global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
   using T = ProjTile<NT, WN>;
-  constexpr int WM = T::WM, BM = T::BM, NP = T::NP, AS = T::AS, BS = T::BS, GA = T::GA, KSTEP = T::KSTEP,
-                GB = T::GB;
-  constexpr int NACC = MODE == 3 ? 3 : 2;
-  extern __shared__ __align__(16) double2 smem[];
+  constexpr int WM = T::WM, BM = T::BM, GA = T::GA, KSTEP = T::KSTEP, GB = T::GB;
+  constexpr int NSLICE = kBK / 4;  // copy slices per stage (one per k-step)
+  extern __shared__ __align__(16) double smem[];
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -115,57 +212,77 @@ __global__ void __launch_bounds__(256, 1) k_project(ProjParams p) {
   const int KT = (h_end - h_begin + kBK - 1) / kBK;
   const int32_t* __restrict__ ptab = p.ptab;
   const double2* __restrict__ grid = p.grid;
+  const double* __restrict__ gsum = p.gsum;
   const double2* __restrict__ V = p.V;
-  const int m = p.m, N = p.N;
+  const double* __restrict__ vsum = p.vsum;
+  const int m = p.m, N = p.N, NP = p.NP;
+  const int ntot = NP / 8;
+  const int t0 = (ntot * wn) / WN;                    // first n-tile of this warp
+  const int nt_active = (ntot * (wn + 1)) / WN - t0;  // <= NT
 
-  // gather role: row ra of the tile, columns kc0 + KSTEP*x
+  // A gather role: row ra of the tile, columns kc0 + KSTEP*x
   const int ra = tid % BM, kc0 = tid / BM;
   const bool va = rb0 + ra < rows;
   const int PA = va ? ptab[p.kb[l] + rb0 + ra] + p.shift[l] : 0;
+  // B load role: elements e = tid + kThreads*y of the kBK x NP tile (fixed per thread)
+  int b_rc[GB];  // (row kr << 16) | column, or -1 if the element is outside the tile
+#pragma unroll
+  for (int y = 0; y < GB; ++y) {
+    const int e = tid + kThreads * y;
+    b_rc[y] = e < kBK * NP ? ((e / NP) << 16) | (e % NP) : -1;
+  }
 
-  auto load_ph = [&](int h0, int (&ph)[GA]) {
+  int ph[GA];
+  auto load_ph = [&](int h0) {
 #pragma unroll
     for (int x = 0; x < GA; ++x) {
       const int h = h0 + kc0 + KSTEP * x;
       ph[x] = h < N ? __ldg(ptab + h) : 0;
     }
   };
-  auto load_stage = [&](int slot, int h0, const int (&ph)[GA]) {
-    double2* As = smem + slot * T::STAGE;
-    double2* Bs = As + kBK * AS;
+  // issue slice `s` of the copies of stage (slot, h0)
+  auto load_slice = [&](int s, int slot, int h0) {
+    const uint32_t st = sbase + (uint32_t)(slot * T::STAGE) * 8u;
 #pragma unroll
     for (int x = 0; x < GA; ++x) {
-      const int kc = kc0 + KSTEP * x;
-      const bool ok = va && (h0 + kc < h_end);
-      cp_async16(As + kc * AS + ra, grid + (ok ? PA - ph[x] : 0), ok ? 16 : 0);
+      if (x % NSLICE == s) {
+        const int kc = kc0 + KSTEP * x;
+        const bool ok = va && (h0 + kc < h_end);
+        const int idx = ok ? PA - ph[x] : 0;
+        cp_async16(st + (uint32_t)(T::A_C + 2 * (kc * T::LDA + ra)) * 8u, grid + idx, ok ? 16 : 0);
+        if constexpr (MODE == 3) cp_async8(st + (uint32_t)(T::A_S + kc * T::LDAS + ra) * 8u, gsum + idx, ok ? 8 : 0);
+      }
     }
 #pragma unroll
     for (int y = 0; y < GB; ++y) {
-      const int e = tid + 256 * y;
-      if (e < kBK * NP) {
-        const int kr = e / NP, col = e % NP;
+      if (y % NSLICE == s && b_rc[y] >= 0) {
+        const int kr = b_rc[y] >> 16, col = b_rc[y] & 0xffff;
         const int h = h0 + kr;
-        const bool ok = (h < h_end) && (col < m);
-        cp_async16_cg(Bs + kr * BS + col, V + (ok ? (size_t)h * m + col : 0), ok ? 16 : 0);
+        const bool okh = h < h_end;
+        const bool ok = okh && (col < m);
+        cp_async16_cg(st + (uint32_t)(T::B_C + 2 * (kr * T::LDB + col)) * 8u, V + (ok ? h * m + col : 0),
+                      ok ? 16 : 0);
+        if constexpr (MODE == 3)
+          cp_async8(st + (uint32_t)(T::B_S + kr * T::LDBS + col) * 8u, vsum + (okh ? h * NP + col : 0), okh ? 8 : 0);
       }
     }
   };
 
-  double acc[NACC][NT][4];
+  double acc[3][NT][4];
 #pragma unroll
-  for (int a = 0; a < NACC; ++a)
+  for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int j = 0; j < NT; ++j)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[a][j][e] = 0.0;
 
-  int ph[GA];
-  load_ph(h_begin, ph);
+  load_ph(h_begin);
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
     if (s < KT) {
-      load_stage(s, h_begin + s * kBK, ph);
-      load_ph(h_begin + (s + 1) * kBK, ph);
+#pragma unroll
+      for (int sl = 0; sl < NSLICE; ++sl) load_slice(sl, s, h_begin + s * kBK);
+      load_ph(h_begin + (s + 1) * kBK);
     }
     cp_async_commit();
   }
@@ -174,142 +291,162 @@ __global__ void __launch_bounds__(256, 1) k_project(ProjParams p) {
     cp_async_wait<kStages - 2>();
     __syncthreads();
     const int nk = kt + kStages - 1;
-    if (nk < KT) {
-      load_stage(nk % kStages, h_begin + nk * kBK, ph);
-      load_ph(h_begin + (nk + 1) * kBK, ph);
-    }
-    cp_async_commit();
+    const bool issue = nk < KT;
+    const int nslot = nk % kStages, nh0 = h_begin + nk * kBK;
 
-    const double2* As = smem + (kt % kStages) * T::STAGE;
-    const double2* Bs = As + kBK * AS;
+    const double* st = smem + (kt % kStages) * T::STAGE;
+    const double2* Ac = reinterpret_cast<const double2*>(st + T::A_C) + wm * 16;
+    const double* As = st + T::A_S + wm * 16;
+    const double2* Bc = reinterpret_cast<const double2*>(st + T::B_C) + t0 * 8;
+    const double* Bs = st + T::B_S + t0 * 8;
 #pragma unroll
-    for (int kk = 0; kk < kBK / 4; ++kk) {
-      const double2 a0 = As[(kk * 4 + q) * AS + wm * 16 + g];
-      const double2 a1 = As[(kk * 4 + q) * AS + wm * 16 + g + 8];
-      const double2* brow = Bs + (kk * 4 + q) * BS + wn * NT * 8 + g;
-      if constexpr (MODE == 3) {
-        const double s0 = a0.x + a0.y, s1 = a1.x + a1.y;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          const double2 b = brow[8 * j];
-          mma16x8x4(acc[0][j], a0.x, a1.x, b.x);
-          mma16x8x4(acc[1][j], a0.y, a1.y, b.y);
-          mma16x8x4(acc[2][j], s0, s1, b.x + b.y);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          const double2 b = brow[8 * j];
-          mma16x8x4(acc[0][j], a0.x, a1.x, b.x);
-          mma16x8x4(acc[1][j], a0.x, a1.x, b.y);
-          mma16x8x4(acc[0][j], -a0.y, -a1.y, b.y);
-          mma16x8x4(acc[1][j], a0.y, a1.y, b.x);
-        }
-      }
+    for (int kk = 0; kk < NSLICE; ++kk) {
+      if (issue) load_slice(kk, nslot, nh0);
+      warp_cmma_k4_n<NT, MODE>(nt_active, acc, Ac + kk * 4 * T::LDA, As + kk * 4 * T::LDAS, T::LDA, T::LDAS,
+                               Bc + kk * 4 * T::LDB, Bs + kk * 4 * T::LDBS, T::LDB, T::LDBS, g, q);
     }
+    if (issue) load_ph(nh0 + kBK);
+    cp_async_commit();
   }
   cp_async_wait<0>();
 
-  // epilogue: Y[chunk][yoff_l + r][col], NP-wide rows (all NP columns written)
+  // epilogue: Y[chunk][yoff_l + r][col], NP-wide rows (padding columns are zero)
   const int r0 = rb0 + wm * 16 + g, r1 = r0 + 8;
   const size_t ybase = (size_t)chunk * p.R_tot + p.yoff[l];
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
-    double re[4], im[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if constexpr (MODE == 3) {
-        re[e] = acc[0][j][e] - acc[1][j][e];
-        im[e] = acc[2][j][e] - acc[0][j][e] - acc[1][j][e];
-      } else {
-        re[e] = acc[0][j][e];
-        im[e] = acc[1][j][e];
+    if (j < nt_active) {
+      double re[4], im[4];
+      acc_to_complex<NT, MODE>(acc, j, re, im);
+      const int col = (t0 + j) * 8 + 2 * q;
+      if (r0 < rows) {
+        double2* y = p.Y + (ybase + r0) * NP + col;
+        y[0] = make_double2(re[0], im[0]);
+        y[1] = make_double2(re[1], im[1]);
       }
-    }
-    const int col = wn * NT * 8 + 8 * j + 2 * q;
-    if (r0 < rows) {
-      double2* y = p.Y + (ybase + r0) * NP + col;
-      y[0] = make_double2(re[0], im[0]);
-      y[1] = make_double2(re[1], im[1]);
-    }
-    if (r1 < rows) {
-      double2* y = p.Y + (ybase + r1) * NP + col;
-      y[0] = make_double2(re[2], im[2]);
-      y[1] = make_double2(re[3], im[3]);
+      if (r1 < rows) {
+        double2* y = p.Y + (ybase + r1) * NP + col;
+        y[0] = make_double2(re[2], im[2]);
+        y[1] = make_double2(re[3], im[3]);
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------------------- reduce
-// grid (RP, d, ceil(m/64)); CTA p of segment l sums rows [rows*p/RP, rows*(p+1)/RP):
-//   S_part[l][p][i][j] = sum_k conj(U[k][i]) * sum_c Y_c[k][j],  i in [i0, i0+64), j < m.
-// Thread (ti, tj) owns i = i0 + ti + 16a (a<4), j = tj + 16b (b<8). DFMA (0.25% of the flops).
-__global__ void __launch_bounds__(256) k_reduce(RedParams p) {
-  __shared__ double2 Us[16][64];
-  __shared__ double2 Ys[16][kMaxNP];
+// grid (RP, d, ceil(m/BI)); CTA (p, l, ib) sums rows k in [rows*p/RP, rows*(p+1)/RP) of segment l:
+//   S_part[l][p][i][j] = sum_k conj(U[k][i]) * sum_c Y_c[k][j],  i in [BI ib, BI ib + BI), j < m
+// with the k_project warp engine (16 warps: WM x WN, BI = 16 WM): A = U^H staged as [k][i] planes
+// (conj, conj-sum), B = sum_c Y_c staged as [k][j] planes; 8 rows k per slab, register-prefetched
+// one slab ahead.
+template <int NT, int WN, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_reduce(RedParams p) {
+  constexpr int WM = 16 / WN, BI = 16 * WM, NPMAX = 8 * NT * WN;
+  constexpr int LDA = BI + 2, LDAS = BI + 4, LDB = NPMAX + 2, LDBS = NPMAX + 4;
+  constexpr int SL = 8;  // rows k per slab
+  __shared__ __align__(16) double2 Ac[SL * LDA];
+  __shared__ double As[SL * LDAS];
+  __shared__ __align__(16) double2 Bc[SL * LDB];
+  __shared__ double Bs[SL * LDBS];
   const int l = blockIdx.y;
   const int P = blockIdx.x;
-  const int i0 = blockIdx.z * 64;
+  const int i0 = blockIdx.z * BI;
   const int rows = p.rows[l];
   const int rbeg = (int)((int64_t)rows * P / p.RP), rend = (int)((int64_t)rows * (P + 1) / p.RP);
-  const int tid = threadIdx.x, ti = tid >> 4, tj = tid & 15;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WM, wn = warp / WM;
+  const int g = lane >> 2, q = lane & 3;
   const int m = p.m, NP = p.NP;
-  double2 acc[4][8];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = make_double2(0.0, 0.0);
+  const int ntot = NP / 8;
+  const int t0 = (ntot * wn) / WN;
+  const int nt_active = (ntot * (wn + 1)) / WN - t0;
+  const bool warp_rows = (i0 + wm * 16) < m;
 
-  for (int s = rbeg; s < rend; s += 16) {
-    for (int e = tid; e < 16 * 64; e += 256) {
-      const int r = e >> 6, ii = e & 63;
+  double acc[3][NT][4];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[a][j][e] = 0.0;
+
+  constexpr int NU = (SL * BI + kThreads - 1) / kThreads;
+  constexpr int NY = (SL * NPMAX + kThreads - 1) / kThreads;
+  double2 ru[NU], ry[NY];
+  auto load_slab = [&](int s) {
+#pragma unroll
+    for (int x = 0; x < NU; ++x) {
+      const int e = tid + kThreads * x;
+      const int r = e / BI, ii = e % BI;
       const int row = s + r, i = i0 + ii;
-      double2 u = make_double2(0.0, 0.0);
-      if (row < rend && i < m) u = cconj(ldg2(p.U + (size_t)(p.kb[l] + row) * m + i));
-      Us[r][ii] = u;
+      ru[x] = (e < SL * BI && row < rend && i < m) ? ldg2(p.U + (size_t)(p.kb[l] + row) * m + i)
+                                                     : make_double2(0.0, 0.0);
     }
-    for (int e = tid; e < 16 * kMaxNP; e += 256) {
-      const int r = e / kMaxNP, jj = e % kMaxNP;
-      const int row = s + r;
-      double2 y = make_double2(0.0, 0.0);
-      if (row < rend && jj < NP) {
-        for (int c = 0; c < p.KC; ++c) {  // fixed chunk order
-          const double2 v = ldg2(p.Y + ((size_t)c * p.R_tot + p.yoff[l] + row) * NP + jj);
-          y.x += v.x;
-          y.y += v.y;
+#pragma unroll
+    for (int y = 0; y < NY; ++y) {
+      const int e = tid + kThreads * y;
+      double2 a2 = make_double2(0.0, 0.0);
+      if (e < SL * NP) {
+        const int r = e / NP, jj = e % NP;
+        const int row = s + r;
+        if (row < rend) {
+          for (int c = 0; c < p.KC; ++c) {  // fixed chunk order
+            const double2 v = ldg2(p.Y + ((size_t)c * p.R_tot + p.yoff[l] + row) * NP + jj);
+            a2.x += v.x;
+            a2.y += v.y;
+          }
         }
       }
-      Ys[r][jj] = y;
+      ry[y] = a2;
+    }
+  };
+  if (rbeg < rend) load_slab(rbeg);
+  for (int s = rbeg; s < rend; s += SL) {
+#pragma unroll
+    for (int x = 0; x < NU; ++x) {
+      const int e = tid + kThreads * x;
+      if (e < SL * BI) {
+        const int r = e / BI, ii = e % BI;
+        const double2 u = make_double2(ru[x].x, -ru[x].y);  // conj(U)
+        Ac[r * LDA + ii] = u;
+        As[r * LDAS + ii] = u.x + u.y;
+      }
+    }
+#pragma unroll
+    for (int y = 0; y < NY; ++y) {
+      const int e = tid + kThreads * y;
+      if (e < SL * NP) {
+        const int r = e / NP, jj = e % NP;
+        Bc[r * LDB + jj] = ry[y];
+        Bs[r * LDBS + jj] = ry[y].x + ry[y].y;
+      }
     }
     __syncthreads();
-#pragma unroll 4
-    for (int r = 0; r < 16; ++r) {
-      double2 u[4], y[8];
+    if (s + SL < rend) load_slab(s + SL);
+    if (warp_rows) {
 #pragma unroll
-      for (int a = 0; a < 4; ++a) u[a] = Us[r][ti + 16 * a];
-#pragma unroll
-      for (int b = 0; b < 8; ++b) y[b] = Ys[r][tj + 16 * b];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          acc[a][b].x = fma(u[a].x, y[b].x, acc[a][b].x);
-          acc[a][b].x = fma(-u[a].y, y[b].y, acc[a][b].x);
-          acc[a][b].y = fma(u[a].x, y[b].y, acc[a][b].y);
-          acc[a][b].y = fma(u[a].y, y[b].x, acc[a][b].y);
-        }
+      for (int kk = 0; kk < SL / 4; ++kk)
+        warp_cmma_k4_n<NT, MODE>(nt_active, acc, Ac + kk * 4 * LDA + wm * 16, As + kk * 4 * LDAS + wm * 16, LDA,
+                                 LDAS, Bc + kk * 4 * LDB + t0 * 8, Bs + kk * 4 * LDBS + t0 * 8, LDB, LDBS, g, q);
     }
     __syncthreads();
   }
   double2* out = p.Spart + ((size_t)l * p.RP + P) * m * m;
+  const int ia = i0 + wm * 16 + g, ib = ia + 8;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int i = i0 + ti + 16 * a;
-    if (i >= m) continue;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const int j = tj + 16 * b;
-      if (j < m) out[(size_t)i * m + j] = acc[a][b];
+  for (int j = 0; j < NT; ++j) {
+    if (j < nt_active) {
+      double re[4], im[4];
+      acc_to_complex<NT, MODE>(acc, j, re, im);
+      const int col = (t0 + j) * 8 + 2 * q;
+      if (ia < m) {
+        if (col < m) out[(size_t)ia * m + col] = make_double2(re[0], im[0]);
+        if (col + 1 < m) out[(size_t)ia * m + col + 1] = make_double2(re[1], im[1]);
+      }
+      if (ib < m) {
+        if (col < m) out[(size_t)ib * m + col] = make_double2(re[2], im[2]);
+        if (col + 1 < m) out[(size_t)ib * m + col + 1] = make_double2(re[3], im[3]);
+      }
     }
   }
 }
@@ -334,15 +471,15 @@ __global__ void k_finalize(int d, int m, int RP, const double2* __restrict__ Spa
 }
 
 // ---------------------------------------------------------------------------- host side
+// 16 warps per CTA; WN column warps with <= NT <= 4 n-tiles each (3M accumulators fit 128 regs)
 ProjShape proj_shape(int m) {
   ProjShape s;
   const int ntot = (m + 7) / 8;
-  s.WN = (ntot + 6) / 7;  // <= 7 n-tiles per warp
-  if (s.WN > 2) s.WN = 2;
+  s.WN = ntot <= 8 ? 2 : 4;
   s.NT = (ntot + s.WN - 1) / s.WN;
-  s.WM = 8 / s.WN;
+  s.WM = 16 / s.WN;
   s.BM = 16 * s.WM;
-  s.NP = 8 * s.NT * s.WN;
+  s.NP = 8 * ntot;
   return s;
 }
 
@@ -358,8 +495,8 @@ int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl) {
   }
   pl->R_tot = R_tot;
   pl->max_rows = max_rows;
-  // split-K: chunk count KC minimizing ceil(waves)/KC (time per CTA ~ 1/KC), subject to
-  // KC * R_tot <= 2 d N (workspace bound) and chunks of >= 64 columns.
+  // split-K: chunk count KC minimizing waves x (chunk columns + pipeline fill), subject to
+  // KC * R_tot <= kYCap d N (workspace bound) and chunks of >= 64 columns.
   const int64_t cap_rows = (int64_t)kYCap * g.d * g.N;
   int kc_max = (int)std::min<int64_t>(64, std::max<int64_t>(1, cap_rows / std::max(R_tot, 1)));
   kc_max = std::max(1, std::min(kc_max, std::max(1, g.N / 64)));
@@ -368,60 +505,80 @@ int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl) {
   for (int kc = 1; kc <= kc_max; ++kc) {
     const double ctas = (double)row_blocks * kc;
     const double waves = std::ceil(ctas / sm_count);
-    // time ~ waves x (chunk columns + pipeline fill/drain of ~4 stages)
     const double cost = waves * ((double)g.N / kc + 4.0 * kBK);
-    if (cost < best - 1e-12) {
+    if (cost < best - 1e-9) {
       best = cost;
       best_kc = kc;
     }
   }
   int chunk_w = (g.N + best_kc - 1) / best_kc;
-  chunk_w = (chunk_w + 3) / 4 * 4;
+  chunk_w = (chunk_w + kBK - 1) / kBK * kBK;
   pl->chunk_w = chunk_w;
   pl->KC = (g.N + chunk_w - 1) / chunk_w;  // every chunk non-empty
-  // reduce partition: about 2 CTAs per SM in total
-  const int ib = (g.m + 63) / 64;
-  int RP = (2 * sm_count) / std::max(1, g.d * ib);
-  RP = std::max(1, std::min(RP, std::max(1, (max_rows + 15) / 16)));
+  // reduce partition: about 1 CTA per SM in total
+  const int ib = (g.m + sh.BM - 1) / sh.BM;
+  int RP = sm_count / std::max(1, g.d * ib);
+  RP = std::max(1, std::min(RP, std::max(1, (max_rows + 7) / 8)));
   pl->RP = RP;
   return 0;
 }
 
-size_t project_workspace_bytes(int d, int N, int m, int sm_count) {
+namespace {
+struct WsLayout {
+  size_t ptab, gsum, vsum, Y, Spart, total;
+};
+WsLayout ws_layout(int d, int n, int N, int m, int sm_count) {
   const ProjShape sh = proj_shape(m);
-  size_t bytes = align_up((size_t)(N + kPtabPad) * sizeof(int32_t), 256);
-  bytes += align_up((size_t)kYCap * d * N * sh.NP * sizeof(double2), 256);  // Y partials (KC*R_tot <= kYCap*dN)
-  const int ib = (m + 63) / 64;
-  int RP = std::max(1, (2 * sm_count) / std::max(1, d * ib));
-  bytes += align_up((size_t)d * RP * m * m * sizeof(double2), 256);
-  return bytes;
+  int64_t box = 1;
+  for (int i = 0; i < d; ++i) box *= (2 * (int64_t)n + 2);
+  WsLayout w{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += align_up(bytes, 256);
+    return o;
+  };
+  w.ptab = take((size_t)(N + kPtabPad) * sizeof(int32_t));
+  w.gsum = take((size_t)box * sizeof(double));
+  w.vsum = take((size_t)N * sh.NP * sizeof(double));
+  w.Y = take((size_t)kYCap * d * N * sh.NP * sizeof(double2));  // Y partials (KC*R_tot <= kYCap*dN)
+  const int ib = (m + sh.BM - 1) / sh.BM;
+  const int RP = std::max(1, sm_count / std::max(1, d * ib));
+  w.Spart = take((size_t)d * RP * m * m * sizeof(double2));
+  w.total = off;
+  return w;
+}
+}  // namespace
+
+size_t project_workspace_bytes(int d, int n, int N, int m, int sm_count) {
+  return ws_layout(d, n, N, m, sm_count).total;
 }
 
 template <int NT, int WN>
-static int launch_project_t(const ProjParams& p, dim3 grid, cudaStream_t st, int mode) {
+static int launch_project_t(const ProjParams& p, const RedParams& r, dim3 grid, dim3 rgrid, cudaStream_t st,
+                            int mode, prony_exec_info* info) {
   const size_t smem = ProjTile<NT, WN>::SMEM;
-  if (mode == 4) {
-    if (cudaFuncSetAttribute(k_project<NT, WN, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return PRONY_ERR_CUDA;
-    k_project<NT, WN, 4><<<grid, 256, smem, st>>>(p);
-  } else {
-    if (cudaFuncSetAttribute(k_project<NT, WN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return PRONY_ERR_CUDA;
-    k_project<NT, WN, 3><<<grid, 256, smem, st>>>(p);
-  }
+  auto kp = mode == 4 ? k_project<NT, WN, 4> : k_project<NT, WN, 3>;
+  auto kr = mode == 4 ? k_reduce<NT, WN, 4> : k_reduce<NT, WN, 3>;
+  if (cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return PRONY_ERR_CUDA;
+  if (info && info->ev_main_begin) cudaEventRecord((cudaEvent_t)info->ev_main_begin, st);
+  kp<<<grid, kThreads, smem, st>>>(p);
+  if (info && info->ev_main_end) cudaEventRecord((cudaEvent_t)info->ev_main_end, st);
+  kr<<<rgrid, kThreads, 0, st>>>(r);
   return PRONY_OK;
 }
 
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
-                   const double* sigma, double2* S, void* ws, cudaStream_t st, prony_exec_info* info) {
+                   const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
+                   prony_exec_info* info) {
+  const WsLayout wl = ws_layout(g.d, g.n, g.N, g.m, sm_count);
   char* w = (char*)ws;
-  int32_t* ptab = (int32_t*)w;
-  w += align_up((size_t)(g.N + kPtabPad) * sizeof(int32_t), 256);
-  double2* Y = (double2*)w;
-  w += align_up((size_t)kYCap * g.d * g.N * pl.shape.NP * sizeof(double2), 256);
-  double2* Spart = (double2*)w;
+  int32_t* ptab = (int32_t*)(w + wl.ptab);
+  double* gsum = (double*)(w + wl.gsum);
+  double* vsum = (double*)(w + wl.vsum);
+  double2* Y = (double2*)(w + wl.Y);
+  double2* Spart = (double2*)(w + wl.Spart);
 
   if (info) {
     info->launches = 0;
@@ -434,11 +591,15 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
     if (cudaMemsetAsync(S, 0, (size_t)g.d * g.m * g.m * sizeof(double2), st) != cudaSuccess) return PRONY_ERR_CUDA;
     return PRONY_OK;
   }
-  k_ptab<<<(g.N + kPtabPad + 255) / 256, 256, 0, st>>>(g.d, g.n, g.N, ptab);
+  int64_t box = 1;
+  for (int i = 0; i < g.d; ++i) box *= (2 * (int64_t)g.n + 2);
+  k_prep<<<2 * sm_count, 256, 0, st>>>(g.d, g.n, g.N, g.m, pl.shape.NP, box, grid, V, ptab, gsum, vsum);
 
   ProjParams p{};
   p.grid = grid;
+  p.gsum = gsum;
   p.V = V;
+  p.vsum = vsum;
   p.ptab = ptab;
   p.Y = Y;
   p.N = g.N;
@@ -458,25 +619,6 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
     p.yoff[l] = pl.yoff[l];
     p.shift[l] = (int)(ipow(L, g.d - 1 - l) + C0);  // s_l = L^(d-l) for l = 1..d
   }
-  dim3 grd((pl.max_rows + pl.shape.BM - 1) / pl.shape.BM, pl.KC, g.d);
-  const int NT = pl.shape.NT, WN = pl.shape.WN;
-  if (info && info->ev_main_begin) cudaEventRecord((cudaEvent_t)info->ev_main_begin, st);
-  const int mode = cmul_mode();
-  int lrc = PRONY_OK;
-  switch (WN * 16 + NT) {
-#define PRONY_CASE(nt, wn) \
-  case wn * 16 + nt:       \
-    lrc = launch_project_t<nt, wn>(p, grd, st, mode); \
-    break;
-    PRONY_CASE(1, 1) PRONY_CASE(2, 1) PRONY_CASE(3, 1) PRONY_CASE(4, 1) PRONY_CASE(5, 1) PRONY_CASE(6, 1)
-    PRONY_CASE(7, 1) PRONY_CASE(4, 2) PRONY_CASE(5, 2) PRONY_CASE(6, 2) PRONY_CASE(7, 2) PRONY_CASE(8, 2)
-#undef PRONY_CASE
-    default:
-      return PRONY_ERR_RANGE;
-  }
-  if (lrc != PRONY_OK) return lrc;
-  if (info && info->ev_main_end) cudaEventRecord((cudaEvent_t)info->ev_main_end, st);
-
   RedParams r{};
   r.Y = Y;
   r.U = U;
@@ -491,7 +633,23 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
     r.rows[l] = g.rows[l];
     r.yoff[l] = pl.yoff[l];
   }
-  k_reduce<<<dim3(pl.RP, g.d, (g.m + 63) / 64), 256, 0, st>>>(r);
+  dim3 grd((pl.max_rows + pl.shape.BM - 1) / pl.shape.BM, pl.KC, g.d);
+  dim3 rgrd(pl.RP, g.d, (g.m + pl.shape.BM - 1) / pl.shape.BM);
+  const int NT = pl.shape.NT, WN = pl.shape.WN;
+  const int mode = cmul_mode();
+  int lrc = PRONY_OK;
+  switch (WN * 16 + NT) {
+#define PRONY_CASE(nt, wn) \
+  case wn * 16 + nt:       \
+    lrc = launch_project_t<nt, wn>(p, r, grd, rgrd, st, mode, info); \
+    break;
+    PRONY_CASE(1, 2) PRONY_CASE(2, 2) PRONY_CASE(3, 2) PRONY_CASE(4, 2)
+    PRONY_CASE(3, 4) PRONY_CASE(4, 4)
+#undef PRONY_CASE
+    default:
+      return PRONY_ERR_RANGE;
+  }
+  if (lrc != PRONY_OK) return lrc;
   const int64_t tot = (int64_t)g.d * g.m * g.m;
   k_finalize<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256, 0, st>>>(g.d, g.m, pl.RP, Spart, sigma, S);
   if (info) {
@@ -499,7 +657,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
     info->main_grid[0] = (int)grd.x;
     info->main_grid[1] = (int)grd.y;
     info->main_grid[2] = (int)grd.z;
-    info->main_block = 256;
+    info->main_block = kThreads;
     info->split_k = pl.KC;
     info->main_flops = 8.0 * g.m * (double)g.N * (double)pl.R_tot;
   }

@@ -11,6 +11,8 @@ namespace prony {
 constexpr int kPtabPad = 4;   // P table padded so the last k-step may read P(h) for h < N+4
 constexpr int kMaxNP = 128;   // padded width of Y rows handled by k_reduce
 constexpr int kYCap = 4;      // split-K bound: KC * (rows in range) <= kYCap * d * N
+constexpr int kBK = 16;       // columns of T_l per pipeline stage of k_project
+constexpr int kStages = 3;    // cp.async ring depth of k_project (<= 227 KB smem)
 
 struct ProjShape {
   int NT, WN, WM, BM, NP;
@@ -33,7 +35,9 @@ struct ProjPlan {
 
 struct ProjParams {
   const double2* grid;
+  const double* gsum;
   const double2* V;
+  const double* vsum;
   const int32_t* ptab;
   double2* Y;
   int N, m, NP, chunk_w, R_tot;
@@ -50,8 +54,9 @@ struct RedParams {
 
 ProjShape proj_shape(int m);
 int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl);
-size_t project_workspace_bytes(int d, int N, int m, int sm_count);
+size_t project_workspace_bytes(int d, int n, int N, int m, int sm_count);
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
-                   const double* sigma, double2* S, void* ws, cudaStream_t st, prony_exec_info* info);
+                   const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
+                   prony_exec_info* info);
 
 }  // namespace prony
