@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "project.cuh"
@@ -158,21 +159,57 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// ---------------------------------------------------------------------------- mbarrier helpers
+__device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(addr), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t addr) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(addr) : "memory");
+}
+// arrive on the mbarrier once all of this thread's prior cp.async copies have landed
+__device__ __forceinline__ void mbar_arrive_cp_async(uint32_t addr) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+template <int R>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(R));
+}
+template <int R>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(R));
+}
+
 // ---------------------------------------------------------------------------- projection
-// CTA = 16 warps = WM (row) x WN (col) warps; CTA tile BM = 16*WM rows of T_l x NP = 8*ntot
-// columns of V (ntot = ceil(m/8) n-tiles split near-evenly over the WN column warps, <= NT each);
-// warp tile 16 rows x 8*nt_active columns. The K loop (columns h of T_l = rows of V) runs in
-// stages of kBK = 16 through a kStages-deep cp.async ring in shared memory:
+// Warp-specialized CTA of kThreads = 512 threads: warpgroups 0-2 are consumers (12 warps =
+// WM x WN, warp tile 16 rows x 8*nt_active columns, 3M/4M DMMA; setmaxnreg 152 registers),
+// warpgroup 3 is the producer (setmaxnreg 40): it fills a kStages-deep ring of kBK-column stages
+// with cp.async and signals each stage on a "full" mbarrier (cp.async.mbarrier.arrive); consumers
+// release a stage on its "empty" mbarrier. No CTA-wide barrier in the main loop.
 //   A planes  Ac[kc][r] = T_l[k_r][h0+kc] = grid[P(k_r) + s_l + C0 - P(h0+kc)],  As = gsum[same]
-//             (implicit Toeplitz gather: one 16-byte + one 8-byte cp.async per element straight
-//             from the L2/L1-resident grid; zero-filled outside the tile)
+//             (implicit Toeplitz gather straight from the L2/L1-resident grid, zero-filled outside)
 //   B planes  Bc[kc][c] = V[h0+kc][c], Bs[kc][c] = Vsum[h0+kc][c] (zero-filled for c >= m, h >= h_end)
-// The next stage's copies are issued in kBK/4 slices interleaved with the current stage's k-steps.
+// CTA tile: BM = 16*WM rows of T_l x NP = 8*ceil(m/8) columns of V (n-tiles split near-evenly
+// over the WN column warps, <= NT <= 4 each).
 constexpr int kThreads = 512;
+constexpr int kConsumerWarps = 12;
+constexpr int kProducerThreads = 128;
+constexpr int kConsumerRegs = 152;
+constexpr int kProducerRegs = 40;
 
 template <int NT, int WN>
 struct ProjTile {
-  static constexpr int WM = 16 / WN;
+  static constexpr int WM = kConsumerWarps / WN;
   static constexpr int BM = 16 * WM;
   static constexpr int NPMAX = 8 * NT * WN;          // smem capacity (NP <= NPMAX)
   static constexpr int LDA = BM + 2, LDAS = BM + 4;  // double2 / double strides (conflict-free)
@@ -182,81 +219,66 @@ struct ProjTile {
   static constexpr int B_C = A_S + kBK * LDAS;
   static constexpr int B_S = B_C + kBK * LDB * 2;
   static constexpr int STAGE = B_S + kBK * LDBS;
-  static constexpr size_t SMEM = (size_t)kStages * STAGE * sizeof(double);
-  static constexpr int GA = kBK * BM / kThreads;           // A elements gathered per thread per stage
-  static constexpr int KSTEP = kThreads / BM;              // column stride between a thread's A elements
-  static constexpr int GB = (kBK * NPMAX + kThreads - 1) / kThreads;  // B elements per thread per stage
+  static constexpr int BAR = kStages * STAGE;        // mbarriers after the stages (2 per stage)
+  static constexpr size_t SMEM = (size_t)(BAR + 2 * kStages) * sizeof(double);
   static_assert(STAGE % 2 == 0, "stage must keep 16-byte alignment");
-  static_assert(GA * KSTEP == kBK, "A gather covers the stage");
 };
 
 template <int NT, int WN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
   using T = ProjTile<NT, WN>;
-  constexpr int WM = T::WM, BM = T::BM, GA = T::GA, KSTEP = T::KSTEP, GB = T::GB;
-  constexpr int NSLICE = kBK / 4;  // copy slices per stage (one per k-step)
+  constexpr int WM = T::WM, BM = T::BM;
   extern __shared__ __align__(16) double smem[];
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t full0 = sbase + (uint32_t)T::BAR * 8u;       // full[s]  at full0 + 8 s
+  const uint32_t empty0 = full0 + (uint32_t)kStages * 8u;     // empty[s] at empty0 + 8 s
 
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % WM, wn = warp / WM;
-  const int g = lane >> 2, q = lane & 3;
   const int l = blockIdx.z;
   const int rows = p.rows[l];
   const int rb0 = blockIdx.x * BM;
-  if (rb0 >= rows) return;
+  if (rb0 >= rows) return;  // whole CTA exits together
   const int chunk = blockIdx.y;
   const int h_begin = chunk * p.chunk_w;
   const int h_end = min(h_begin + p.chunk_w, p.N);
   const int KT = (h_end - h_begin + kBK - 1) / kBK;
-  const int32_t* __restrict__ ptab = p.ptab;
-  const double2* __restrict__ grid = p.grid;
-  const double* __restrict__ gsum = p.gsum;
-  const double2* __restrict__ V = p.V;
-  const double* __restrict__ vsum = p.vsum;
   const int m = p.m, N = p.N, NP = p.NP;
-  const int ntot = NP / 8;
-  const int t0 = (ntot * wn) / WN;                    // first n-tile of this warp
-  const int nt_active = (ntot * (wn + 1)) / WN - t0;  // <= NT
 
-  // A gather role: row ra of the tile, columns kc0 + KSTEP*x
-  const int ra = tid % BM, kc0 = tid / BM;
-  const bool va = rb0 + ra < rows;
-  const int PA = va ? ptab[p.kb[l] + rb0 + ra] + p.shift[l] : 0;
-  // B load role: elements e = tid + kThreads*y of the kBK x NP tile (fixed per thread)
-  int b_rc[GB];  // (row kr << 16) | column, or -1 if the element is outside the tile
-#pragma unroll
-  for (int y = 0; y < GB; ++y) {
-    const int e = tid + kThreads * y;
-    b_rc[y] = e < kBK * NP ? ((e / NP) << 16) | (e % NP) : -1;
-  }
-
-  int ph[GA];
-  auto load_ph = [&](int h0) {
-#pragma unroll
-    for (int x = 0; x < GA; ++x) {
-      const int h = h0 + kc0 + KSTEP * x;
-      ph[x] = h < N ? __ldg(ptab + h) : 0;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full0 + 8u * s, kProducerThreads);
+      mbar_init(empty0 + 8u * s, kConsumerWarps);
     }
-  };
-  // issue slice `s` of the copies of stage (slot, h0)
-  auto load_slice = [&](int s, int slot, int h0) {
-    const uint32_t st = sbase + (uint32_t)(slot * T::STAGE) * 8u;
-#pragma unroll
-    for (int x = 0; x < GA; ++x) {
-      if (x % NSLICE == s) {
-        const int kc = kc0 + KSTEP * x;
-        const bool ok = va && (h0 + kc < h_end);
-        const int idx = ok ? PA - ph[x] : 0;
+  }
+  __syncthreads();
+
+  if (tid >= kConsumerWarps * 32) {
+    // ================================================================== producer warpgroup
+    setmaxnreg_dec<kProducerRegs>();
+    const int pt = tid - kConsumerWarps * 32;  // 0..127
+    const int32_t* __restrict__ ptab = p.ptab;
+    const double2* __restrict__ grid = p.grid;
+    const double* __restrict__ gsum = p.gsum;
+    const double2* __restrict__ V = p.V;
+    const double* __restrict__ vsum = p.vsum;
+    const int kb = p.kb[l], shift = p.shift[l];
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % kStages;
+      if (kt >= kStages) mbar_wait(empty0 + 8u * s, (uint32_t)((kt / kStages) - 1) & 1u);
+      const int h0 = h_begin + kt * kBK;
+      const uint32_t st = sbase + (uint32_t)(s * T::STAGE) * 8u;
+      // A gather: kBK x BM elements
+      for (int e = pt; e < kBK * BM; e += kProducerThreads) {
+        const int kc = e / BM, ra = e % BM;
+        const int h = h0 + kc;
+        const bool ok = (rb0 + ra < rows) && (h < h_end);
+        const int idx = ok ? __ldg(ptab + kb + rb0 + ra) + shift - __ldg(ptab + h) : 0;
         cp_async16(st + (uint32_t)(T::A_C + 2 * (kc * T::LDA + ra)) * 8u, grid + idx, ok ? 16 : 0);
         if constexpr (MODE == 3) cp_async8(st + (uint32_t)(T::A_S + kc * T::LDAS + ra) * 8u, gsum + idx, ok ? 8 : 0);
       }
-    }
-#pragma unroll
-    for (int y = 0; y < GB; ++y) {
-      if (y % NSLICE == s && b_rc[y] >= 0) {
-        const int kr = b_rc[y] >> 16, col = b_rc[y] & 0xffff;
+      // B rows: kBK x NP elements
+      for (int e = pt; e < kBK * NP; e += kProducerThreads) {
+        const int kr = e / NP, col = e % NP;
         const int h = h0 + kr;
         const bool okh = h < h_end;
         const bool ok = okh && (col < m);
@@ -265,8 +287,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
         if constexpr (MODE == 3)
           cp_async8(st + (uint32_t)(T::B_S + kr * T::LDBS + col) * 8u, vsum + (okh ? h * NP + col : 0), okh ? 8 : 0);
       }
+      mbar_arrive_cp_async(full0 + 8u * s);
     }
-  };
+    cp_async_wait<0>();
+    return;
+  }
+
+  // ==================================================================== consumer warpgroups
+  setmaxnreg_inc<kConsumerRegs>();
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WM, wn = warp / WM;
+  const int g = lane >> 2, q = lane & 3;
+  const int ntot = NP / 8;
+  const int t0 = (ntot * wn) / WN;                    // first n-tile of this warp
+  const int nt_active = (ntot * (wn + 1)) / WN - t0;  // <= NT
 
   double acc[3][NT][4];
 #pragma unroll
@@ -276,39 +310,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[a][j][e] = 0.0;
 
-  load_ph(h_begin);
+  auto run = [&](auto na_c) {
+    constexpr int NA = decltype(na_c)::value;
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % kStages;
+      mbar_wait(full0 + 8u * s, (uint32_t)(kt / kStages) & 1u);
+      if constexpr (NA > 0) {
+        const double* st = smem + s * T::STAGE;
+        const double2* Ac = reinterpret_cast<const double2*>(st + T::A_C) + wm * 16;
+        const double* As = st + T::A_S + wm * 16;
+        const double2* Bc = reinterpret_cast<const double2*>(st + T::B_C) + t0 * 8;
+        const double* Bs = st + T::B_S + t0 * 8;
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
-    if (s < KT) {
-#pragma unroll
-      for (int sl = 0; sl < NSLICE; ++sl) load_slice(sl, s, h_begin + s * kBK);
-      load_ph(h_begin + (s + 1) * kBK);
+        for (int kk = 0; kk < kBK / 4; ++kk)
+          warp_cmma_k4<NT, NA, MODE>(acc, Ac + kk * 4 * T::LDA, As + kk * 4 * T::LDAS, T::LDA, T::LDAS,
+                                     Bc + kk * 4 * T::LDB, Bs + kk * 4 * T::LDBS, T::LDB, T::LDBS, g, q);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8u * s);
     }
-    cp_async_commit();
-  }
-
-  for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<kStages - 2>();
-    __syncthreads();
-    const int nk = kt + kStages - 1;
-    const bool issue = nk < KT;
-    const int nslot = nk % kStages, nh0 = h_begin + nk * kBK;
-
-    const double* st = smem + (kt % kStages) * T::STAGE;
-    const double2* Ac = reinterpret_cast<const double2*>(st + T::A_C) + wm * 16;
-    const double* As = st + T::A_S + wm * 16;
-    const double2* Bc = reinterpret_cast<const double2*>(st + T::B_C) + t0 * 8;
-    const double* Bs = st + T::B_S + t0 * 8;
-#pragma unroll
-    for (int kk = 0; kk < NSLICE; ++kk) {
-      if (issue) load_slice(kk, nslot, nh0);
-      warp_cmma_k4_n<NT, MODE>(nt_active, acc, Ac + kk * 4 * T::LDA, As + kk * 4 * T::LDAS, T::LDA, T::LDAS,
-                               Bc + kk * 4 * T::LDB, Bs + kk * 4 * T::LDBS, T::LDB, T::LDBS, g, q);
+  };
+  if (nt_active == NT) {
+    run(std::integral_constant<int, NT>{});
+  } else if (nt_active == 0) {
+    run(std::integral_constant<int, 0>{});
+  } else if constexpr (NT > 1) {
+    if (nt_active == NT - 1) {
+      run(std::integral_constant<int, NT - 1>{});
+    } else if constexpr (NT > 2) {
+      if (nt_active == NT - 2) {
+        run(std::integral_constant<int, NT - 2>{});
+      } else if constexpr (NT > 3) {
+        if (nt_active == NT - 3) run(std::integral_constant<int, NT - 3>{});
+      }
     }
-    if (issue) load_ph(nh0 + kBK);
-    cp_async_commit();
   }
-  cp_async_wait<0>();
 
   // epilogue: Y[chunk][yoff_l + r][col], NP-wide rows (padding columns are zero)
   const int r0 = rb0 + wm * 16 + g, r1 = r0 + 8;
@@ -341,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
 // one slab ahead.
 template <int NT, int WN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_reduce(RedParams p) {
-  constexpr int WM = 16 / WN, BI = 16 * WM, NPMAX = 8 * NT * WN;
+  constexpr int WM = (kThreads / 32) / WN, BI = 16 * WM, NPMAX = 8 * NT * WN;
   constexpr int LDA = BI + 2, LDAS = BI + 4, LDB = NPMAX + 2, LDBS = NPMAX + 4;
   constexpr int SL = 8;  // rows k per slab
   __shared__ __align__(16) double2 Ac[SL * LDA];
@@ -477,8 +513,9 @@ ProjShape proj_shape(int m) {
   const int ntot = (m + 7) / 8;
   s.WN = ntot <= 8 ? 2 : 4;
   s.NT = (ntot + s.WN - 1) / s.WN;
-  s.WM = 16 / s.WN;
-  s.BM = 16 * s.WM;
+  s.WM = kConsumerWarps / s.WN;    // k_project consumer warps along rows
+  s.BM = 16 * s.WM;                // k_project rows per CTA
+  s.BI = 16 * (kThreads / 32) / s.WN;  // k_reduce rows i per CTA
   s.NP = 8 * ntot;
   return s;
 }
@@ -516,7 +553,7 @@ int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl) {
   pl->chunk_w = chunk_w;
   pl->KC = (g.N + chunk_w - 1) / chunk_w;  // every chunk non-empty
   // reduce partition: about 1 CTA per SM in total
-  const int ib = (g.m + sh.BM - 1) / sh.BM;
+  const int ib = (g.m + sh.BI - 1) / sh.BI;
   int RP = sm_count / std::max(1, g.d * ib);
   RP = std::max(1, std::min(RP, std::max(1, (max_rows + 7) / 8)));
   pl->RP = RP;
@@ -542,7 +579,7 @@ WsLayout ws_layout(int d, int n, int N, int m, int sm_count) {
   w.gsum = take((size_t)box * sizeof(double));
   w.vsum = take((size_t)N * sh.NP * sizeof(double));
   w.Y = take((size_t)kYCap * d * N * sh.NP * sizeof(double2));  // Y partials (KC*R_tot <= kYCap*dN)
-  const int ib = (m + sh.BM - 1) / sh.BM;
+  const int ib = (m + sh.BI - 1) / sh.BI;
   const int RP = std::max(1, sm_count / std::max(1, d * ib));
   w.Spart = take((size_t)d * RP * m * m * sizeof(double2));
   w.total = off;
@@ -634,7 +671,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
     r.yoff[l] = pl.yoff[l];
   }
   dim3 grd((pl.max_rows + pl.shape.BM - 1) / pl.shape.BM, pl.KC, g.d);
-  dim3 rgrd(pl.RP, g.d, (g.m + pl.shape.BM - 1) / pl.shape.BM);
+  dim3 rgrd(pl.RP, g.d, (g.m + pl.shape.BI - 1) / pl.shape.BI);
   const int NT = pl.shape.NT, WN = pl.shape.WN;
   const int mode = cmul_mode();
   int lrc = PRONY_OK;
