@@ -181,6 +181,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// expect `bytes` of bulk-copy transactions on the mbarrier (counts as one arrival)
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t addr, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(addr), "r"(bytes)
+               : "memory");
+}
+// bulk global -> shared copy (size multiple of 16, 16-byte aligned), completes on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void* gsrc, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(sdst),
+               "l"(gsrc), "r"(bytes), "r"(mbar)
+               : "memory");
+}
 template <int R>
 __device__ __forceinline__ void setmaxnreg_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(R));
@@ -204,8 +215,9 @@ __device__ __forceinline__ void setmaxnreg_dec() {
 constexpr int kThreads = 512;
 constexpr int kConsumerWarps = 12;
 constexpr int kProducerThreads = 128;
-constexpr int kConsumerRegs = 152;
-constexpr int kProducerRegs = 40;
+constexpr int kGatherThreads = 96;  // producer threads doing the A gather (warp 3 issues the B bulk copies)
+constexpr int kConsumerRegs = 160;
+constexpr int kProducerRegs = 32;
 
 template <int NT, int WN>
 struct ProjTile {
@@ -244,11 +256,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
   const int KT = (h_end - h_begin + kBK - 1) / kBK;
   const int m = p.m, N = p.N, NP = p.NP;
 
+  // zero the B planes of every slot once: padding columns [m, NP) are never written by the bulk
+  // copies, and rows past h_end of a partial last stage must not hold garbage (A is 0 there)
+  for (int s = 0; s < kStages; ++s)
+    for (int e = tid; e < kBK * (T::LDB * 2 + T::LDBS); e += kThreads) smem[s * T::STAGE + T::B_C + e] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full0 + 8u * s, kProducerThreads);
+      mbar_init(full0 + 8u * s, kGatherThreads + 1);  // A-gather cp.async arrivals + B expect_tx
       mbar_init(empty0 + 8u * s, kConsumerWarps);
     }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
@@ -256,40 +273,67 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
     // ================================================================== producer warpgroup
     setmaxnreg_dec<kProducerRegs>();
     const int pt = tid - kConsumerWarps * 32;  // 0..127
+    const int plane = pt & 31;
     const int32_t* __restrict__ ptab = p.ptab;
-    const double2* __restrict__ grid = p.grid;
-    const double* __restrict__ gsum = p.gsum;
-    const double2* __restrict__ V = p.V;
-    const double* __restrict__ vsum = p.vsum;
-    const int kb = p.kb[l], shift = p.shift[l];
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % kStages;
-      if (kt >= kStages) mbar_wait(empty0 + 8u * s, (uint32_t)((kt / kStages) - 1) & 1u);
-      const int h0 = h_begin + kt * kBK;
-      const uint32_t st = sbase + (uint32_t)(s * T::STAGE) * 8u;
-      // A gather: kBK x BM elements
-      for (int e = pt; e < kBK * BM; e += kProducerThreads) {
-        const int kc = e / BM, ra = e % BM;
-        const int h = h0 + kc;
-        const bool ok = (rb0 + ra < rows) && (h < h_end);
-        const int idx = ok ? __ldg(ptab + kb + rb0 + ra) + shift - __ldg(ptab + h) : 0;
-        cp_async16(st + (uint32_t)(T::A_C + 2 * (kc * T::LDA + ra)) * 8u, grid + idx, ok ? 16 : 0);
-        if constexpr (MODE == 3) cp_async8(st + (uint32_t)(T::A_S + kc * T::LDAS + ra) * 8u, gsum + idx, ok ? 8 : 0);
+    if (pt < kGatherThreads) {
+      // A gather: thread owns tile row ra and columns kc = kc0 + (kGatherThreads/BM) j
+      constexpr int CPT = kBK * BM / kGatherThreads;  // columns per thread
+      constexpr int KCS = kGatherThreads / BM;        // column stride
+      const int ra = pt % BM, kc0 = pt / BM;
+      const bool vr = rb0 + ra < rows;
+      const int PA = vr ? __ldg(ptab + p.kb[l] + rb0 + ra) + p.shift[l] : 0;
+      const double2* __restrict__ grid = p.grid;
+      const double* __restrict__ gsum = p.gsum;
+      // lane i < kBK holds P(h0 + i) of the stage being issued (prefetched one stage ahead)
+      int ph_next = (plane < kBK && h_begin + plane < N) ? __ldg(ptab + h_begin + plane) : 0;
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % kStages;
+        const int h0 = h_begin + kt * kBK;
+        const int ph = ph_next;
+        const int hn = h0 + kBK + plane;
+        ph_next = (plane < kBK && hn < N) ? __ldg(ptab + hn) : 0;
+        if (kt >= kStages) mbar_wait(empty0 + 8u * s, (uint32_t)((kt / kStages) - 1) & 1u);
+        const uint32_t st = sbase + (uint32_t)(s * T::STAGE) * 8u;
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+          const int kc = kc0 + KCS * j;
+          const int phc = __shfl_sync(0xffffffffu, ph, kc);
+          const bool ok = vr && (h0 + kc < h_end);
+          const int idx = ok ? PA - phc : 0;
+          cp_async16(st + (uint32_t)(T::A_C + 2 * (kc * T::LDA + ra)) * 8u, grid + idx, ok ? 16 : 0);
+          if constexpr (MODE == 3)
+            cp_async8(st + (uint32_t)(T::A_S + kc * T::LDAS + ra) * 8u, gsum + idx, ok ? 8 : 0);
+        }
+        mbar_arrive_cp_async(full0 + 8u * s);
       }
-      // B rows: kBK x NP elements
-      for (int e = pt; e < kBK * NP; e += kProducerThreads) {
-        const int kr = e / NP, col = e % NP;
-        const int h = h0 + kr;
-        const bool okh = h < h_end;
-        const bool ok = okh && (col < m);
-        cp_async16_cg(st + (uint32_t)(T::B_C + 2 * (kr * T::LDB + col)) * 8u, V + (ok ? h * m + col : 0),
-                      ok ? 16 : 0);
-        if constexpr (MODE == 3)
-          cp_async8(st + (uint32_t)(T::B_S + kr * T::LDBS + col) * 8u, vsum + (okh ? h * NP + col : 0), okh ? 8 : 0);
+      cp_async_wait<0>();
+    } else {
+      // B rows: one bulk copy per V row (lanes 0..15) and per Vsum row (lanes 16..31)
+      const int kr = plane & (kBK - 1);
+      const bool sum_plane = plane >= kBK;
+      const double2* __restrict__ V = p.V;
+      const double* __restrict__ vsum = p.vsum;
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % kStages;
+        const int h0 = h_begin + kt * kBK;
+        if (kt >= kStages) mbar_wait(empty0 + 8u * s, (uint32_t)((kt / kStages) - 1) & 1u);
+        const int nrows = min(kBK, h_end - h0);
+        const uint32_t bytes_row = (uint32_t)m * 16u + (MODE == 3 ? (uint32_t)NP * 8u : 0u);
+        if (plane == 0) mbar_arrive_expect_tx(full0 + 8u * s, bytes_row * (uint32_t)nrows);
+        __syncwarp();
+        const uint32_t st = sbase + (uint32_t)(s * T::STAGE) * 8u;
+        if (kr < nrows) {
+          const int h = h0 + kr;
+          if (!sum_plane) {
+            bulk_g2s(st + (uint32_t)(T::B_C + 2 * kr * T::LDB) * 8u, V + (size_t)h * m, (uint32_t)m * 16u,
+                     full0 + 8u * s);
+          } else if constexpr (MODE == 3) {
+            bulk_g2s(st + (uint32_t)(T::B_S + kr * T::LDBS) * 8u, vsum + (size_t)h * NP, (uint32_t)NP * 8u,
+                     full0 + 8u * s);
+          }
+        }
       }
-      mbar_arrive_cp_async(full0 + 8u * s);
     }
-    cp_async_wait<0>();
     return;
   }
 
