@@ -25,6 +25,26 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
+def build_variant(out_path: str, defines: list[str]) -> str:
+    """Build an experimental variant (extra -D flags) to `out_path` (A/B timing; not the product)."""
+    objs = []
+    for src in SOURCES:
+        obj = out_path + "." + src.replace(".cu", ".o")
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {src}")
+        objs.append(obj)
+    r = subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out_path, *objs,
+                        "-lcudart"], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    for o in objs:
+        os.remove(o)
+    return out_path
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB

@@ -11,7 +11,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libprony.so")
+LIB_PATH = os.environ.get("PRONY_LIB") or os.path.join(_HERE, "libprony.so")  # PRONY_LIB: A/B builds
 
 PRONY_OK = 0
 PRONY_ERR_INVALID = 1

@@ -216,8 +216,22 @@ constexpr int kThreads = 512;
 constexpr int kConsumerWarps = 12;
 constexpr int kProducerThreads = 128;
 constexpr int kGatherThreads = 96;  // producer threads doing the A gather (warp 3 issues the B bulk copies)
-constexpr int kConsumerRegs = 160;
-constexpr int kProducerRegs = 32;
+#ifndef PRONY_CONSUMER_REGS
+#define PRONY_CONSUMER_REGS 160
+#endif
+#ifndef PRONY_PRODUCER_REGS
+#define PRONY_PRODUCER_REGS 32
+#endif
+#ifndef PRONY_KK_UNROLL
+#define PRONY_KK_UNROLL 4
+#endif
+#ifndef PRONY_GATHER_UNROLL
+#define PRONY_GATHER_UNROLL 2
+#endif
+constexpr int kKkUnroll = PRONY_KK_UNROLL;
+constexpr int kGatherUnroll = PRONY_GATHER_UNROLL;
+constexpr int kConsumerRegs = PRONY_CONSUMER_REGS;  // 384 x 160 + 128 x 32 = 65536 registers
+constexpr int kProducerRegs = PRONY_PRODUCER_REGS;
 
 template <int NT, int WN>
 struct ProjTile {
@@ -294,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
         ph_next = (plane < kBK && hn < N) ? __ldg(ptab + hn) : 0;
         if (kt >= kStages) mbar_wait(empty0 + 8u * s, (uint32_t)((kt / kStages) - 1) & 1u);
         const uint32_t st = sbase + (uint32_t)(s * T::STAGE) * 8u;
-#pragma unroll
+#pragma unroll kGatherUnroll
         for (int j = 0; j < CPT; ++j) {
           const int kc = kc0 + KCS * j;
           const int phc = __shfl_sync(0xffffffffu, ph, kc);
@@ -365,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
         const double* As = st + T::A_S + wm * 16;
         const double2* Bc = reinterpret_cast<const double2*>(st + T::B_C) + t0 * 8;
         const double* Bs = st + T::B_S + t0 * 8;
-#pragma unroll
+#pragma unroll kKkUnroll
         for (int kk = 0; kk < kBK / 4; ++kk)
           warp_cmma_k4<NT, NA, MODE>(acc, Ac + kk * 4 * T::LDA, As + kk * 4 * T::LDAS, T::LDA, T::LDAS,
                                      Bc + kk * 4 * T::LDB, Bs + kk * 4 * T::LDBS, T::LDB, T::LDBS, g, q);
