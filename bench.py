@@ -335,6 +335,7 @@ def run_ours(args, cfg):
             except (OSError, ValueError):
                 traffic = None
         achieved = flops_proj / proj_avg_s / 1e12
+        cm = 1.0 if os.environ.get("PRONY_CMUL", "3m").startswith("4") else 0.75
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -350,6 +351,10 @@ def run_ours(args, cfg):
                          "traffic": traffic,
                          "peak_source": "cuBLAS ZGEMM 4096^3 complex128 measured in this run (MEASURED_PEAKS.json has no FP64 entry)",
                          "flops_per_launch": flops_proj, "avg_launch_ms": proj_avg_s * 1e3,
+                         # 3M executes 3 of 4 real products, on NP = 8 ceil(m/8) padded columns:
+                         "executed_tflops": achieved * cm * (8 * ((m + 7) // 8)) / m,
+                         "executed_frac": (achieved * cm * (8 * ((m + 7) // 8)) / m) / peak if peak else None,
+                         "cmul": "4M" if cm == 1.0 else "3M",
                          "share_of_step": sum(proj_ms) / sum(step_ms),
                          "grid": list(infos_p[0].main_grid), "split_k": infos_p[0].split_k},
             "kernels_ms": {"k_project": statistics.mean(proj_ms), "k_vls": statistics.mean(vls_ms)},

@@ -1,0 +1,86 @@
+"""Multi-GPU sharding host logic on CPU: world_size-2 gloo processes each compute their share of the
+pencil (unit range / column range) with the oracle, and sharding.allreduce_pencil (the same call the
+GPU path makes over NCCL) must reproduce the single-process pencil."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2012_11430_b200 import sharding  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, d, n, m, order, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import workload as W
+    prob = W.make_problem(W.custom_config(d, n, m, 1e-6, 97), with_svd=True)
+    u0, u1 = sharding.unit_range(d, n, world, rank)
+    c0, c1 = sharding.column_range(d, n, world, rank)
+    S = oracle.project_units(prob.grid, prob.U, prob.V, prob.sigma, d, n, u0, u1, order)
+    A = oracle.vandermonde(prob.z, d, n, c0, c1)
+    G, b = oracle.ls_products(A, prob.grid, d, n, c0, c1)
+    Sr, Gr, br = sharding.allreduce_pencil(torch.from_numpy(S), torch.from_numpy(G), torch.from_numpy(b))
+    if rank == 0:
+        np.savez(out_path, S=Sr.numpy(), G=Gr.numpy(), b=br.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("d,n,m,order", [(3, 4, 6, 1), (3, 4, 6, 0), (2, 9, 5, 1)])
+def test_allreduce_pencil_world2_gloo(tmp_path, oracle_mod, d, n, m, order):
+    import workload as W
+    out = str(tmp_path / "res.npz")
+    mp.spawn(_worker, args=(2, _free_port(), d, n, m, order, out), nprocs=2, join=True)
+    res = np.load(out)
+    prob = W.make_problem(W.custom_config(d, n, m, 1e-6, 97), with_svd=True)
+    S = oracle_mod.project(prob.grid, prob.U, prob.V, prob.sigma, d, n)
+    A = oracle_mod.vandermonde(prob.z, d, n)
+    G, b = oracle_mod.ls_products(A, prob.grid, d, n)
+    assert np.linalg.norm(res["S"] - S) / np.linalg.norm(S) < 1e-13
+    assert np.linalg.norm(res["G"] - G) / np.linalg.norm(G) < 1e-13
+    assert np.linalg.norm(res["b"] - b) / np.linalg.norm(b) < 1e-13
+
+
+@pytest.mark.parametrize("total,parts", [(0, 1), (10, 3), (80802, 8), (7, 8)])
+def test_split_range_partitions(total, parts):
+    ranges = [sharding.split_range(total, parts, i) for i in range(parts)]
+    assert ranges[0][0] == 0 and ranges[-1][1] == total
+    for (a, b), (c, _) in zip(ranges, ranges[1:]):
+        assert b == c and a <= b
+    sizes = [b - a for a, b in ranges]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def test_default_unit_order():
+    assert sharding.default_unit_order(3, 3) == 0   # l-sharding when ranks divide d
+    assert sharding.default_unit_order(2, 2) == 0
+    assert sharding.default_unit_order(3, 2) == 1   # row-major otherwise (cfg3 on 2/4 GPUs)
+    assert sharding.default_unit_order(2, 8) == 1
+    assert sharding.default_unit_order(2, 1) == 1
+
+
+def test_pack_unpack_roundtrip():
+    d, m = 3, 5
+    S = torch.randn(d, m, m, dtype=torch.complex128)
+    G = torch.randn(m, m, dtype=torch.complex128)
+    b = torch.randn(m, dtype=torch.complex128)
+    S2, G2, b2 = sharding.unpack(sharding.pack(S, G, b), d, m)
+    assert torch.equal(S, S2) and torch.equal(G, G2) and torch.equal(b, b2)

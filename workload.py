@@ -14,7 +14,7 @@ What it synthesizes (recipe also stated in DESIGN.md §3):
   last coordinate fastest
 * the paper's test family t_j(i) = ((i-1)m+j-1) 10^-ceil(log10(dm)), c_j = j+ij
                                                          (PAPER.md:577-580)
-* the rank-m SVD inputs U, V, Sigma of the NOISE-FREE T (reading R7): any
+* the rank-m SVD inputs U, V, Sigma of the NOISE-FREE T (reading R20): any
   valid reduced SVD is a legal input of eq_generateSl; the planted
   one is obtained without forming T from the factorization T = B diag(c) B^H with
   B[k,j] = exp(-2 pi i <t_j,k>) (a QR of B and an m x m SVD, numpy library calls).
