@@ -208,26 +208,23 @@ def run_ours(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # gloo: functional check of the N>1 path with several ranks on one GPU (no waiting kernels)
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
 
     prob = W.make_problem(cfg)
     c = prob.cfg
     d, n, m, N = c.d, c.n, c.m, c.N
-    order = sharding.default_unit_order(d, world)
-    u0, u1 = sharding.unit_range(d, n, world, rank)
-    c0, c1 = sharding.column_range(d, n, world, rank)
-
     tg = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     grid, U, V, sigma, z = tg(prob.grid), tg(prob.U), tg(prob.V), tg(prob.sigma), tg(prob.z)
-    ws_p = pb.alloc_workspace(pb.WS_PROJECT, d, n, m, dev)
-    ws_l = pb.alloc_workspace(pb.WS_LS, d, n, m, dev)
-    S = torch.empty((d, m, m), dtype=torch.complex128, device=dev)
-    G = torch.empty((m, m), dtype=torch.complex128, device=dev)
-    b = torch.empty(m, dtype=torch.complex128, device=dev)
-    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    pencil = sharding.DistributedPencil(d, n, m, dev, world, rank)
+    order = pencil.order
+    st = pencil.status
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -238,16 +235,7 @@ def run_ours(args, cfg):
         return evs
 
     def step(info_p=None, info_l=None):
-        pb.project(grid, U, V, sigma, d, n, m, u0, u1, order, out=S, workspace=ws_p, stream=stream, info=info_p)
-        full = world == 1
-        outs = {"G": G, "b": b}
-        res = pb.vandermonde_ls(z, grid, d, n, m, c0, c1, want_solution=full, out=outs, workspace=ws_l,
-                                dev_status=st, stream=stream, info=info_l)
-        if world > 1:
-            Sr, Gr, br = sharding.allreduce_pencil(S, G, b)
-            cc, tt = pb.ls_solve(Gr.contiguous(), br.contiguous(), z, d, m, dev_status=st, stream=stream)
-            return Sr, cc, tt
-        return S, res["c"], res["t"]
+        return pencil(grid, U, V, sigma, z, stream=stream, info_p=info_p, info_l=info_l)
 
     # warm-up (also validates the device status once)
     for _ in range(max(args.warmup, 0)):
@@ -288,19 +276,21 @@ def run_ours(args, cfg):
     total_ms_max = float(t[0])
     launches_per_step = infos_p[0].launches + infos_l[0].launches + (1 if world > 1 else 0)
 
-    # ---- end to end through the host-buffer C-ABI call (N = 1) / host-staged sharded path (N > 1)
-    e2e = None
+    # ---- end to end from pinned host buffers: N = 1 through the C-ABI host call prony_pencil_host;
+    # N > 1 through the sharded public API (pinned H2D of the inputs on every rank, the pencil, D2H of
+    # S, c, t on rank 0), the whole interval timed on the device (max over ranks)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    hg, hU, hV, hs, hz = pin(prob.grid), pin(prob.U), pin(prob.V), pin(prob.sigma), pin(prob.z)
+    h2d = sum(x.numel() * x.element_size() for x in (hg, hU, hV, hs, hz))
+    Ke = max(2, min(K, 5))
+    e_ms = []
     if world == 1:
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        hg, hU, hV, hs, hz = pin(prob.grid), pin(prob.U), pin(prob.V), pin(prob.sigma), pin(prob.z)
         outs = {k: torch.empty(s, dtype=dt).pin_memory() for k, s, dt in
                 [("S", (d, m, m), torch.complex128), ("G", (m, m), torch.complex128), ("b", (m,), torch.complex128),
                  ("c", (m,), torch.complex128), ("t", (m, d), torch.float64)]}
         ws_h = pb.alloc_workspace(pb.WS_PENCIL_HOST, d, n, m, dev)
         for _ in range(2):
             pb.pencil_host(hg, hU, hV, hs, hz, d, n, m, workspace=ws_h, outputs=outs, stream=stream)
-        Ke = max(2, min(K, 5))
-        e_ms = []
         for i in range(Ke):
             flush.fill_(i & 0xFF)
             torch.cuda.synchronize()
@@ -312,11 +302,45 @@ def run_ours(args, cfg):
             e1.synchronize()
             assert r["status"] == 0
             e_ms.append(e0.elapsed_time(e1))
-        h2d = sum(x.numel() * x.element_size() for x in (hg, hU, hV, hs, hz))
         d2h = sum(x.numel() * x.element_size() for x in outs.values() if isinstance(x, torch.Tensor)) + 4
-        e2e = {"value": Ke / (sum(e_ms) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": sum(e_ms) / Ke, "api": "prony_pencil_host (pinned host buffers)"}
+        api = "prony_pencil_host (C ABI, pinned host buffers)"
         del ws_h
+    else:
+        dg, dU, dV, ds, dz = (torch.empty_like(x, device=dev) for x in (hg, hU, hV, hs, hz))
+        hS = torch.empty((d, m, m), dtype=torch.complex128).pin_memory()
+        hc = torch.empty(m, dtype=torch.complex128).pin_memory()
+        ht = torch.empty((m, d), dtype=torch.float64).pin_memory()
+
+        def e2e_step():
+            for dst, src in ((dg, hg), (dU, hU), (dV, hV), (ds, hs), (dz, hz)):
+                dst.copy_(src, non_blocking=True)
+            Sx, cx, tx = pencil(dg, dU, dV, ds, dz, stream=stream)
+            if rank == 0:
+                hS.copy_(Sx, non_blocking=True)
+                hc.copy_(cx, non_blocking=True)
+                ht.copy_(tx, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        for i in range(Ke):
+            flush.fill_(i & 0xFF)
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_step()
+            e1.record(stream)
+            e1.synchronize()
+            e_ms.append(e0.elapsed_time(e1))
+        d2h = (hS.numel() + hc.numel()) * 16 + ht.numel() * 8
+        api = "sharding.DistributedPencil (pinned H2D per rank, all-reduce, D2H on rank 0)"
+    te = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": Ke / (float(te[0]) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+           "d2h_bytes_per_step": d2h, "ms_per_step": float(te[0]) / Ke, "api": api}
 
     # ---- roofline of the dominant kernel (k_project), measured live above
     flops_proj = infos_p[0].main_flops
@@ -324,7 +348,7 @@ def run_ours(args, cfg):
     peak = zgemm_peak_tflops(torch) if rank == 0 else None
 
     if rank == 0:
-        value = world * K / (total_ms_max * 1e-3)
+        value = K / (total_ms_max * 1e-3)   # one pencil per step, sharded over the ranks
         ms_per_step = total_ms_max / K
         F = pencil_flops(d, N, m)
         traffic = None
@@ -338,12 +362,13 @@ def run_ours(args, cfg):
         cm = 1.0 if os.environ.get("PRONY_CMUL", "3m").startswith("4") else 0.75
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded planted exponential sum, complex Gaussian noise 1e-6)",
             "config": {"workload": f"{c.name}: d={d} n={n} N={N} m={m} noise={c.noise} (BASELINE configs[3])",
                        "d": d, "n": n, "N": N, "m": m, "parallelism": f"dp{world} ({'l-major' if order == 0 else 'row-major'} units)",
                        "l2": "flushed (256 MiB write) before every timed step, outside the timed interval",
-                       "pencils_per_step": world},
+                       "pencils_per_step": 1, "comm": "1 x all_reduce(SUM) of packed [S,G,b] per step" if world > 1 else "none"},
             "tflops": F * value / 1e12,
             "pct_peak": (F * value / 1e12) / (peak * world) if peak else None,
             "roofline": {"bound": "tensor", "kernel": "k_project (complex FP64 DMMA, implicit Toeplitz gather)",
@@ -378,6 +403,7 @@ def main():
     ap.add_argument("--cfg", default="cfg4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -56,3 +56,40 @@ def allreduce_pencil(S: torch.Tensor, G: torch.Tensor, b: torch.Tensor, group=No
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(torch.view_as_real(buf), op=dist.ReduceOp.SUM, group=group)
     return unpack(buf, d, m)
+
+
+class DistributedPencil:
+    """One pencil sharded over the ranks of the default process group (strong scaling of a single
+    pencil): rank r computes the partial pencil of its unit range and the partial LS
+    products of its column range on its own GPU (libprony), one all_reduce(SUM) of the packed
+    [S, G, b] completes them on every rank, and prony_ls_solve gives c, t locally.
+    Workspaces and output buffers are allocated once (no allocation per call)."""
+
+    def __init__(self, d: int, n: int, m: int, device, world: int = 1, rank: int = 0, unit_order: int | None = None):
+        from . import binding as pb
+        self.pb = pb
+        self.d, self.n, self.m = d, n, m
+        self.world, self.rank = world, rank
+        self.order = default_unit_order(d, world) if unit_order is None else unit_order
+        self.u0, self.u1 = unit_range(d, n, world, rank)
+        self.c0, self.c1 = column_range(d, n, world, rank)
+        self.ws_p = pb.alloc_workspace(pb.WS_PROJECT, d, n, m, device)
+        self.ws_l = pb.alloc_workspace(pb.WS_LS, d, n, m, device)
+        self.S = torch.empty((d, m, m), dtype=torch.complex128, device=device)
+        self.G = torch.empty((m, m), dtype=torch.complex128, device=device)
+        self.b = torch.empty(m, dtype=torch.complex128, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def __call__(self, grid, U, V, sigma, z, stream=None, info_p=None, info_l=None):
+        pb, d, n, m = self.pb, self.d, self.n, self.m
+        pb.project(grid, U, V, sigma, d, n, m, self.u0, self.u1, self.order, out=self.S, workspace=self.ws_p,
+                   stream=stream, info=info_p)
+        full = self.world == 1
+        res = pb.vandermonde_ls(z, grid, d, n, m, self.c0, self.c1, want_solution=full,
+                                out={"G": self.G, "b": self.b}, workspace=self.ws_l, dev_status=self.status,
+                                stream=stream, info=info_l)
+        if full:
+            return self.S, res["c"], res["t"]
+        Sr, Gr, br = allreduce_pencil(self.S, self.G, self.b)
+        c, t = pb.ls_solve(Gr.contiguous(), br.contiguous(), z, d, m, dev_status=self.status, stream=stream)
+        return Sr, c, t
