@@ -192,7 +192,7 @@ int prony_vandermonde_ls_ex(int d, int n, int m, const prony_c128* z, const pron
  * non-null, t = (-arg z / 2 pi) mod 1 (R4), for G, b already summed over all
  * columns (e.g. after the all-reduce of per-rank prony_vandermonde_ls partials).
  *   G, b, z     device m x m, m, m x d prony_c128;  c device m prony_c128;  t nullable m x d doubles.
- *   workspace   >= prony_workspace_size(PRONY_WS_LS).
+ *   workspace   unused (nullable; the factor lives in shared memory), kept for ABI stability.
  *   dev_status  PRONY_ERR_SINGULAR if G is not Hermitian positive definite (c is then NaN).
  */
 int prony_ls_solve(int d, int m, const prony_c128* G, const prony_c128* b, const prony_c128* z, prony_c128* c,

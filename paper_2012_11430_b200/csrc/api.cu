@@ -206,11 +206,10 @@ int prony_ls_solve(int d, int m, const prony_c128* G, const prony_c128* b, const
                    double* t, void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream) {
   if (d < 1 || d > PRONY_MAX_D || m < 1) return PRONY_ERR_INVALID;
   if (m > PRONY_MAX_M) return PRONY_ERR_RANGE;
-  if (!G || !b || !z || !c || !workspace) return PRONY_ERR_INVALID;
-  if (!aligned16(G) || !aligned16(b) || !aligned16(z) || !aligned16(c) || (t && ((uintptr_t)t & 7u)) ||
-      ((uintptr_t)workspace & 255u))
+  (void)workspace_bytes;  // the solve keeps its factor in shared memory; no scratch is needed
+  if (!G || !b || !z || !c) return PRONY_ERR_INVALID;
+  if (!aligned16(G) || !aligned16(b) || !aligned16(z) || !aligned16(c) || (t && ((uintptr_t)t & 7u)))
     return PRONY_ERR_INVALID;
-  if (workspace_bytes < (size_t)m * m * sizeof(double2) + 256 + (size_t)m * sizeof(double2)) return PRONY_ERR_WORKSPACE;
   return ls_solve_launch(d, m, (const double2*)G, (const double2*)b, (const double2*)z, (double2*)c, t, workspace,
                          dev_status, (cudaStream_t)stream);
 }

@@ -2,15 +2,17 @@
 // normal equations of argmin ||A^T c - f||_2; R10), c = conj(G^-1 b), t.
 //
 //   k_powers     pw[l][j][a] = z_j(l)^a, a = 0..n, by repeated multiplication (R9)
-//   k_vls        per column block: A tile (m x 32) in smem from the power tables
-//                (A[j][k] = prod_l pw[l][j][k_l]), optional coalesced A write (HBM-bound),
-//                G_part += A_tile A_tile^H and b_part += A_tile conj(f_tile) (DFMA)
+//   k_vls        per column block (16 warps): A tile (m x 16 columns) built in shared memory from
+//                the power tables (A[j][k] = prod_l pw[l][j][k_l]), optional coalesced A write,
+//                G_part += A_tile conj(A_tile)^T on the DMMA warp engine (3M), b_part += A conj(f)
 //   k_ls_reduce  fixed-order sum of the partials -> G, b
-//   k_solve      one CTA: Cholesky G = L L^H, L y = b, L^H x = y, c = conj(x); t = (-arg z/2pi) mod 1
+//   k_solve      one CTA, factor resident in shared memory: right-looking Cholesky G = L L^H,
+//                L y = b, L^H x = y, c = conj(x); t = (-arg z / 2 pi) mod 1 (R4)
 #include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
+#include "engine.cuh"
 #include "vandermonde_ls.cuh"
 
 namespace prony {
@@ -28,43 +30,70 @@ __global__ void k_powers(int d, int n, int m, const double2* __restrict__ z, dou
   }
 }
 
-// grid (CB, ceil(m/64)); CTA cb handles columns [cbeg, cend) of I_n in tiles of kTile.
-__global__ void __launch_bounds__(256) k_vls(VlsParams p) {
-  __shared__ double2 As[kMaxM][kTile + 1];
-  __shared__ double2 Fs[kTile];
+// grid (CB, ceil(m/BI)); CTA (cb, ib) handles columns [cbeg, cend) of I_n in tiles of kTile and
+// rows i in [BI ib, BI ib + BI) of G. Shared memory (dynamic): At[kTile][cap] (A[j][k], double2),
+// Sp[kTile][cap] (Re+Im), Sm[kTile][cap] (Re-Im), Fs[kTile] (conj f). A operand rows i, B operand
+// conj(A) rows j (engine CONJB) -> G[i][j] = sum_k A[i][k] conj(A[j][k]).
+template <int NT, int WN>
+__global__ void __launch_bounds__(kVlsThreads, 1) k_vls(VlsParams p) {
+  constexpr int WM = (kVlsThreads / 32) / WN, BI = 16 * WM;
+  extern __shared__ __align__(16) double vsm[];
+  const int cap = p.cap;  // row capacity of the smem planes (>= every row read)
+  const int lda = cap + 2, lds = cap + 4;
+  double2* At = reinterpret_cast<double2*>(vsm);
+  double* Sp = vsm + 2 * kTile * lda;
+  double* Sm = Sp + kTile * lds;
+  double2* Fs = reinterpret_cast<double2*>(Sm + kTile * lds);
+
   const int cb = blockIdx.x;
-  const int i0 = blockIdx.y * 64;
-  const int tid = threadIdx.x, ti = tid >> 4, tj = tid & 15;
+  const int i0 = blockIdx.y * BI;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WM, wn = warp / WM;
+  const int g = lane >> 2, q = lane & 3;
   const int m = p.m, d = p.d, n = p.n;
+  const int ntot = (m + 7) / 8;
+  const int t0 = (ntot * wn) / WN;
+  const int nt_active = (ntot * (wn + 1)) / WN - t0;
+  const bool warp_rows = (i0 + wm * 16) < m;
   const int64_t W = p.col_end - p.col_begin;
   const int64_t cbeg = p.col_begin + W * cb / p.CB;
   const int64_t cend = p.col_begin + W * (cb + 1) / p.CB;
   const int L = 2 * n + 2;
-  double2 acc[4][8];
+
+  // rows >= m of the planes stay zero
+  for (int e = tid; e < kTile * lda; e += kVlsThreads) At[e] = make_double2(0.0, 0.0);
+  for (int e = tid; e < kTile * lds; e += kVlsThreads) Sp[e] = Sm[e] = 0.0;
+
+  double acc[3][NT][4];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[a][j][e] = 0.0;
   double2 bacc = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = make_double2(0.0, 0.0);
+  __syncthreads();
 
   for (int64_t c0 = cbeg; c0 < cend; c0 += kTile) {
-    // A tile: As[j][kk] = prod_l pw[l][j][k_l], k = c0 + kk
-    for (int e = tid; e < m * kTile; e += 256) {
+    // A tile: A[j][k] = prod_l pw[l][j][k_l], k = c0 + kk, product in order l = 1..d (R9)
+    for (int e = tid; e < m * kTile; e += kVlsThreads) {
       const int j = e / kTile, kk = e % kTile;
       const int64_t k = c0 + kk;
       double2 a = make_double2(0.0, 0.0);
       if (k < cend) {
-        int digit[PRONY_MAX_D];
+        int dig[PRONY_MAX_D];
         int64_t r = k;
-        for (int l = d - 1; l >= 0; --l) {
-          digit[l] = (int)(r % (n + 1));
+        for (int l = d - 1; l >= 0; --l) {  // digits of k, last coordinate fastest
+          dig[l] = (int)(r % (n + 1));
           r /= (n + 1);
         }
-        a = p.pw[((size_t)0 * m + j) * (n + 1) + digit[0]];
-        for (int l = 1; l < d; ++l) a = cmul(a, p.pw[((size_t)l * m + j) * (n + 1) + digit[l]]);
+        a = p.pw[(size_t)j * (n + 1) + dig[0]];
+        for (int l = 1; l < d; ++l) a = cmul(a, p.pw[((size_t)l * m + j) * (n + 1) + dig[l]]);
         if (p.A && blockIdx.y == 0) p.A[(size_t)j * W + (k - p.col_begin)] = a;
       }
-      As[j][kk] = a;
+      At[kk * lda + j] = a;
+      Sp[kk * lds + j] = a.x + a.y;
+      Sm[kk * lds + j] = a.x - a.y;
     }
     if (tid < kTile) {
       const int64_t k = c0 + tid;
@@ -81,33 +110,18 @@ __global__ void __launch_bounds__(256) k_vls(VlsParams p) {
       Fs[tid] = f;
     }
     __syncthreads();
-#pragma unroll 4
-    for (int kk = 0; kk < kTile; ++kk) {
-      double2 u[4], v[8];
+    if (warp_rows) {
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int i = i0 + ti + 16 * a;
-        u[a] = i < m ? As[i][kk] : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const int j = tj + 16 * b;
-        v[b] = j < m ? cconj(As[j][kk]) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          acc[a][b].x = fma(u[a].x, v[b].x, acc[a][b].x);
-          acc[a][b].x = fma(-u[a].y, v[b].y, acc[a][b].x);
-          acc[a][b].y = fma(u[a].x, v[b].y, acc[a][b].y);
-          acc[a][b].y = fma(u[a].y, v[b].x, acc[a][b].y);
-        }
+      for (int kk = 0; kk < kTile / 4; ++kk)
+        warp_cmma_k4_n<NT, 3, true>(nt_active, acc, At + kk * 4 * lda + i0 + wm * 16,
+                                    Sp + kk * 4 * lds + i0 + wm * 16, lda, lds, At + kk * 4 * lda + t0 * 8,
+                                    Sm + kk * 4 * lds + t0 * 8, lda, lds, g, q);
     }
-    if (tid < 64 && i0 + tid < m) {
+    if (tid < BI && i0 + tid < m) {
       const int i = i0 + tid;
+#pragma unroll 4
       for (int kk = 0; kk < kTile; ++kk) {
-        const double2 a = As[i][kk], f = Fs[kk];
+        const double2 a = At[kk * lda + i], f = Fs[kk];
         bacc.x = fma(a.x, f.x, bacc.x);
         bacc.x = fma(-a.y, f.y, bacc.x);
         bacc.y = fma(a.x, f.y, bacc.y);
@@ -117,17 +131,24 @@ __global__ void __launch_bounds__(256) k_vls(VlsParams p) {
     __syncthreads();
   }
   double2* G = p.Gpart + (size_t)cb * m * m;
+  const int ia = i0 + wm * 16 + g, ib = ia + 8;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int i = i0 + ti + 16 * a;
-    if (i >= m) continue;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const int j = tj + 16 * b;
-      if (j < m) G[(size_t)i * m + j] = acc[a][b];
+  for (int j = 0; j < NT; ++j) {
+    if (j < nt_active) {
+      double re[4], im[4];
+      acc_to_complex<NT, 3>(acc, j, re, im);
+      const int col = (t0 + j) * 8 + 2 * q;
+      if (ia < m) {
+        if (col < m) G[(size_t)ia * m + col] = make_double2(re[0], im[0]);
+        if (col + 1 < m) G[(size_t)ia * m + col + 1] = make_double2(re[1], im[1]);
+      }
+      if (ib < m) {
+        if (col < m) G[(size_t)ib * m + col] = make_double2(re[2], im[2]);
+        if (col + 1 < m) G[(size_t)ib * m + col + 1] = make_double2(re[3], im[3]);
+      }
     }
   }
-  if (tid < 64 && i0 + tid < m) p.bpart[(size_t)cb * m + i0 + tid] = bacc;
+  if (tid < BI && i0 + tid < m) p.bpart[(size_t)cb * m + i0 + tid] = bacc;
 }
 
 __global__ void k_ls_reduce(int m, int CB, const double2* __restrict__ Gpart, const double2* __restrict__ bpart,
@@ -146,90 +167,91 @@ __global__ void k_ls_reduce(int m, int CB, const double2* __restrict__ Gpart, co
   }
 }
 
-// One CTA (256 threads). Lw: m x m scratch (lower Cholesky factor), y: m scratch.
-__global__ void __launch_bounds__(256) k_solve(int d, int m, const double2* __restrict__ G,
-                                               const double2* __restrict__ b, const double2* __restrict__ z,
-                                               double2* __restrict__ Lw, double2* __restrict__ y,
-                                               double2* __restrict__ c, double* __restrict__ t, int32_t* status) {
+// One CTA of kSolveThreads. The lower triangle of G lives packed in shared memory (L[i][k] at
+// i(i+1)/2 + k); right-looking Cholesky (column j: pivot, scale the column, rank-1 update of the
+// trailing triangle), then column-oriented forward / backward substitution.
+__global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const double2* __restrict__ G,
+                                                         const double2* __restrict__ b,
+                                                         const double2* __restrict__ z, double2* __restrict__ c,
+                                                         double* __restrict__ t, int32_t* status) {
+  extern __shared__ __align__(16) double2 Ls[];  // m(m+1)/2 packed + y[m]
+  double2* y = Ls + (size_t)m * (m + 1) / 2;
   __shared__ int bad;
-  __shared__ double ljj_s;
   const int tid = threadIdx.x;
+  auto at = [](int i, int k) { return i * (i + 1) / 2 + k; };
   if (tid == 0) bad = 0;
-  for (int e = tid; e < m * m; e += blockDim.x) Lw[e] = G[e];
+  for (int i = tid; i < m; i += kSolveThreads) {
+    for (int k = 0; k <= i; ++k) Ls[at(i, k)] = G[(size_t)i * m + k];
+    y[i] = b[i];
+  }
   __syncthreads();
-  // left-looking Cholesky, column j: L[j][j] = sqrt(G[j][j] - sum_p |L[j][p]|^2),
-  // L[i][j] = (G[i][j] - sum_{p<j} L[i][p] conj(L[j][p])) / L[j][j]   (i > j)
   for (int j = 0; j < m; ++j) {
-    if (tid == 0) {
-      double djj = Lw[(size_t)j * m + j].x;
-      for (int q = 0; q < j; ++q) {
-        const double2 v = Lw[(size_t)j * m + q];
-        djj -= v.x * v.x + v.y * v.y;
-      }
-      if (!(djj > 0.0)) bad = 1;
-      ljj_s = bad ? 1.0 : sqrt(djj);
-      Lw[(size_t)j * m + j] = make_double2(ljj_s, 0.0);
+    const double djj = Ls[at(j, j)].x;
+    if (!(djj > 0.0)) {  // uniform branch: every thread read the same value
+      if (tid == 0) bad = 1;
+      break;
+    }
+    const double ljj = sqrt(djj);
+    const double inv = 1.0 / ljj;
+    __syncthreads();
+    if (tid == 0) Ls[at(j, j)] = make_double2(ljj, 0.0);
+    for (int i = j + 1 + tid; i < m; i += kSolveThreads) {
+      const double2 v = Ls[at(i, j)];
+      Ls[at(i, j)] = make_double2(v.x * inv, v.y * inv);
     }
     __syncthreads();
-    const double ljj = ljj_s;
-    for (int i = j + 1 + tid; i < m; i += blockDim.x) {
-      double2 s = Lw[(size_t)i * m + j];
-      for (int q = 0; q < j; ++q) {
-        const double2 a = Lw[(size_t)i * m + q], bb = cconj(Lw[(size_t)j * m + q]);
-        s.x -= a.x * bb.x - a.y * bb.y;
-        s.y -= a.x * bb.y + a.y * bb.x;
+    // trailing update: L[i][k] -= L[i][j] conj(L[k][j]), j < k <= i
+    const int r = m - j - 1;
+    for (int ii = tid / 8; ii < r; ii += kSolveThreads / 8) {
+      const int i = j + 1 + ii;
+      const double2 a = Ls[at(i, j)];
+      for (int kk = tid % 8; kk <= ii; kk += 8) {
+        const int k = j + 1 + kk;
+        const double2 bb = Ls[at(k, j)];
+        double2 v = Ls[at(i, k)];
+        v.x -= a.x * bb.x + a.y * bb.y;  // a conj(bb)
+        v.y -= a.y * bb.x - a.x * bb.y;
+        Ls[at(i, k)] = v;
       }
-      Lw[(size_t)i * m + j] = make_double2(s.x / ljj, s.y / ljj);
     }
     __syncthreads();
   }
+  __syncthreads();
   if (bad) {
     if (tid == 0) set_status(status, PRONY_ERR_SINGULAR);
-    for (int i = tid; i < m; i += blockDim.x) c[i] = make_double2(NAN, NAN);
-  } else if (tid < 32) {
-    // forward: L y = b ; backward: L^H x = y  (one warp, lane-parallel dot products)
-    const int lane = tid;
-    for (int i = 0; i < m; ++i) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int q = lane; q < i; q += 32) {
-        const double2 a = Lw[(size_t)i * m + q], v = y[q];
-        s.x += a.x * v.x - a.y * v.y;
-        s.y += a.x * v.y + a.y * v.x;
+    for (int i = tid; i < m; i += kSolveThreads) c[i] = make_double2(NAN, NAN);
+  } else {
+    // forward: L y = b (column oriented)
+    for (int j = 0; j < m; ++j) {
+      const double ljj = Ls[at(j, j)].x;
+      const double2 yj = make_double2(y[j].x / ljj, y[j].y / ljj);
+      __syncthreads();
+      if (tid == 0) y[j] = yj;
+      for (int i = j + 1 + tid; i < m; i += kSolveThreads) {
+        const double2 a = Ls[at(i, j)];
+        y[i].x -= a.x * yj.x - a.y * yj.y;
+        y[i].y -= a.x * yj.y + a.y * yj.x;
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
-      }
-      if (lane == 0) {
-        const double2 bi = b[i];
-        const double lii = Lw[(size_t)i * m + i].x;
-        y[i] = make_double2((bi.x - s.x) / lii, (bi.y - s.y) / lii);
-      }
-      __syncwarp();
+      __syncthreads();
     }
-    for (int i = m - 1; i >= 0; --i) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int q = i + 1 + lane; q < m; q += 32) {
-        const double2 a = cconj(Lw[(size_t)q * m + i]), v = y[q];
-        s.x += a.x * v.x - a.y * v.y;
-        s.y += a.x * v.y + a.y * v.x;
+    // backward: L^H x = y, x overwrites y (column j of L^H is the conjugated row j of L)
+    for (int j = m - 1; j >= 0; --j) {
+      const double ljj = Ls[at(j, j)].x;
+      const double2 xj = make_double2(y[j].x / ljj, y[j].y / ljj);
+      __syncthreads();
+      if (tid == 0) y[j] = xj;
+      for (int i = tid; i < j; i += kSolveThreads) {
+        const double2 a = cconj(Ls[at(j, i)]);
+        y[i].x -= a.x * xj.x - a.y * xj.y;
+        y[i].y -= a.x * xj.y + a.y * xj.x;
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
-      }
-      if (lane == 0) {
-        const double2 yi = y[i];
-        const double lii = Lw[(size_t)i * m + i].x;
-        y[i] = make_double2((yi.x - s.x) / lii, (yi.y - s.y) / lii);
-      }
-      __syncwarp();
+      __syncthreads();
     }
-    for (int i = lane; i < m; i += 32) c[i] = cconj(y[i]);
+    for (int i = tid; i < m; i += kSolveThreads) c[i] = cconj(y[i]);
   }
   if (t) {
     const double inv2pi = 0.15915494309189533577;  // 1 / (2 pi)
-    for (int e = tid; e < m * d; e += blockDim.x) {
+    for (int e = tid; e < m * d; e += kSolveThreads) {
       const double2 zz = z[e];
       double v = -atan2(zz.y, zz.x) * inv2pi;  // (-arg z / 2 pi) mod 1  (R4)
       v = v - floor(v);
@@ -240,23 +262,61 @@ __global__ void __launch_bounds__(256) k_solve(int d, int m, const double2* __re
 }
 
 // ---------------------------------------------------------------------------- host side
-static int vls_cb(int64_t W, int m, int sm_count) {
-  const int ib = (m + 63) / 64;
-  int64_t tiles = (W + kTile - 1) / kTile;
-  int64_t cb = (2 * (int64_t)sm_count) / ib;
+namespace {
+struct VlsShape {
+  int NT, WN, BI, cap;
+};
+VlsShape vls_shape(int m) {
+  VlsShape s;
+  const int ntot = (m + 7) / 8;
+  s.WN = ntot <= 8 ? 2 : 4;
+  s.NT = (ntot + s.WN - 1) / s.WN;
+  s.BI = 16 * ((kVlsThreads / 32) / s.WN);
+  const int rows_a = (m + s.BI - 1) / s.BI * s.BI;  // A-operand rows read (whole i-blocks)
+  const int rows_b = 8 * s.NT * s.WN;              // B-operand rows read
+  s.cap = std::max(rows_a, rows_b);
+  return s;
+}
+size_t vls_smem(int cap) {
+  const int lda = cap + 2, lds = cap + 4;
+  return (size_t)(2 * kTile * lda + 2 * kTile * lds) * sizeof(double) + kTile * sizeof(double2);
+}
+int vls_cb(int64_t W, int m, int sm_count) {
+  const VlsShape s = vls_shape(m);
+  const int ib = (m + s.BI - 1) / s.BI;
+  const int64_t tiles = (W + kTile - 1) / kTile;
+  int64_t cb = std::max<int64_t>(1, sm_count / ib);
   cb = std::max<int64_t>(1, std::min<int64_t>(cb, tiles));
   return (int)cb;
 }
+size_t solve_smem(int m) { return ((size_t)m * (m + 1) / 2 + m) * sizeof(double2); }
+}  // namespace
 
 size_t ls_workspace_bytes(int d, int n, int m, int sm_count) {
   size_t bytes = align_up((size_t)d * m * (n + 1) * sizeof(double2), 256);  // power tables
-  const int ib = (m + 63) / 64;
-  const int cbmax = std::max(1, (2 * sm_count) / ib);
+  const int cbmax = std::max(1, sm_count);
   bytes += align_up((size_t)cbmax * m * m * sizeof(double2), 256);  // G partials
   bytes += align_up((size_t)cbmax * m * sizeof(double2), 256);      // b partials
-  bytes += align_up((size_t)m * m * sizeof(double2), 256);          // Cholesky factor
-  bytes += align_up((size_t)m * sizeof(double2), 256);              // y
   return bytes;
+}
+
+template <int NT, int WN>
+static int launch_vls_t(const VlsParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+  if (cudaFuncSetAttribute(k_vls<NT, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return PRONY_ERR_CUDA;
+  k_vls<NT, WN><<<grid, kVlsThreads, smem, st>>>(p);
+  return PRONY_OK;
+}
+
+int ls_solve_launch(int d, int m, const double2* G, const double2* b, const double2* z, double2* c, double* t,
+                    void* ws, int32_t* status, cudaStream_t st) {
+  (void)ws;
+  const size_t smem = solve_smem(m);
+  if (cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return PRONY_ERR_CUDA;
+  k_solve<<<1, kSolveThreads, smem, st>>>(d, m, G, b, z, c, t, status);
+  if (cudaGetLastError() != cudaSuccess) return PRONY_ERR_CUDA;
+  return PRONY_OK;
 }
 
 int ls_launch(int d, int n, int m, int N, const double2* z, const double2* grid, int64_t col_begin, int64_t col_end,
@@ -265,15 +325,10 @@ int ls_launch(int d, int n, int m, int N, const double2* z, const double2* grid,
   char* w = (char*)ws;
   double2* pw = (double2*)w;
   w += align_up((size_t)d * m * (n + 1) * sizeof(double2), 256);
-  const int ib = (m + 63) / 64;
-  const int cbmax = std::max(1, (2 * sm_count) / ib);
+  const int cbmax = std::max(1, sm_count);
   double2* Gpart = (double2*)w;
   w += align_up((size_t)cbmax * m * m * sizeof(double2), 256);
   double2* bpart = (double2*)w;
-  w += align_up((size_t)cbmax * m * sizeof(double2), 256);
-  double2* Lw = (double2*)w;
-  w += align_up((size_t)m * m * sizeof(double2), 256);
-  double2* yv = (double2*)w;
 
   const int64_t W = col_end - col_begin;
   if (info) {
@@ -289,6 +344,7 @@ int ls_launch(int d, int n, int m, int N, const double2* z, const double2* grid,
     return PRONY_OK;
   }
   k_powers<<<(d * m + 127) / 128, 128, 0, st>>>(d, n, m, z, pw);
+  const VlsShape sh = vls_shape(m);
   VlsParams p{};
   p.d = d;
   p.n = n;
@@ -296,20 +352,35 @@ int ls_launch(int d, int n, int m, int N, const double2* z, const double2* grid,
   p.col_begin = col_begin;
   p.col_end = col_end;
   p.CB = vls_cb(W, m, sm_count);
+  p.cap = sh.cap;
   p.pw = pw;
   p.grid = grid;
   p.A = A;
   p.Gpart = Gpart;
   p.bpart = bpart;
+  const int ib = (m + sh.BI - 1) / sh.BI;
+  const dim3 vgrid(p.CB, ib);
+  const size_t smem = vls_smem(sh.cap);
   if (info && info->ev_main_begin) cudaEventRecord((cudaEvent_t)info->ev_main_begin, st);
-  k_vls<<<dim3(p.CB, ib), 256, 0, st>>>(p);
+  int rc = PRONY_OK;
+  switch (sh.WN * 16 + sh.NT) {
+#define PRONY_VCASE(nt, wn) \
+  case wn * 16 + nt:        \
+    rc = launch_vls_t<nt, wn>(p, vgrid, smem, st); \
+    break;
+    PRONY_VCASE(1, 2) PRONY_VCASE(2, 2) PRONY_VCASE(3, 2) PRONY_VCASE(4, 2) PRONY_VCASE(3, 4) PRONY_VCASE(4, 4)
+#undef PRONY_VCASE
+    default:
+      return PRONY_ERR_RANGE;
+  }
+  if (rc != PRONY_OK) return rc;
   if (info && info->ev_main_end) cudaEventRecord((cudaEvent_t)info->ev_main_end, st);
   int launches = 3;
   k_ls_reduce<<<(m * m + m + 255) / 256, 256, 0, st>>>(m, p.CB, Gpart, bpart, G, b);
   if (col_begin == 0 && col_end == N && (c || t)) {
-    double2* cc = c ? c : yv;  // c is required by the solve; if only t is wanted, solve into scratch
-    if (c) k_solve<<<1, 256, 0, st>>>(d, m, G, b, z, Lw, yv, cc, t, status);
-    else k_solve<<<1, 256, 0, st>>>(d, m, G, b, z, Lw, yv, Lw, t, status);
+    // only t requested: solve into the (now consumed) G partial buffer
+    rc = ls_solve_launch(d, m, G, b, z, c ? c : Gpart, t, nullptr, status, st);
+    if (rc != PRONY_OK) return rc;
     ++launches;
   }
   if (info) {
@@ -317,19 +388,10 @@ int ls_launch(int d, int n, int m, int N, const double2* z, const double2* grid,
     info->main_grid[0] = p.CB;
     info->main_grid[1] = ib;
     info->main_grid[2] = 1;
-    info->main_block = 256;
+    info->main_block = kVlsThreads;
     info->split_k = p.CB;
     info->main_flops = 8.0 * m * (double)m * (double)W + 8.0 * m * (double)W;
   }
-  if (cudaGetLastError() != cudaSuccess) return PRONY_ERR_CUDA;
-  return PRONY_OK;
-}
-
-int ls_solve_launch(int d, int m, const double2* G, const double2* b, const double2* z, double2* c, double* t,
-                    void* ws, int32_t* status, cudaStream_t st) {
-  double2* Lw = (double2*)ws;
-  double2* yv = (double2*)((char*)ws + align_up((size_t)m * m * sizeof(double2), 256));
-  k_solve<<<1, 256, 0, st>>>(d, m, G, b, z, Lw, yv, c, t, status);
   if (cudaGetLastError() != cudaSuccess) return PRONY_ERR_CUDA;
   return PRONY_OK;
 }

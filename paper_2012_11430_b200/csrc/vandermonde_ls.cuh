@@ -9,10 +9,12 @@
 namespace prony {
 
 constexpr int kMaxM = PRONY_MAX_M;
-constexpr int kTile = 16;  // columns of A per smem tile
+constexpr int kTile = 16;          // columns of A per smem tile of k_vls
+constexpr int kVlsThreads = 512;   // 16 warps (DMMA warp engine)
+constexpr int kSolveThreads = 512;
 
 struct VlsParams {
-  int d, n, m, CB;
+  int d, n, m, CB, cap;
   int64_t col_begin, col_end;
   const double2* pw;
   const double2* grid;
