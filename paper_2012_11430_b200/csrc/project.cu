@@ -75,15 +75,19 @@ __global__ void k_prep(int d, int n, int N, int m, int NP, int64_t box, const do
 //   B planes  Bc[kc][c] = V[h0+kc][c], Bs[kc][c] = Vsum[h0+kc][c] (zero-filled for c >= m, h >= h_end)
 // CTA tile: BM = 16*WM rows of T_l x NP = 8*ceil(m/8) columns of V (n-tiles split near-evenly
 // over the WN column warps, <= NT <= 4 each).
-constexpr int kThreads = 512;
-constexpr int kConsumerWarps = 12;
+#ifndef PRONY_CONSUMER_WARPS
+#define PRONY_CONSUMER_WARPS 12
+#endif
+constexpr int kConsumerWarps = PRONY_CONSUMER_WARPS;    // 12 (3 warpgroups) or 8 (2 warpgroups)
+constexpr int kThreads = 32 * (kConsumerWarps + 4);     // + the producer warpgroup
+constexpr int kReduceThreads = 512;
 constexpr int kProducerThreads = 128;
 constexpr int kGatherThreads = 96;  // producer threads doing the A gather (warp 3 issues the B bulk copies)
 #ifndef PRONY_CONSUMER_REGS
-#define PRONY_CONSUMER_REGS 160
+#define PRONY_CONSUMER_REGS (PRONY_CONSUMER_WARPS == 12 ? 160 : 232)
 #endif
 #ifndef PRONY_PRODUCER_REGS
-#define PRONY_PRODUCER_REGS 32
+#define PRONY_PRODUCER_REGS (PRONY_CONSUMER_WARPS == 12 ? 32 : 40)
 #endif
 #ifndef PRONY_KK_UNROLL
 #define PRONY_KK_UNROLL 4
@@ -93,8 +97,14 @@ constexpr int kGatherThreads = 96;  // producer threads doing the A gather (warp
 #endif
 constexpr int kKkUnroll = PRONY_KK_UNROLL;
 constexpr int kGatherUnroll = PRONY_GATHER_UNROLL;
-constexpr int kConsumerRegs = PRONY_CONSUMER_REGS;  // 384 x 160 + 128 x 32 = 65536 registers
+constexpr int kConsumerRegs = PRONY_CONSUMER_REGS;  // 384 x 160 + 128 x 32 = 65536 (12 warps); 256 x 240 + 4096 (8)
 constexpr int kProducerRegs = PRONY_PRODUCER_REGS;
+// setmaxnreg only redistributes the CTA's launch-time register pool (kThreads x the per-thread count
+// ptxas assigns under __launch_bounds__(kThreads, 1), a multiple of 8): the split must fit in it or
+// the consumers' allocation never succeeds
+constexpr int kLaunchRegs = (65536 / kThreads) / 8 * 8 > 255 ? 255 : (65536 / kThreads) / 8 * 8;
+static_assert(kConsumerRegs * 32 * kConsumerWarps + kProducerRegs * 128 <= kLaunchRegs * kThreads,
+              "setmaxnreg split exceeds the CTA register pool");
 
 template <int NT, int WN>
 struct ProjTile {
@@ -109,7 +119,8 @@ struct ProjTile {
   static constexpr int B_S = B_C + kBK * LDB * 2;
   static constexpr int STAGE = B_S + kBK * LDBS;
   static constexpr int BAR = kStages * STAGE;        // mbarriers after the stages (2 per stage)
-  static constexpr size_t SMEM = (size_t)(BAR + 2 * kStages) * sizeof(double);
+  static constexpr int PAT = BAR + 2 * kStages;      // row table P(k_r) + s_l + C0 (BM ints)
+  static constexpr size_t SMEM = (size_t)PAT * sizeof(double) + (size_t)BM * sizeof(int);
   static_assert(STAGE % 2 == 0, "stage must keep 16-byte alignment");
 };
 
@@ -137,6 +148,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
   // copies, and rows past h_end of a partial last stage must not hold garbage (A is 0 there)
   for (int s = 0; s < kStages; ++s)
     for (int e = tid; e < kBK * (T::LDB * 2 + T::LDBS); e += kThreads) smem[s * T::STAGE + T::B_C + e] = 0.0;
+  int* sPA = reinterpret_cast<int*>(smem + T::PAT);
+  for (int r = tid; r < BM; r += kThreads)
+    sPA[r] = (rb0 + r < rows) ? p.ptab[p.kb[l] + rb0 + r] + p.shift[l] : -1;  // -1: row outside
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full0 + 8u * s, kGatherThreads + 1);  // A-gather cp.async arrivals + B expect_tx
@@ -153,12 +167,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
     const int plane = pt & 31;
     const int32_t* __restrict__ ptab = p.ptab;
     if (pt < kGatherThreads) {
-      // A gather: thread owns tile row ra and columns kc = kc0 + (kGatherThreads/BM) j
-      constexpr int CPT = kBK * BM / kGatherThreads;  // columns per thread
-      constexpr int KCS = kGatherThreads / BM;        // column stride
-      const int ra = pt % BM, kc0 = pt / BM;
-      const bool vr = rb0 + ra < rows;
-      const int PA = vr ? __ldg(ptab + p.kb[l] + rb0 + ra) + p.shift[l] : 0;
+      // A gather over the kBK x BM tile: element e = pt + kGatherThreads * j -> (kc = e / BM, ra = e % BM);
+      // P(k_ra) + shift comes from the shared row table sPA, P(h0 + kc) from lane kc (shfl)
       const double2* __restrict__ grid = p.grid;
       const double* __restrict__ gsum = p.gsum;
       // lane i < kBK holds P(h0 + i) of the stage being issued (prefetched one stage ahead)
@@ -172,11 +182,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
         if (kt >= kStages) mbar_wait(empty0 + 8u * s, (uint32_t)((kt / kStages) - 1) & 1u);
         const uint32_t st = sbase + (uint32_t)(s * T::STAGE) * 8u;
 #pragma unroll kGatherUnroll
-        for (int j = 0; j < CPT; ++j) {
-          const int kc = kc0 + KCS * j;
+        for (int e = pt; e < kBK * BM; e += kGatherThreads) {
+          const int kc = e / BM, ra = e % BM;
           const int phc = __shfl_sync(0xffffffffu, ph, kc);
-          const bool ok = vr && (h0 + kc < h_end);
-          const int idx = ok ? PA - phc : 0;
+          const int pa = sPA[ra];
+          const bool ok = (pa >= 0) && (h0 + kc < h_end);
+          const int idx = ok ? pa - phc : 0;
           cp_async16(st + (uint32_t)(T::A_C + 2 * (kc * T::LDA + ra)) * 8u, grid + idx, ok ? 16 : 0);
           if constexpr (MODE == 3)
             cp_async8(st + (uint32_t)(T::A_S + kc * T::LDAS + ra) * 8u, gsum + idx, ok ? 8 : 0);
@@ -297,8 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
 // (conj, conj-sum), B = sum_c Y_c staged as [k][j] planes; 8 rows k per slab, register-prefetched
 // one slab ahead.
 template <int NT, int WN, int MODE>
-__global__ void __launch_bounds__(kThreads, 1) k_reduce(RedParams p) {
-  constexpr int WM = (kThreads / 32) / WN, BI = 16 * WM, NPMAX = 8 * NT * WN;
+__global__ void __launch_bounds__(kReduceThreads, 1) k_reduce(RedParams p) {
+  constexpr int WM = (kReduceThreads / 32) / WN, BI = 16 * WM, NPMAX = 8 * NT * WN;
   constexpr int LDA = BI + 2, LDAS = BI + 4, LDB = NPMAX + 2, LDBS = NPMAX + 4;
   constexpr int SL = 8;  // rows k per slab
   __shared__ __align__(16) double2 Ac[SL * LDA];
@@ -327,13 +338,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_reduce(RedParams p) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[a][j][e] = 0.0;
 
-  constexpr int NU = (SL * BI + kThreads - 1) / kThreads;
-  constexpr int NY = (SL * NPMAX + kThreads - 1) / kThreads;
+  constexpr int NU = (SL * BI + kReduceThreads - 1) / kReduceThreads;
+  constexpr int NY = (SL * NPMAX + kReduceThreads - 1) / kReduceThreads;
   double2 ru[NU], ry[NY];
   auto load_slab = [&](int s) {
 #pragma unroll
     for (int x = 0; x < NU; ++x) {
-      const int e = tid + kThreads * x;
+      const int e = tid + kReduceThreads * x;
       const int r = e / BI, ii = e % BI;
       const int row = s + r, i = i0 + ii;
       ru[x] = (e < SL * BI && row < rend && i < m) ? ldg2(p.U + (size_t)(p.kb[l] + row) * m + i)
@@ -341,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_reduce(RedParams p) {
     }
 #pragma unroll
     for (int y = 0; y < NY; ++y) {
-      const int e = tid + kThreads * y;
+      const int e = tid + kReduceThreads * y;
       double2 a2 = make_double2(0.0, 0.0);
       if (e < SL * NP) {
         const int r = e / NP, jj = e % NP;
@@ -361,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_reduce(RedParams p) {
   for (int s = rbeg; s < rend; s += SL) {
 #pragma unroll
     for (int x = 0; x < NU; ++x) {
-      const int e = tid + kThreads * x;
+      const int e = tid + kReduceThreads * x;
       if (e < SL * BI) {
         const int r = e / BI, ii = e % BI;
         const double2 u = make_double2(ru[x].x, -ru[x].y);  // conj(U)
@@ -371,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_reduce(RedParams p) {
     }
 #pragma unroll
     for (int y = 0; y < NY; ++y) {
-      const int e = tid + kThreads * y;
+      const int e = tid + kReduceThreads * y;
       if (e < SL * NP) {
         const int r = e / NP, jj = e % NP;
         Bc[r * LDB + jj] = ry[y];
@@ -428,15 +439,28 @@ __global__ void k_finalize(int d, int m, int RP, const double2* __restrict__ Spa
 }
 
 // ---------------------------------------------------------------------------- host side
-// 16 warps per CTA; WN column warps with <= NT <= 4 n-tiles each (3M accumulators fit 128 regs)
+// k_project: 12 consumer warps = WM x WN. WM = 4 puts all column parts of one 16-row m-tile on the
+// same SM sub-partition (warp w -> SMSP w % 4 = wm), so every SMSP gets exactly ceil(m/8) n-tiles of
+// DMMA work per k-step (balanced for any m); NT <= 5 keeps the 3M accumulators within 160 registers.
+// k_reduce: 16 warps, WN column warps with <= 4 n-tiles (3M accumulators within 128 registers).
 ProjShape proj_shape(int m) {
   ProjShape s;
   const int ntot = (m + 7) / 8;
-  s.WN = ntot <= 8 ? 2 : 4;
+  if (kConsumerWarps == 8) {
+    s.WN = 2;  // WM = 4: warp w -> SMSP w % 4 = wm, balanced; NT <= 8 (3M accumulators in 240 regs)
+  } else if (ntot <= 2) {
+    s.WN = 2;
+  } else if (ntot <= 15) {
+    s.WN = 3;
+  } else {
+    s.WN = 4;
+  }
   s.NT = (ntot + s.WN - 1) / s.WN;
-  s.WM = kConsumerWarps / s.WN;    // k_project consumer warps along rows
-  s.BM = 16 * s.WM;                // k_project rows per CTA
-  s.BI = 16 * (kThreads / 32) / s.WN;  // k_reduce rows i per CTA
+  s.WM = kConsumerWarps / s.WN;  // k_project consumer warps along rows
+  s.BM = 16 * s.WM;              // k_project rows per CTA
+  s.rWN = ntot <= 8 ? 2 : 4;
+  s.rNT = (ntot + s.rWN - 1) / s.rWN;
+  s.BI = 16 * (kReduceThreads / 32) / s.rWN;  // k_reduce rows i per CTA
   s.NP = 8 * ntot;
   return s;
 }
@@ -513,17 +537,21 @@ size_t project_workspace_bytes(int d, int n, int N, int m, int sm_count) {
 }
 
 template <int NT, int WN>
-static int launch_project_t(const ProjParams& p, const RedParams& r, dim3 grid, dim3 rgrid, cudaStream_t st,
-                            int mode, prony_exec_info* info) {
+static int launch_project_t(const ProjParams& p, dim3 grid, cudaStream_t st, int mode, prony_exec_info* info) {
   const size_t smem = ProjTile<NT, WN>::SMEM;
   auto kp = mode == 4 ? k_project<NT, WN, 4> : k_project<NT, WN, 3>;
-  auto kr = mode == 4 ? k_reduce<NT, WN, 4> : k_reduce<NT, WN, 3>;
   if (cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return PRONY_ERR_CUDA;
   if (info && info->ev_main_begin) cudaEventRecord((cudaEvent_t)info->ev_main_begin, st);
   kp<<<grid, kThreads, smem, st>>>(p);
   if (info && info->ev_main_end) cudaEventRecord((cudaEvent_t)info->ev_main_end, st);
-  kr<<<rgrid, kThreads, 0, st>>>(r);
+  return PRONY_OK;
+}
+
+template <int NT, int WN>
+static int launch_reduce_t(const RedParams& r, dim3 rgrid, cudaStream_t st, int mode) {
+  auto kr = mode == 4 ? k_reduce<NT, WN, 4> : k_reduce<NT, WN, 3>;
+  kr<<<rgrid, kReduceThreads, 0, st>>>(r);
   return PRONY_OK;
 }
 
@@ -599,11 +627,27 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   switch (WN * 16 + NT) {
 #define PRONY_CASE(nt, wn) \
   case wn * 16 + nt:       \
-    lrc = launch_project_t<nt, wn>(p, r, grd, rgrd, st, mode, info); \
+    lrc = launch_project_t<nt, wn>(p, grd, st, mode, info); \
     break;
-    PRONY_CASE(1, 2) PRONY_CASE(2, 2) PRONY_CASE(3, 2) PRONY_CASE(4, 2)
-    PRONY_CASE(3, 4) PRONY_CASE(4, 4)
+#if PRONY_CONSUMER_WARPS == 12
+    PRONY_CASE(1, 2) PRONY_CASE(1, 3) PRONY_CASE(2, 3) PRONY_CASE(3, 3) PRONY_CASE(4, 3) PRONY_CASE(5, 3)
+    PRONY_CASE(4, 4)
+#else
+    PRONY_CASE(1, 2) PRONY_CASE(2, 2) PRONY_CASE(3, 2) PRONY_CASE(4, 2) PRONY_CASE(5, 2) PRONY_CASE(6, 2)
+    PRONY_CASE(7, 2) PRONY_CASE(8, 2)
+#endif
 #undef PRONY_CASE
+    default:
+      return PRONY_ERR_RANGE;
+  }
+  if (lrc != PRONY_OK) return lrc;
+  switch (pl.shape.rWN * 16 + pl.shape.rNT) {
+#define PRONY_RCASE(nt, wn) \
+  case wn * 16 + nt:        \
+    lrc = launch_reduce_t<nt, wn>(r, rgrd, st, mode); \
+    break;
+    PRONY_RCASE(1, 2) PRONY_RCASE(2, 2) PRONY_RCASE(3, 2) PRONY_RCASE(4, 2) PRONY_RCASE(3, 4) PRONY_RCASE(4, 4)
+#undef PRONY_RCASE
     default:
       return PRONY_ERR_RANGE;
   }

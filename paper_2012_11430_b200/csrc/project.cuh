@@ -15,7 +15,9 @@ constexpr int kBK = 16;       // columns of T_l per pipeline stage of k_project
 constexpr int kStages = 3;    // cp.async ring depth of k_project (<= 227 KB smem)
 
 struct ProjShape {
-  int NT, WN, WM, BM, BI, NP;
+  int NT, WN, WM, BM;  // k_project consumer layout
+  int rNT, rWN, BI;    // k_reduce layout
+  int NP;
 };
 
 // rows of T_l covered by a call: for l = 1..d (index l-1), rows [kb, kb+rows) of I_n
