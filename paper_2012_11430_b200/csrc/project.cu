@@ -120,7 +120,7 @@ struct ProjTile {
   static constexpr int STAGE = B_S + kBK * LDBS;
   static constexpr int BAR = kStages * STAGE;        // mbarriers after the stages (2 per stage)
   static constexpr int PAT = BAR + 2 * kStages;      // row table P(k_r) + s_l + C0 (BM ints)
-  static constexpr size_t SMEM = (size_t)PAT * sizeof(double) + (size_t)BM * sizeof(int);
+  static constexpr size_t SMEM = (size_t)PAT * sizeof(double) + (size_t)(BM + 4) * sizeof(int);
   static_assert(STAGE % 2 == 0, "stage must keep 16-byte alignment");
 };
 
@@ -299,36 +299,101 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
       }
     }
   }
+
+  // split-K fixup: the last of the KC chunk CTAs of this row block sums the KC partial tiles in
+  // fixed chunk order (deterministic whatever the arrival order) into chunk slot 0
+  if (p.KC > 1) {
+    constexpr int kCons = kConsumerWarps * 32;
+    __threadfence();  // make this thread's partial-tile stores visible device-wide
+    asm volatile("bar.sync 1, %0;\n" ::"r"(kCons) : "memory");
+    int* flag = reinterpret_cast<int*>(smem + T::PAT) + BM;  // after the row table
+    if (tid == 0) {
+      const int old = atomicAdd(p.counters + l * p.nrb + blockIdx.x, 1);
+      *flag = (old == p.KC - 1);
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(kCons) : "memory");
+    if (*flag) {
+      __threadfence();
+      const int nr = min(BM, rows - rb0);
+      const size_t cstride = (size_t)p.R_tot * NP;
+      double2* y0 = p.Y + ((size_t)p.yoff[l] + rb0) * NP;
+      for (int e = tid; e < nr * NP; e += kCons) {
+        double2 s = __ldcg(y0 + e);
+        for (int c = 1; c < p.KC; ++c) {
+          const double2 v = __ldcg(y0 + c * cstride + e);
+          s.x += v.x;
+          s.y += v.y;
+        }
+        y0[e] = s;
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------- reduce
-// grid (RP, d, ceil(m/BI)); CTA (p, l, ib) sums rows k in [rows*p/RP, rows*(p+1)/RP) of segment l:
-//   S_part[l][p][i][j] = sum_k conj(U[k][i]) * sum_c Y_c[k][j],  i in [BI ib, BI ib + BI), j < m
-// with the k_project warp engine (16 warps: WM x WN, BI = 16 WM): A = U^H staged as [k][i] planes
-// (conj, conj-sum), B = sum_c Y_c staged as [k][j] planes; 8 rows k per slab, register-prefetched
-// one slab ahead.
+// grid (RP, d, ceil(NP/64)); CTA (p, l, jb) sums rows k in [rows*p/RP, rows*(p+1)/RP) of segment l,
+// computed transposed so both operands stream as contiguous rows:
+//   S_part[l][p][i][j] = sum_k conj(U[k][i]) Y[k][j]   <=>   S_part^T = Y^T conj(U)
+// (Y = chunk slot 0, where k_project's last-arriving chunk CTA left the sum of the KC partials)
+// A operand = Y_c rows (columns j in [64 jb, 64 jb + 64)), B operand = U rows under CONJB (conj).
+// K loop over (16-row slab, chunk c) stages, kRedStages-deep cp.async ring; the 3M sum planes
+// (Re+Im of Y, Re-Im of U) are formed in shared memory after each stage lands.
+constexpr int kRedSlab = 16;
+constexpr int kRedStages = 3;
+template <int NT, int WN>
+struct RedTile {
+  static constexpr int WM = (kReduceThreads / 32) / WN;  // 4 (WN = 4) or 8 (WN = 2)
+  static constexpr int BJ = 16 * WM;                      // rows j of S^T per CTA
+  static constexpr int NPU = 8 * NT * WN;                 // capacity of the i dimension
+  static constexpr int LDY = BJ + 2, LDYS = BJ + 4, LDU = NPU + 2, LDUS = NPU + 4;
+  static constexpr int Y_C = 0, Y_S = Y_C + 2 * kRedSlab * LDY, U_C = Y_S + kRedSlab * LDYS,
+                       U_S = U_C + 2 * kRedSlab * LDU, STAGE = U_S + kRedSlab * LDUS;
+  static constexpr size_t SMEM = kRedStages * (size_t)STAGE * sizeof(double);
+  static_assert(STAGE % 2 == 0 && Y_S % 2 == 0 && U_C % 2 == 0 && U_S % 2 == 0, "16-byte alignment");
+};
+
 template <int NT, int WN, int MODE>
 __global__ void __launch_bounds__(kReduceThreads, 1) k_reduce(RedParams p) {
-  constexpr int WM = (kReduceThreads / 32) / WN, BI = 16 * WM, NPMAX = 8 * NT * WN;
-  constexpr int LDA = BI + 2, LDAS = BI + 4, LDB = NPMAX + 2, LDBS = NPMAX + 4;
-  constexpr int SL = 8;  // rows k per slab
-  __shared__ __align__(16) double2 Ac[SL * LDA];
-  __shared__ double As[SL * LDAS];
-  __shared__ __align__(16) double2 Bc[SL * LDB];
-  __shared__ double Bs[SL * LDBS];
+  using T = RedTile<NT, WN>;
+  constexpr int WM = T::WM, BJ = T::BJ;
+  extern __shared__ __align__(16) double rsm[];
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(rsm);
   const int l = blockIdx.y;
   const int P = blockIdx.x;
-  const int i0 = blockIdx.z * BI;
+  const int j0 = blockIdx.z * BJ;
   const int rows = p.rows[l];
   const int rbeg = (int)((int64_t)rows * P / p.RP), rend = (int)((int64_t)rows * (P + 1) / p.RP);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp % WM, wn = warp / WM;
   const int g = lane >> 2, q = lane & 3;
-  const int m = p.m, NP = p.NP;
-  const int ntot = NP / 8;
+  const int m = p.m, NP = p.NP, KC = p.KC;
+  const int ntot = (m + 7) / 8;  // n-tiles over i
   const int t0 = (ntot * wn) / WN;
   const int nt_active = (ntot * (wn + 1)) / WN - t0;
-  const bool warp_rows = (i0 + wm * 16) < m;
+  const bool warp_rows = (j0 + wm * 16) < NP;
+  const int nslab = (rend - rbeg + kRedSlab - 1) / kRedSlab;
+  const int nstage = nslab * KC;
+
+  auto issue = [&](int stg, int buf) {
+    const int slab = stg / KC, c = stg % KC;
+    const int r0 = rbeg + slab * kRedSlab;
+    const uint32_t st = sbase + (uint32_t)(buf * T::STAGE) * 8u;
+    for (int e = tid; e < kRedSlab * BJ; e += kReduceThreads) {
+      const int r = e / BJ, jj = e % BJ;
+      const int row = r0 + r, j = j0 + jj;
+      const bool ok = row < rend && j < NP;
+      const double2* src = p.Y + (ok ? ((size_t)c * p.R_tot + p.yoff[l] + row) * NP + j : 0);
+      cp_async16(st + (uint32_t)(T::Y_C + 2 * (r * T::LDY + jj)) * 8u, src, ok ? 16 : 0);
+    }
+    for (int e = tid; e < kRedSlab * T::NPU; e += kReduceThreads) {
+      const int r = e / T::NPU, i = e % T::NPU;
+      const int row = r0 + r;
+      const bool ok = row < rend && i < m;
+      const double2* src = p.U + (ok ? (size_t)(p.kb[l] + row) * m + i : 0);
+      cp_async16(st + (uint32_t)(T::U_C + 2 * (r * T::LDU + i)) * 8u, src, ok ? 16 : 0);
+    }
+    cp_async_commit();
+  };
 
   double acc[3][NT][4];
 #pragma unroll
@@ -338,82 +403,61 @@ __global__ void __launch_bounds__(kReduceThreads, 1) k_reduce(RedParams p) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[a][j][e] = 0.0;
 
-  constexpr int NU = (SL * BI + kReduceThreads - 1) / kReduceThreads;
-  constexpr int NY = (SL * NPMAX + kReduceThreads - 1) / kReduceThreads;
-  double2 ru[NU], ry[NY];
-  auto load_slab = [&](int s) {
 #pragma unroll
-    for (int x = 0; x < NU; ++x) {
-      const int e = tid + kReduceThreads * x;
-      const int r = e / BI, ii = e % BI;
-      const int row = s + r, i = i0 + ii;
-      ru[x] = (e < SL * BI && row < rend && i < m) ? ldg2(p.U + (size_t)(p.kb[l] + row) * m + i)
-                                                     : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int y = 0; y < NY; ++y) {
-      const int e = tid + kReduceThreads * y;
-      double2 a2 = make_double2(0.0, 0.0);
-      if (e < SL * NP) {
-        const int r = e / NP, jj = e % NP;
-        const int row = s + r;
-        if (row < rend) {
-          for (int c = 0; c < p.KC; ++c) {  // fixed chunk order
-            const double2 v = ldg2(p.Y + ((size_t)c * p.R_tot + p.yoff[l] + row) * NP + jj);
-            a2.x += v.x;
-            a2.y += v.y;
-          }
-        }
-      }
-      ry[y] = a2;
-    }
-  };
-  if (rbeg < rend) load_slab(rbeg);
-  for (int s = rbeg; s < rend; s += SL) {
-#pragma unroll
-    for (int x = 0; x < NU; ++x) {
-      const int e = tid + kReduceThreads * x;
-      if (e < SL * BI) {
-        const int r = e / BI, ii = e % BI;
-        const double2 u = make_double2(ru[x].x, -ru[x].y);  // conj(U)
-        Ac[r * LDA + ii] = u;
-        As[r * LDAS + ii] = u.x + u.y;
-      }
-    }
-#pragma unroll
-    for (int y = 0; y < NY; ++y) {
-      const int e = tid + kReduceThreads * y;
-      if (e < SL * NP) {
-        const int r = e / NP, jj = e % NP;
-        Bc[r * LDB + jj] = ry[y];
-        Bs[r * LDBS + jj] = ry[y].x + ry[y].y;
-      }
-    }
-    __syncthreads();
-    if (s + SL < rend) load_slab(s + SL);
-    if (warp_rows) {
-#pragma unroll
-      for (int kk = 0; kk < SL / 4; ++kk)
-        warp_cmma_k4_n<NT, MODE>(nt_active, acc, Ac + kk * 4 * LDA + wm * 16, As + kk * 4 * LDAS + wm * 16, LDA,
-                                 LDAS, Bc + kk * 4 * LDB + t0 * 8, Bs + kk * 4 * LDBS + t0 * 8, LDB, LDBS, g, q);
-    }
-    __syncthreads();
+  for (int s = 0; s < kRedStages - 1; ++s) {
+    if (s < nstage) issue(s, s);
+    else cp_async_commit();
   }
-  double2* out = p.Spart + ((size_t)l * p.RP + P) * m * m;
-  const int ia = i0 + wm * 16 + g, ib = ia + 8;
-#pragma unroll
-  for (int j = 0; j < NT; ++j) {
-    if (j < nt_active) {
-      double re[4], im[4];
-      acc_to_complex<NT, MODE>(acc, j, re, im);
-      const int col = (t0 + j) * 8 + 2 * q;
-      if (ia < m) {
-        if (col < m) out[(size_t)ia * m + col] = make_double2(re[0], im[0]);
-        if (col + 1 < m) out[(size_t)ia * m + col + 1] = make_double2(re[1], im[1]);
+  for (int stg = 0; stg < nstage; ++stg) {
+    const int buf = stg % kRedStages;
+    cp_async_wait<kRedStages - 2>();
+    __syncthreads();
+    // refill the slot consumed in the previous iteration (all threads passed the barrier above)
+    if (stg + kRedStages - 1 < nstage) issue(stg + kRedStages - 1, (stg + kRedStages - 1) % kRedStages);
+    else cp_async_commit();
+    double* sb = rsm + buf * T::STAGE;
+    {  // sum planes: Re+Im of Y, Re-Im of U (the B operand is conj(U))
+      const double2* Yc = reinterpret_cast<const double2*>(sb + T::Y_C);
+      const double2* Uc = reinterpret_cast<const double2*>(sb + T::U_C);
+      for (int e = tid; e < kRedSlab * BJ; e += kReduceThreads) {
+        const int r = e / BJ, jj = e % BJ;
+        const double2 v = Yc[r * T::LDY + jj];
+        sb[T::Y_S + r * T::LDYS + jj] = v.x + v.y;
       }
-      if (ib < m) {
-        if (col < m) out[(size_t)ib * m + col] = make_double2(re[2], im[2]);
-        if (col + 1 < m) out[(size_t)ib * m + col + 1] = make_double2(re[3], im[3]);
+      for (int e = tid; e < kRedSlab * T::NPU; e += kReduceThreads) {
+        const int r = e / T::NPU, i = e % T::NPU;
+        const double2 v = Uc[r * T::LDU + i];
+        sb[T::U_S + r * T::LDUS + i] = v.x - v.y;
+      }
+    }
+    __syncthreads();
+    if (warp_rows) {
+      const double2* Ac = reinterpret_cast<const double2*>(sb + T::Y_C) + wm * 16;
+      const double* As = sb + T::Y_S + wm * 16;
+      const double2* Bc = reinterpret_cast<const double2*>(sb + T::U_C) + t0 * 8;
+      const double* Bs = sb + T::U_S + t0 * 8;
+#pragma unroll
+      for (int kk = 0; kk < kRedSlab / 4; ++kk)
+        warp_cmma_k4_n<NT, MODE, true>(nt_active, acc, Ac + kk * 4 * T::LDY, As + kk * 4 * T::LDYS, T::LDY,
+                                       T::LDYS, Bc + kk * 4 * T::LDU, Bs + kk * 4 * T::LDUS, T::LDU, T::LDUS, g, q);
+    }
+  }
+  // acc rows = j, columns = i  ->  S_part[i][j]
+  double2* out = p.Spart + ((size_t)l * p.RP + P) * m * m;
+  const int ja = j0 + wm * 16 + g, jb = ja + 8;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    if (t < nt_active) {
+      double re[4], im[4];
+      acc_to_complex<NT, MODE>(acc, t, re, im);
+      const int i = (t0 + t) * 8 + 2 * q;
+      if (ja < m) {
+        if (i < m) out[(size_t)i * m + ja] = make_double2(re[0], im[0]);
+        if (i + 1 < m) out[(size_t)(i + 1) * m + ja] = make_double2(re[1], im[1]);
+      }
+      if (jb < m) {
+        if (i < m) out[(size_t)i * m + jb] = make_double2(re[2], im[2]);
+        if (i + 1 < m) out[(size_t)(i + 1) * m + jb] = make_double2(re[3], im[3]);
       }
     }
   }
@@ -460,7 +504,7 @@ ProjShape proj_shape(int m) {
   s.BM = 16 * s.WM;              // k_project rows per CTA
   s.rWN = ntot <= 8 ? 2 : 4;
   s.rNT = (ntot + s.rWN - 1) / s.rWN;
-  s.BI = 16 * (kReduceThreads / 32) / s.rWN;  // k_reduce rows i per CTA
+  s.BI = 16 * (kReduceThreads / 32) / s.rWN;  // k_reduce rows j of S^T per CTA
   s.NP = 8 * ntot;
   return s;
 }
@@ -498,16 +542,16 @@ int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl) {
   pl->chunk_w = chunk_w;
   pl->KC = (g.N + chunk_w - 1) / chunk_w;  // every chunk non-empty
   // reduce partition: about 1 CTA per SM in total
-  const int ib = (g.m + sh.BI - 1) / sh.BI;
+  const int ib = (sh.NP + sh.BI - 1) / sh.BI;  // j-blocks of k_reduce
   int RP = sm_count / std::max(1, g.d * ib);
-  RP = std::max(1, std::min(RP, std::max(1, (max_rows + 7) / 8)));
+  RP = std::max(1, std::min(RP, std::max(1, (max_rows + 15) / 16)));
   pl->RP = RP;
   return 0;
 }
 
 namespace {
 struct WsLayout {
-  size_t ptab, gsum, vsum, Y, Spart, total;
+  size_t ptab, gsum, vsum, Y, Spart, counters, total;
 };
 WsLayout ws_layout(int d, int n, int N, int m, int sm_count) {
   const ProjShape sh = proj_shape(m);
@@ -524,9 +568,10 @@ WsLayout ws_layout(int d, int n, int N, int m, int sm_count) {
   w.gsum = take((size_t)box * sizeof(double));
   w.vsum = take((size_t)N * sh.NP * sizeof(double));
   w.Y = take((size_t)kYCap * d * N * sh.NP * sizeof(double2));  // Y partials (KC*R_tot <= kYCap*dN)
-  const int ib = (m + sh.BI - 1) / sh.BI;
+  const int ib = (sh.NP + sh.BI - 1) / sh.BI;
   const int RP = std::max(1, sm_count / std::max(1, d * ib));
   w.Spart = take((size_t)d * RP * m * m * sizeof(double2));
+  w.counters = take((size_t)d * ((N + 15) / 16 + 1) * sizeof(int));  // split-K arrival counters
   w.total = off;
   return w;
 }
@@ -551,7 +596,11 @@ static int launch_project_t(const ProjParams& p, dim3 grid, cudaStream_t st, int
 template <int NT, int WN>
 static int launch_reduce_t(const RedParams& r, dim3 rgrid, cudaStream_t st, int mode) {
   auto kr = mode == 4 ? k_reduce<NT, WN, 4> : k_reduce<NT, WN, 3>;
-  kr<<<rgrid, kReduceThreads, 0, st>>>(r);
+  const size_t smem = RedTile<NT, WN>::SMEM;
+  if (cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return PRONY_ERR_CUDA;
+  rgrid.z = (r.NP + RedTile<NT, WN>::BJ - 1) / RedTile<NT, WN>::BJ;
+  kr<<<rgrid, kReduceThreads, smem, st>>>(r);
   return PRONY_OK;
 }
 
@@ -565,6 +614,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   double* vsum = (double*)(w + wl.vsum);
   double2* Y = (double2*)(w + wl.Y);
   double2* Spart = (double2*)(w + wl.Spart);
+  int* counters = (int*)(w + wl.counters);
 
   if (info) {
     info->launches = 0;
@@ -579,6 +629,9 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   }
   int64_t box = 1;
   for (int i = 0; i < g.d; ++i) box *= (2 * (int64_t)g.n + 2);
+  const int nrb = (pl.max_rows + pl.shape.BM - 1) / pl.shape.BM;
+  if (pl.KC > 1 && cudaMemsetAsync(counters, 0, (size_t)g.d * nrb * sizeof(int), st) != cudaSuccess)
+    return PRONY_ERR_CUDA;
   k_prep<<<2 * sm_count, 256, 0, st>>>(g.d, g.n, g.N, g.m, pl.shape.NP, box, grid, V, ptab, gsum, vsum);
 
   ProjParams p{};
@@ -593,6 +646,9 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   p.NP = pl.shape.NP;
   p.chunk_w = pl.chunk_w;
   p.R_tot = pl.R_tot;
+  p.KC = pl.KC;
+  p.nrb = nrb;
+  p.counters = counters;
   const int L = 2 * g.n + 2;
   int64_t C0 = 0, s = 1;
   for (int i = 0; i < g.d; ++i) {
@@ -611,7 +667,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   r.Spart = Spart;
   r.m = g.m;
   r.NP = pl.shape.NP;
-  r.KC = pl.KC;
+  r.KC = 1;  // k_project's fixup left the summed tile in chunk slot 0
   r.R_tot = pl.R_tot;
   r.RP = pl.RP;
   for (int l = 0; l < g.d; ++l) {
@@ -620,7 +676,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
     r.yoff[l] = pl.yoff[l];
   }
   dim3 grd((pl.max_rows + pl.shape.BM - 1) / pl.shape.BM, pl.KC, g.d);
-  dim3 rgrd(pl.RP, g.d, (g.m + pl.shape.BI - 1) / pl.shape.BI);
+  dim3 rgrd(pl.RP, g.d, (pl.shape.NP + pl.shape.BI - 1) / pl.shape.BI);
   const int NT = pl.shape.NT, WN = pl.shape.WN;
   const int mode = cmul_mode();
   int lrc = PRONY_OK;

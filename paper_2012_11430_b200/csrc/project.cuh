@@ -42,7 +42,8 @@ struct ProjParams {
   const double* vsum;
   const int32_t* ptab;
   double2* Y;
-  int N, m, NP, chunk_w, R_tot;
+  int* counters;  // [d][nrb] split-K arrival counters (zeroed per call)
+  int N, m, NP, chunk_w, R_tot, KC, nrb;
   int kb[PRONY_MAX_D], rows[PRONY_MAX_D], yoff[PRONY_MAX_D], shift[PRONY_MAX_D];
 };
 

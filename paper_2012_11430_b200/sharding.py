@@ -79,17 +79,27 @@ class DistributedPencil:
         self.G = torch.empty((m, m), dtype=torch.complex128, device=device)
         self.b = torch.empty(m, dtype=torch.complex128, device=device)
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        # the LS step is independent of the projection: it runs on a side stream and fills the SMs
+        # the projection's last wave leaves idle
+        self.side = torch.cuda.Stream(device=device)
+        self.ev_in = torch.cuda.Event()
+        self.ev_ls = torch.cuda.Event()
 
     def __call__(self, grid, U, V, sigma, z, stream=None, info_p=None, info_l=None):
         pb, d, n, m = self.pb, self.d, self.n, self.m
+        main = stream if stream is not None else torch.cuda.current_stream()
+        self.ev_in.record(main)
         pb.project(grid, U, V, sigma, d, n, m, self.u0, self.u1, self.order, out=self.S, workspace=self.ws_p,
-                   stream=stream, info=info_p)
+                   stream=main, info=info_p)
         full = self.world == 1
+        self.side.wait_event(self.ev_in)
         res = pb.vandermonde_ls(z, grid, d, n, m, self.c0, self.c1, want_solution=full,
                                 out={"G": self.G, "b": self.b}, workspace=self.ws_l, dev_status=self.status,
-                                stream=stream, info=info_l)
+                                stream=self.side, info=info_l)
+        self.ev_ls.record(self.side)
+        main.wait_event(self.ev_ls)
         if full:
             return self.S, res["c"], res["t"]
         Sr, Gr, br = allreduce_pencil(self.S, self.G, self.b)
-        c, t = pb.ls_solve(Gr.contiguous(), br.contiguous(), z, d, m, dev_status=self.status, stream=stream)
+        c, t = pb.ls_solve(Gr.contiguous(), br.contiguous(), z, d, m, dev_status=self.status, stream=main)
         return Sr, c, t

@@ -125,6 +125,24 @@ def test_project_cmul_modes(pb, orc, mode, d, n, m, monkeypatch):
         assert rel(S[l], S_or[l]) <= 1e-13
 
 
+@pytest.mark.parametrize("u0,u1,order", [(0, 100, 0), (4096 + 7, 4096 + 300, 0), (11, 913, 1), (0, 8192, 1)])
+def test_project_small_ranges_many_chunks(pb, orc, u0, u1, order):
+    """Small unit ranges over a long K (N = 4096) make the planner split K into many chunks:
+    exercises the split-K arrival counters and the last-arriver fixup of k_project."""
+    prob = problem(2, 63, 20, 5151, 1e-6, random_uv=True)
+    c = prob.cfg
+    S = run_project(pb, prob, unit_begin=u0, unit_end=u1, unit_order=order)
+    S2 = run_project(pb, prob, unit_begin=u0, unit_end=u1, unit_order=order)
+    torch.cuda.synchronize()
+    assert torch.equal(S, S2)                       # deterministic whatever the arrival order
+    S_or = orc.project_units(prob.grid, prob.U, prob.V, prob.sigma, c.d, c.n, u0, u1, order)
+    for l in range(c.d):
+        if np.linalg.norm(S_or[l]) == 0:
+            assert float(S[l].abs().max()) == 0.0
+        else:
+            assert rel(S[l], S_or[l]) <= TOL
+
+
 def test_project_empty_range_is_zero(pb):
     prob = problem(2, 5, 4, 5, random_uv=True)
     S = run_project(pb, prob, unit_begin=7, unit_end=7)
