@@ -90,7 +90,8 @@ typedef enum prony_workspace_kind {
   PRONY_WS_PROJECT = 0,      /* prony_project, any unit range */
   PRONY_WS_LS = 1,           /* prony_vandermonde_ls, any column range */
   PRONY_WS_PENCIL_HOST = 2,  /* prony_pencil_host: device copies of inputs/outputs + both above */
-  PRONY_WS_BUILD = 3         /* prony_build_pencil (round 1: 0) */
+  PRONY_WS_BUILD = 3,        /* prony_build_pencil */
+  PRONY_WS_APPLY = 4         /* prony_toeplitz_apply, any r */
 } prony_workspace_kind;
 
 /* unit orders of prony_project: units u in [0, d*N) */
@@ -197,6 +198,19 @@ int prony_vandermonde_ls_ex(int d, int n, int m, const prony_c128* z, const pron
  */
 int prony_ls_solve(int d, int m, const prony_c128* G, const prony_c128* b, const prony_c128* z, prony_c128* c,
                    double* t, void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream);
+
+/*
+ * prony_toeplitz_apply — Y = T_l X (l = 1..d), Y = T X (l = 0) or, with conj = 1 and l = 0,
+ * Y = T^H X, for an N x r block X; T = [f(k-h)], T_l = [f(k-h+e_l)] generated implicitly
+ * from the grid exactly as in prony_project (never materialized). This is the operator the block
+ * power SVD of T (Alg. 3) applies; any r >= 1 (processed in column passes).
+ *   X           device N x r prony_c128, row stride ldx (elements, >= r)
+ *   Y           device N x r prony_c128, row stride ldy (>= r), overwritten
+ *   workspace   >= prony_workspace_size(PRONY_WS_APPLY)   (m argument ignored for this kind)
+ * Errors: PRONY_ERR_INVALID for conj with l != 0, l out of [0, d], null/misaligned pointers.
+ */
+int prony_toeplitz_apply(int d, int n, const prony_c128* grid, int ell, int conj, const prony_c128* X, int ldx, int r,
+                         prony_c128* Y, int ldy, void* workspace, size_t workspace_bytes, prony_stream_t stream);
 
 /*
  * prony_pencil_host — one full pencil (prony_project over [0, dN) + prony_vandermonde_ls over

@@ -10,7 +10,8 @@ from .binding import (  # noqa: F401
     EXPORTS, ExecInfo, make_exec_info, MAX_D, MAX_M, PRONY_ERR_CUDA, PRONY_ERR_INVALID, PRONY_ERR_RANGE, PRONY_ERR_SINGULAR,
     PRONY_ERR_UNIMPLEMENTED, PRONY_ERR_WORKSPACE, PRONY_OK, UNITS_L_MAJOR, UNITS_ROW_MAJOR, WS_LS,
     WS_PENCIL_HOST, WS_PROJECT, PronyError, alloc_workspace, build_pencil, device_info, lib, ls_solve,
-    pencil_host, project, status_string, vandermonde_ls, workspace_size,
+    pencil_host, project, status_string, toeplitz_apply, vandermonde_ls, workspace_size,
+    WS_APPLY,
 )
 from . import sharding  # noqa: F401
 

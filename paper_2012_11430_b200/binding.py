@@ -23,14 +23,14 @@ PRONY_ERR_CUDA = 6
 PRONY_ERR_UNIMPLEMENTED = 7
 PRONY_ERR_WORKSPACE = 8
 
-WS_PROJECT, WS_LS, WS_PENCIL_HOST, WS_BUILD = 0, 1, 2, 3
+WS_PROJECT, WS_LS, WS_PENCIL_HOST, WS_BUILD, WS_APPLY = 0, 1, 2, 3, 4
 UNITS_L_MAJOR, UNITS_ROW_MAJOR = 0, 1
 MAX_D, MAX_M = 8, 128
 
 # every symbol include/prony.h declares (checked by tests/test_abi.py)
 EXPORTS = ("prony_abi_version", "prony_status_string", "prony_device_info", "prony_workspace_size",
            "prony_project", "prony_project_ex", "prony_vandermonde_ls", "prony_vandermonde_ls_ex", "prony_ls_solve",
-           "prony_pencil_host", "prony_build_pencil")
+           "prony_toeplitz_apply", "prony_pencil_host", "prony_build_pencil")
 
 
 class ExecInfo(ctypes.Structure):
@@ -75,10 +75,11 @@ def lib() -> ctypes.CDLL:
         L.prony_project_ex.argtypes = L.prony_project.argtypes + [vp]
         L.prony_vandermonde_ls_ex.argtypes = L.prony_vandermonde_ls.argtypes + [vp]
         L.prony_ls_solve.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, sz, vp, vp]
+        L.prony_toeplitz_apply.argtypes = [i32, i32, vp, i32, i32, vp, i32, i32, vp, i32, vp, sz, vp]
         L.prony_pencil_host.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp]
         L.prony_build_pencil.argtypes = [i32, i32, i32, vp, ctypes.c_uint64, vp, vp, vp, vp, vp, vp, sz, vp, vp]
         for f in ("prony_device_info", "prony_workspace_size", "prony_project", "prony_vandermonde_ls", "prony_ls_solve",
-                  "prony_project_ex", "prony_vandermonde_ls_ex",
+                  "prony_project_ex", "prony_vandermonde_ls_ex", "prony_toeplitz_apply",
                   "prony_pencil_host", "prony_build_pencil"):
             getattr(L, f).restype = i32
         _lib = L
@@ -213,6 +214,24 @@ def ls_solve(G, b, z, d: int, m: int, want_t: bool = True, workspace=None, dev_s
                               _ptr(dev_status), _stream(stream))
     _check(rc, "prony_ls_solve")
     return c, t
+
+
+def toeplitz_apply(grid, X, d: int, n: int, ell: int = 0, conj: bool = False, out=None, workspace=None,
+                   stream=None):
+    """Y = T_l X (l = 1..d), T X (l = 0) or T^H X (l = 0, conj) with the implicit gather."""
+    _dev_tensor(grid, torch.complex128, "grid")
+    if not (isinstance(X, torch.Tensor) and X.is_cuda and X.dtype == torch.complex128 and X.dim() == 2
+            and X.stride(1) == 1):
+        raise TypeError("X must be a CUDA complex128 matrix with unit column stride")
+    N, r = X.shape
+    if out is None:
+        out = torch.empty((N, r), dtype=torch.complex128, device=X.device)
+    if workspace is None:
+        workspace = alloc_workspace(WS_APPLY, d, n, 1, X.device)
+    rc = lib().prony_toeplitz_apply(d, n, _ptr(grid), int(ell), int(bool(conj)), _ptr(X), X.stride(0), r, _ptr(out),
+                                    out.stride(0), _ptr(workspace), workspace.numel(), _stream(stream))
+    _check(rc, "prony_toeplitz_apply")
+    return out
 
 
 def pencil_host(grid, U, V, sigma, z, d: int, n: int, m: int, workspace=None, outputs=None, stream=None):

@@ -136,6 +136,7 @@ int prony_workspace_size(int kind, int d, int n, int m, size_t* bytes) {
     case PRONY_WS_LS: *bytes = ws_ls(d, n, m, sms); return PRONY_OK;
     case PRONY_WS_PENCIL_HOST: *bytes = host_layout(d, n, m, N, sms).total; return PRONY_OK;
     case PRONY_WS_BUILD: *bytes = 0; return PRONY_OK;
+    case PRONY_WS_APPLY: *bytes = apply_workspace_bytes(d, n, (int)N); return PRONY_OK;
     default: return PRONY_ERR_INVALID;
   }
 }
@@ -212,6 +213,22 @@ int prony_ls_solve(int d, int m, const prony_c128* G, const prony_c128* b, const
     return PRONY_ERR_INVALID;
   return ls_solve_launch(d, m, (const double2*)G, (const double2*)b, (const double2*)z, (double2*)c, t, workspace,
                          dev_status, (cudaStream_t)stream);
+}
+
+int prony_toeplitz_apply(int d, int n, const prony_c128* grid, int ell, int conj, const prony_c128* X, int ldx, int r,
+                         prony_c128* Y, int ldy, void* workspace, size_t workspace_bytes, prony_stream_t stream) {
+  int64_t N = 0;
+  int rc = validate_dnm(d, n, 1, &N);
+  if (rc) return rc;
+  if (ell < 0 || ell > d || (conj && ell != 0) || r < 1 || ldx < r || ldy < r) return PRONY_ERR_INVALID;
+  if (!grid || !X || !Y || !workspace) return PRONY_ERR_INVALID;
+  if (!aligned16(grid) || !aligned16(X) || !aligned16(Y) || ((uintptr_t)workspace & 255u)) return PRONY_ERR_INVALID;
+  if (N * (int64_t)std::max(ldx, ldy) >= (int64_t(1) << 31)) return PRONY_ERR_RANGE;
+  const int sms = sm_count_current();
+  if (sms <= 0) return PRONY_ERR_CUDA;
+  if (workspace_bytes < apply_workspace_bytes(d, n, (int)N)) return PRONY_ERR_WORKSPACE;
+  return toeplitz_apply_launch(d, n, (int)N, (const double2*)grid, ell, conj, (const double2*)X, ldx, r, (double2*)Y,
+                               ldy, workspace, sms, (cudaStream_t)stream);
 }
 
 int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,

@@ -28,7 +28,7 @@ static int cmul_mode() {
 }
 
 // ---------------------------------------------------------------------------- prep
-__global__ void k_prep(int d, int n, int N, int m, int NP, int64_t box, const double2* __restrict__ grid,
+__global__ void k_prep(int d, int n, int N, int m, int ldv, int NP, int64_t box, const double2* __restrict__ grid,
                        const double2* __restrict__ V, int32_t* __restrict__ ptab, double* __restrict__ gsum,
                        double* __restrict__ vsum) {
   const int L = 2 * n + 2;
@@ -57,7 +57,7 @@ __global__ void k_prep(int d, int n, int N, int m, int NP, int64_t box, const do
     const int c = (int)(e % NP);
     double s = 0.0;
     if (c < m) {
-      const double2 v = V[h * m + c];
+      const double2 v = V[h * ldv + c];
       s = v.x + v.y;
     }
     vsum[e] = s;
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
         if (kr < nrows) {
           const int h = h0 + kr;
           if (!sum_plane) {
-            bulk_g2s(st + (uint32_t)(T::B_C + 2 * kr * T::LDB) * 8u, V + (size_t)h * m, (uint32_t)m * 16u,
+            bulk_g2s(st + (uint32_t)(T::B_C + 2 * kr * T::LDB) * 8u, V + (size_t)h * p.ldv, (uint32_t)m * 16u,
                      full0 + 8u * s);
           } else if constexpr (MODE == 3) {
             bulk_g2s(st + (uint32_t)(T::B_S + kr * T::LDBS) * 8u, vsum + (size_t)h * NP, (uint32_t)NP * 8u,
@@ -632,12 +632,13 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   const int nrb = (pl.max_rows + pl.shape.BM - 1) / pl.shape.BM;
   if (pl.KC > 1 && cudaMemsetAsync(counters, 0, (size_t)g.d * nrb * sizeof(int), st) != cudaSuccess)
     return PRONY_ERR_CUDA;
-  k_prep<<<2 * sm_count, 256, 0, st>>>(g.d, g.n, g.N, g.m, pl.shape.NP, box, grid, V, ptab, gsum, vsum);
+  k_prep<<<2 * sm_count, 256, 0, st>>>(g.d, g.n, g.N, g.m, g.m, pl.shape.NP, box, grid, V, ptab, gsum, vsum);
 
   ProjParams p{};
   p.grid = grid;
   p.gsum = gsum;
   p.V = V;
+  p.ldv = g.m;
   p.vsum = vsum;
   p.ptab = ptab;
   p.Y = Y;
@@ -718,6 +719,155 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
     info->main_block = kThreads;
     info->split_k = pl.KC;
     info->main_flops = 8.0 * g.m * (double)g.N * (double)pl.R_tot;
+  }
+  if (cudaGetLastError() != cudaSuccess) return PRONY_ERR_CUDA;
+  return PRONY_OK;
+}
+
+// ---------------------------------------------------------------------------- Toeplitz apply
+// Y = T_l X (l = 1..d), Y = T X (l = 0) or Y = T^H X (l = 0, conj) for an N x r block X, with the
+// k_project pipeline (the same implicit gather; NEXT-1 reuses it for the block power SVD).
+// T^H[h][k] = conj(f(k-h)) = f'(h-k) with f'(v) = conj(f(-v)): the same Toeplitz form on the reflected,
+// conjugated grid (built by k_reflect_conj; points whose reflection leaves the box are never read
+// for l = 0 and are set to 0).
+__global__ void k_reflect_conj(int d, int n, int64_t box, const double2* __restrict__ grid, double2* __restrict__ out) {
+  const int L = 2 * n + 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < box; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e, idx = 0, s = 1;
+    bool inside = true;
+    for (int i = d - 1; i >= 0; --i) {
+      const int v = (int)(r % L) - n;  // coordinate in {-n..n+1}
+      r /= L;
+      const int w = -v;                // reflected coordinate
+      if (w < -n || w > n + 1) inside = false;
+      idx += (int64_t)(w + n) * s;
+      s *= L;
+    }
+    out[e] = inside ? cconj(grid[idx]) : make_double2(0.0, 0.0);
+  }
+}
+
+__global__ void k_copy_cols(int N, int w, int NP, const double2* __restrict__ Y0, double2* __restrict__ Yout, int ldy,
+                            int c0) {
+  const int64_t tot = (int64_t)N * w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / w;
+    const int j = (int)(e % w);
+    Yout[k * ldy + c0 + j] = Y0[k * NP + j];
+  }
+}
+
+namespace {
+constexpr int kApplyMaxW = 120;  // columns per k_project pass (NT <= 5 over WN = 3 warps)
+struct ApplyLayout {
+  size_t refl, ptab, gsum, vsum, Y, counters, total;
+};
+ApplyLayout apply_layout(int d, int n, int N) {
+  int64_t box = 1;
+  for (int i = 0; i < d; ++i) box *= (2 * (int64_t)n + 2);
+  ApplyLayout a{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += align_up(bytes, 256);
+    return o;
+  };
+  a.refl = take((size_t)box * sizeof(double2));
+  a.ptab = take((size_t)(N + kPtabPad) * sizeof(int32_t));
+  a.gsum = take((size_t)box * sizeof(double));
+  a.vsum = take((size_t)N * kApplyMaxW * sizeof(double));
+  a.Y = take((size_t)kYCap * N * kApplyMaxW * sizeof(double2));
+  a.counters = take((size_t)((N + 15) / 16 + 1) * sizeof(int));
+  a.total = off;
+  return a;
+}
+}  // namespace
+
+size_t apply_workspace_bytes(int d, int n, int N) { return apply_layout(d, n, N).total; }
+
+int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int conj, const double2* X, int ldx, int r,
+                          double2* Yout, int ldy, void* ws, int sm_count, cudaStream_t st) {
+  const ApplyLayout al = apply_layout(d, n, N);
+  char* w = (char*)ws;
+  double2* refl = (double2*)(w + al.refl);
+  int32_t* ptab = (int32_t*)(w + al.ptab);
+  double* gsum = (double*)(w + al.gsum);
+  double* vsum = (double*)(w + al.vsum);
+  double2* Y = (double2*)(w + al.Y);
+  int* counters = (int*)(w + al.counters);
+  int64_t box = 1;
+  for (int i = 0; i < d; ++i) box *= (2 * (int64_t)n + 2);
+  const double2* g = grid;
+  if (conj) {
+    k_reflect_conj<<<2 * sm_count, 256, 0, st>>>(d, n, box, grid, refl);
+    g = refl;
+  }
+  const int L = 2 * n + 2;
+  int64_t C0 = 0, s = 1;
+  for (int i = 0; i < d; ++i) {
+    C0 += (int64_t)n * s;
+    s *= L;
+  }
+  const int shift = (int)(C0 + (ell >= 1 ? ipow(L, d - ell) : 0));
+  const int npass = (r + kApplyMaxW - 1) / kApplyMaxW;
+  const int mode = cmul_mode();
+  for (int ps = 0; ps < npass; ++ps) {
+    const int c0 = (int)((int64_t)r * ps / npass), c1 = (int)((int64_t)r * (ps + 1) / npass);
+    const int wcols = c1 - c0;
+    ProjGeom gg{};
+    gg.d = 1;
+    gg.n = n;
+    gg.m = wcols;
+    gg.N = N;
+    gg.kb[0] = 0;
+    gg.rows[0] = N;
+    ProjPlan pl{};
+    project_plan(gg, sm_count, &pl);
+    const int nrb = (pl.max_rows + pl.shape.BM - 1) / pl.shape.BM;
+    if (pl.KC > 1 && cudaMemsetAsync(counters, 0, (size_t)nrb * sizeof(int), st) != cudaSuccess) return PRONY_ERR_CUDA;
+    k_prep<<<2 * sm_count, 256, 0, st>>>(d, n, N, wcols, ldx, pl.shape.NP, box, g, X + c0, ptab, gsum, vsum);
+    ProjParams p{};
+    p.grid = g;
+    p.gsum = gsum;
+    p.V = X + c0;
+    p.ldv = ldx;
+    p.vsum = vsum;
+    p.ptab = ptab;
+    p.Y = Y;
+    p.N = N;
+    p.m = wcols;
+    p.NP = pl.shape.NP;
+    p.chunk_w = pl.chunk_w;
+    p.R_tot = pl.R_tot;
+    p.KC = pl.KC;
+    p.nrb = nrb;
+    p.counters = counters;
+    p.kb[0] = 0;
+    p.rows[0] = N;
+    p.yoff[0] = 0;
+    p.shift[0] = shift;
+    dim3 grd(nrb, pl.KC, 1);
+    int lrc = PRONY_OK;
+    switch (pl.shape.WN * 16 + pl.shape.NT) {
+#define PRONY_CASE(nt, wn) \
+  case wn * 16 + nt:       \
+    lrc = launch_project_t<nt, wn>(p, grd, st, mode, nullptr); \
+    break;
+#if PRONY_CONSUMER_WARPS == 12
+      PRONY_CASE(1, 2) PRONY_CASE(1, 3) PRONY_CASE(2, 3) PRONY_CASE(3, 3) PRONY_CASE(4, 3) PRONY_CASE(5, 3)
+      PRONY_CASE(4, 4)
+#else
+      PRONY_CASE(1, 2) PRONY_CASE(2, 2) PRONY_CASE(3, 2) PRONY_CASE(4, 2) PRONY_CASE(5, 2) PRONY_CASE(6, 2)
+      PRONY_CASE(7, 2) PRONY_CASE(8, 2)
+#endif
+#undef PRONY_CASE
+      default:
+        return PRONY_ERR_RANGE;
+    }
+    if (lrc != PRONY_OK) return lrc;
+    const int64_t tot = (int64_t)N * wcols;
+    k_copy_cols<<<(int)std::min<int64_t>((tot + 255) / 256, 8 * sm_count), 256, 0, st>>>(N, wcols, pl.shape.NP, Y,
+                                                                                        Yout, ldy, c0);
   }
   if (cudaGetLastError() != cudaSuccess) return PRONY_ERR_CUDA;
   return PRONY_OK;

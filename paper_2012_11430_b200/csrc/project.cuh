@@ -39,6 +39,7 @@ struct ProjParams {
   const double2* grid;
   const double* gsum;
   const double2* V;
+  int ldv;  // row stride of V (elements)
   const double* vsum;
   const int32_t* ptab;
   double2* Y;
@@ -61,5 +62,9 @@ size_t project_workspace_bytes(int d, int n, int N, int m, int sm_count);
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
                    const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
                    prony_exec_info* info);
+
+size_t apply_workspace_bytes(int d, int n, int N);
+int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int conj, const double2* X, int ldx, int r,
+                          double2* Yout, int ldy, void* ws, int sm_count, cudaStream_t st);
 
 }  // namespace prony

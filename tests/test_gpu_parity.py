@@ -168,6 +168,39 @@ def test_project_spectrum_recovers_nodes(pb):
             assert np.min(np.abs(ev - zj)) < 1e-10
 
 
+# ------------------------------------------------------------------ Toeplitz apply (NEXT-1 operator)
+@pytest.mark.parametrize("d,n,r,noise", [(2, 7, 5, 1e-6), (3, 4, 130, 0.0), (1, 30, 3, 1e-3), (4, 3, 17, 1e-6)])
+def test_toeplitz_apply_dense_oracle(pb, orc, d, n, r, noise):
+    """Y = T_l X, T X and T^H X against the oracle's dense T_l times X."""
+    prob = problem(d, n, 3, 600 + d + n + r, noise, random_uv=True)
+    N = prob.cfg.N
+    rng = np.random.default_rng(r)
+    X = rng.standard_normal((N, r)) + 1j * rng.standard_normal((N, r))
+    Xd = dev(X)
+    for ell in range(0, d + 1):
+        Y = pb.toeplitz_apply(dev(prob.grid), Xd, d, n, ell).cpu().numpy()
+        T = orc.T_dense(prob.grid, d, n, ell)
+        assert rel(Y, T @ X) <= 1e-13
+    Yh = pb.toeplitz_apply(dev(prob.grid), Xd, d, n, 0, conj=True).cpu().numpy()
+    T = orc.T_dense(prob.grid, d, n, 0)
+    assert rel(Yh, T.conj().T @ X) <= 1e-13
+
+
+def test_toeplitz_apply_strided_columns(pb, orc):
+    """X and Y as column slices of wider matrices (row strides ldx, ldy > r)."""
+    prob = problem(2, 9, 3, 77, 1e-6, random_uv=True)
+    N = prob.cfg.N
+    rng = np.random.default_rng(5)
+    Xw = rng.standard_normal((N, 40)) + 1j * rng.standard_normal((N, 40))
+    Xd = dev(Xw)
+    Yw = torch.zeros((N, 50), dtype=torch.complex128, device="cuda")
+    pb.toeplitz_apply(dev(prob.grid), Xd[:, 6:29], 2, 9, 1, out=Yw[:, 10:33])
+    T1 = orc.T_dense(prob.grid, 2, 9, 1)
+    Y = Yw.cpu().numpy()
+    assert rel(Y[:, 10:33], T1 @ Xw[:, 6:29]) <= 1e-13
+    assert np.all(Y[:, :10] == 0) and np.all(Y[:, 33:] == 0)
+
+
 # ------------------------------------------------------------------ full-size configs
 def _closed_form_S(prob):
     """F1 (noise-free, any U V sigma): S_l = (U* B) diag(c z_l) (B^H V) Sigma^-1."""
