@@ -14,8 +14,10 @@
  *                        and, over the full column range, c = conj(G^-1 b) and
  *                        t_j = (-arg z_j / 2 pi) mod 1 (reading R4).
  *   prony_pencil_host    both of the above from HOST buffers (copies in, results out).
- *   prony_build_pencil   reduced SVD of T (Alg. 3) + prony_project:
- *                        not implemented in this round (returns PRONY_ERR_UNIMPLEMENTED).
+ *   prony_build_pencil   reduced SVD of T (block power method Alg. 3) on the
+ *                        device, then prony_project (Algorithm 1 lines 1-3).
+ *   prony_diagonalize    C_mu, its eigenvectors W, z = diag(W^-1 S_l W), t (Algorithm 1 lines 4-6).
+ *   prony_toeplitz_apply T_l X, T X, T^H X with the implicit gather (the operator of the SVD).
  *
  * Layout conventions (readings R1, R2):
  *   - complex numbers are prony_c128 {re, im} (== cuDoubleComplex == torch.complex128).
@@ -91,7 +93,8 @@ typedef enum prony_workspace_kind {
   PRONY_WS_LS = 1,           /* prony_vandermonde_ls, any column range */
   PRONY_WS_PENCIL_HOST = 2,  /* prony_pencil_host: device copies of inputs/outputs + both above */
   PRONY_WS_BUILD = 3,        /* prony_build_pencil */
-  PRONY_WS_APPLY = 4         /* prony_toeplitz_apply, any r */
+  PRONY_WS_APPLY = 4,        /* prony_toeplitz_apply, any r */
+  PRONY_WS_DIAG = 5          /* prony_diagonalize */
 } prony_workspace_kind;
 
 /* unit orders of prony_project: units u in [0, d*N) */
@@ -229,13 +232,40 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
                       prony_stream_t stream);
 
 /*
- * prony_build_pencil — reduced rank-m SVD of T on the device (block power method, Alg. 3,
- * P:179-201, reusing the implicit Toeplitz apply) followed by prony_project.
- * Round 1: returns PRONY_ERR_UNIMPLEMENTED after validating its arguments.
+ * prony_build_pencil — Algorithm 1 lines 1-3 on the device: the reduced SVD T = U Sigma V*
+ * (eq_T_svd) by the block power method of Alg. 3 with starting dimension 2m
+ * (P:595), T V and T^H U applied by the implicit-Toeplitz gather of prony_project, Cholesky-QR steps,
+ * rank determination by diagonal-pivoted Cholesky of the Gram of Vbar_1 (equivalent to the pivoted QR
+ * of P:193/P:203 in exact arithmetic; trailing-norm tolerance max(tol, 1e-7), R22), and the
+ * SVD of Q_k by one-sided Jacobi; then S_1..S_d = U* T_l V Sigma^-1 over all units (prony_project).
+ * SYNCHRONOUS: the stream is synchronized once per power iteration (the rank and the residual steer it).
+ *   grid            device L^d samples (as prony_project)
+ *   seed            seeds the random starting block V_0 (counter-based generator, R14)
+ *   tol             rank / convergence tolerance (P:581 noise-free N*eps_M; P:627 the noise level)
+ *   max_iter        power iterations (>= 1)
+ *   S               device d x m x m;  U, V device N x m;  sigma device m (nonincreasing)
+ *   rank_out        host int32: detected rank r_1 (PRONY_ERR_RANK if < m)
+ *   resid_out       nullable host double: ||T V_k - U_k Q_k||_F / ||T||_F at exit
+ *   workspace       >= prony_workspace_size(PRONY_WS_BUILD)
+ * Returns PRONY_OK, PRONY_ERR_RANK (rank below m), PRONY_ERR_NOT_CONVERGED (residual above tol after
+ * max_iter; outputs are still written), or validation / CUDA errors.
  */
-int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t seed, prony_c128* S, prony_c128* U,
-                       prony_c128* V, double* sigma, int32_t* rank_out, void* workspace, size_t workspace_bytes,
-                       int32_t* dev_status, prony_stream_t stream);
+int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t seed, double tol, int max_iter,
+                       prony_c128* S, prony_c128* U, prony_c128* V, double* sigma, int32_t* rank_out,
+                       double* resid_out, void* workspace, size_t workspace_bytes, int32_t* dev_status,
+                       prony_stream_t stream);
+
+/*
+ * prony_diagonalize — Algorithm 1 lines 4-6: C_mu = sum_l mu_l S_l, W from the
+ * eigendecomposition of C_mu (Hessenberg + shifted QR + back substitution; unit columns), the
+ * simultaneous diagonalization z_tau(j)(l) = (W^-1 S_l W)_jj (by LU with partial pivoting)
+ * and t = (-arg z / 2 pi) mod 1 (R4). One small CTA; asynchronous.
+ *   S   device d x m x m;  mu device d (unit norm);  z device m x d;  t nullable device m x d;
+ *   W   device m x m (eigenvectors, columns);  workspace >= prony_workspace_size(PRONY_WS_DIAG)
+ *   dev_status: PRONY_ERR_NOT_CONVERGED (QR iteration cap) or PRONY_ERR_SINGULAR (W singular)
+ */
+int prony_diagonalize(int d, int m, const prony_c128* S, const prony_c128* mu, prony_c128* z, double* t, prony_c128* W,
+                      void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -8,8 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libprony.so")
-SOURCES = ["api.cu", "project.cu", "vandermonde_ls.cu"]
-HEADERS = ["common.cuh", "engine.cuh", "project.cuh", "vandermonde_ls.cuh"]
+SOURCES = ["api.cu", "project.cu", "vandermonde_ls.cu", "dense.cu", "svd.cu"]
+HEADERS = ["common.cuh", "engine.cuh", "project.cuh", "vandermonde_ls.cuh", "dense.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -23,14 +23,14 @@ PRONY_ERR_CUDA = 6
 PRONY_ERR_UNIMPLEMENTED = 7
 PRONY_ERR_WORKSPACE = 8
 
-WS_PROJECT, WS_LS, WS_PENCIL_HOST, WS_BUILD, WS_APPLY = 0, 1, 2, 3, 4
+WS_PROJECT, WS_LS, WS_PENCIL_HOST, WS_BUILD, WS_APPLY, WS_DIAG = 0, 1, 2, 3, 4, 5
 UNITS_L_MAJOR, UNITS_ROW_MAJOR = 0, 1
 MAX_D, MAX_M = 8, 128
 
 # every symbol include/prony.h declares (checked by tests/test_abi.py)
 EXPORTS = ("prony_abi_version", "prony_status_string", "prony_device_info", "prony_workspace_size",
            "prony_project", "prony_project_ex", "prony_vandermonde_ls", "prony_vandermonde_ls_ex", "prony_ls_solve",
-           "prony_toeplitz_apply", "prony_pencil_host", "prony_build_pencil")
+           "prony_toeplitz_apply", "prony_pencil_host", "prony_build_pencil", "prony_diagonalize")
 
 
 class ExecInfo(ctypes.Structure):
@@ -77,9 +77,11 @@ def lib() -> ctypes.CDLL:
         L.prony_ls_solve.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, sz, vp, vp]
         L.prony_toeplitz_apply.argtypes = [i32, i32, vp, i32, i32, vp, i32, i32, vp, i32, vp, sz, vp]
         L.prony_pencil_host.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp]
-        L.prony_build_pencil.argtypes = [i32, i32, i32, vp, ctypes.c_uint64, vp, vp, vp, vp, vp, vp, sz, vp, vp]
+        L.prony_build_pencil.argtypes = [i32, i32, i32, vp, ctypes.c_uint64, ctypes.c_double, i32, vp, vp, vp, vp, vp,
+                                         vp, vp, sz, vp, vp]
+        L.prony_diagonalize.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, sz, vp, vp]
         for f in ("prony_device_info", "prony_workspace_size", "prony_project", "prony_vandermonde_ls", "prony_ls_solve",
-                  "prony_project_ex", "prony_vandermonde_ls_ex", "prony_toeplitz_apply",
+                  "prony_project_ex", "prony_vandermonde_ls_ex", "prony_toeplitz_apply", "prony_diagonalize",
                   "prony_pencil_host", "prony_build_pencil"):
             getattr(L, f).restype = i32
         _lib = L
@@ -262,16 +264,44 @@ def pencil_host(grid, U, V, sigma, z, d: int, n: int, m: int, workspace=None, ou
     return outputs
 
 
-def build_pencil(grid, d: int, n: int, m: int, seed: int = 0):
-    """Device SVD + projection (NEXT-1): not in this round; raises PronyError(UNIMPLEMENTED)."""
+def build_pencil(grid, d: int, n: int, m: int, seed: int = 0, tol: float | None = None, max_iter: int = 4,
+                 workspace=None, stream=None, check: bool = True):
+    """Algorithm 1 lines 1-3 on the device: block power reduced SVD of T (Alg. 3) and
+    S_l = U* T_l V Sigma^-1. tol defaults to N eps_M. Synchronous. Returns a dict with
+    S (d,m,m), U, V (N,m), sigma (m,), rank, resid, status (PRONY_OK / _RANK / _NOT_CONVERGED)."""
+    _dev_tensor(grid, torch.complex128, "grid")
     N = (n + 1) ** d
+    if tol is None:
+        tol = N * 2.220446049250313e-16
     dev = grid.device
     S = torch.empty((d, m, m), dtype=torch.complex128, device=dev)
     U = torch.empty((N, m), dtype=torch.complex128, device=dev)
     V = torch.empty((N, m), dtype=torch.complex128, device=dev)
     s = torch.empty(m, dtype=torch.float64, device=dev)
-    r = torch.empty(1, dtype=torch.int32, device=dev)
-    rc = lib().prony_build_pencil(d, n, m, _ptr(grid), int(seed), _ptr(S), _ptr(U), _ptr(V), _ptr(s), _ptr(r),
-                                  None, 0, None, _stream(None))
-    _check(rc, "prony_build_pencil")
-    return S, U, V, s, r
+    rank = ctypes.c_int32(0)
+    resid = ctypes.c_double(-1.0)
+    if workspace is None:
+        workspace = alloc_workspace(WS_BUILD, d, n, m, dev)
+    rc = lib().prony_build_pencil(d, n, m, _ptr(grid), int(seed), float(tol), int(max_iter), _ptr(S), _ptr(U), _ptr(V),
+                                  _ptr(s), ctypes.byref(rank), ctypes.byref(resid), _ptr(workspace), workspace.numel(),
+                                  None, _stream(stream))
+    if check and rc not in (PRONY_OK, PRONY_ERR_NOT_CONVERGED, PRONY_ERR_RANK):
+        _check(rc, "prony_build_pencil")
+    return {"S": S, "U": U, "V": V, "sigma": s, "rank": rank.value, "resid": resid.value, "status": rc}
+
+
+def diagonalize(S, mu, d: int, m: int, workspace=None, dev_status=None, stream=None):
+    """Algorithm 1 lines 4-6 on the device: C_mu = sum mu_l S_l, W = eigenvectors, z = diag(W^-1 S_l W),
+    t = (-arg z / 2 pi) mod 1. Returns (z (m,d), t (m,d), W (m,m))."""
+    _dev_tensor(S, torch.complex128, "S")
+    _dev_tensor(mu, torch.complex128, "mu")
+    dev = S.device
+    z = torch.empty((m, d), dtype=torch.complex128, device=dev)
+    t = torch.empty((m, d), dtype=torch.float64, device=dev)
+    W = torch.empty((m, m), dtype=torch.complex128, device=dev)
+    if workspace is None:
+        workspace = alloc_workspace(WS_DIAG, d, m, m, dev)
+    rc = lib().prony_diagonalize(d, m, _ptr(S), _ptr(mu), _ptr(z), _ptr(t), _ptr(W), _ptr(workspace),
+                                 workspace.numel(), _ptr(dev_status), _stream(stream))
+    _check(rc, "prony_diagonalize")
+    return z, t, W

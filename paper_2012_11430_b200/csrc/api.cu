@@ -10,6 +10,7 @@
 #include "common.cuh"
 #include "project.cuh"
 #include "vandermonde_ls.cuh"
+#include "dense.cuh"
 
 using namespace prony;
 
@@ -135,7 +136,10 @@ int prony_workspace_size(int kind, int d, int n, int m, size_t* bytes) {
     case PRONY_WS_PROJECT: *bytes = ws_project(d, n, N, m, sms); return PRONY_OK;
     case PRONY_WS_LS: *bytes = ws_ls(d, n, m, sms); return PRONY_OK;
     case PRONY_WS_PENCIL_HOST: *bytes = host_layout(d, n, m, N, sms).total; return PRONY_OK;
-    case PRONY_WS_BUILD: *bytes = 0; return PRONY_OK;
+    case PRONY_WS_BUILD:
+      *bytes = std::max(svd_workspace_bytes(d, n, (int)N, m), ws_project(d, n, N, m, sms));
+      return PRONY_OK;
+    case PRONY_WS_DIAG: *bytes = diag_workspace_bytes(d, m); return PRONY_OK;
     case PRONY_WS_APPLY: *bytes = apply_workspace_bytes(d, n, (int)N); return PRONY_OK;
     default: return PRONY_ERR_INVALID;
   }
@@ -276,16 +280,49 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
   return PRONY_OK;
 }
 
-int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t seed, prony_c128* S, prony_c128* U,
-                       prony_c128* V, double* sigma, int32_t* rank_out, void* workspace, size_t workspace_bytes,
-                       int32_t* dev_status, prony_stream_t stream) {
-  (void)seed; (void)workspace_bytes; (void)dev_status; (void)stream;
+int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t seed, double tol, int max_iter,
+                       prony_c128* S, prony_c128* U, prony_c128* V, double* sigma, int32_t* rank_out,
+                       double* resid_out, void* workspace, size_t workspace_bytes, int32_t* dev_status,
+                       prony_stream_t stream) {
   int64_t N = 0;
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
-  if (!grid || !S || !U || !V || !sigma || !rank_out) return PRONY_ERR_INVALID;
-  (void)workspace;
-  return PRONY_ERR_UNIMPLEMENTED;
+  if (!grid || !S || !U || !V || !sigma || !rank_out || !workspace || max_iter < 1 || !(tol >= 0.0))
+    return PRONY_ERR_INVALID;
+  if (!aligned16(grid) || !aligned16(S) || !aligned16(U) || !aligned16(V) || ((uintptr_t)sigma & 7u) ||
+      ((uintptr_t)workspace & 255u))
+    return PRONY_ERR_INVALID;
+  if (2 * m > 256) return PRONY_ERR_RANGE;  // starting block 2m columns: Jacobi pair table limit
+  const int sms = sm_count_current();
+  if (sms <= 0) return PRONY_ERR_CUDA;
+  const size_t need = std::max(svd_workspace_bytes(d, n, (int)N, m), ws_project(d, n, N, m, sms));
+  if (workspace_bytes < need) return PRONY_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rank = 0, iters = 0;
+  double resid = -1.0;
+  const int src = block_power_svd(d, n, (int)N, (const double2*)grid, m, tol, max_iter, seed, (double2*)U,
+                                  (double2*)V, sigma, &rank, &iters, &resid, workspace, sms, st);
+  *rank_out = rank;
+  if (resid_out) *resid_out = resid;
+  if (src != PRONY_OK && src != PRONY_ERR_NOT_CONVERGED) return src;
+  rc = prony_project(d, n, m, grid, U, V, sigma, 0, (int64_t)d * N, PRONY_UNITS_L_MAJOR, S, workspace,
+                     workspace_bytes, dev_status, stream);
+  if (rc) return rc;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return PRONY_ERR_CUDA;
+  return src;
+}
+
+int prony_diagonalize(int d, int m, const prony_c128* S, const prony_c128* mu, prony_c128* z, double* t, prony_c128* W,
+                      void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream) {
+  if (d < 1 || d > PRONY_MAX_D || m < 1) return PRONY_ERR_INVALID;
+  if (m > PRONY_MAX_M) return PRONY_ERR_RANGE;
+  if (!S || !mu || !z || !W || !workspace) return PRONY_ERR_INVALID;
+  if (!aligned16(S) || !aligned16(mu) || !aligned16(z) || !aligned16(W) || (t && ((uintptr_t)t & 7u)) ||
+      ((uintptr_t)workspace & 255u))
+    return PRONY_ERR_INVALID;
+  if (workspace_bytes < diag_workspace_bytes(d, m)) return PRONY_ERR_WORKSPACE;
+  return diagonalize_launch(d, m, (const double2*)S, (const double2*)mu, (double2*)z, t, (double2*)W, workspace,
+                            dev_status, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -1,0 +1,764 @@
+// dense.cu — the small dense linear algebra of Algorithm 1 that runs on the device outside the
+// measured hot path (NEXT-1): tall-skinny Gram / Cholesky-QR with diagonal pivoting
+// (rank determination of the block power method, Alg. 3), the SVD of the projected
+// r x r matrix Q_k (one-sided Jacobi), the eigendecomposition of C_mu (Hessenberg reduction
+// + shifted QR + back substitution) and the simultaneous diagonalization W^-1 S_l W.
+// Everything is FP64 complex; the N-sized products use all SMs, the r x r / m x m algorithms run in
+// one CTA (or one warp) on L2-resident matrices. All matrices are row-major.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "dense.cuh"
+
+namespace prony {
+
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {  // c + a*b
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // conj(a) * b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  const double den = b.x * b.x + b.y * b.y;
+  return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double2 warp_sum2(double2 v) { return make_double2(warp_sum(v.x), warp_sum(v.y)); }
+
+// ---------------------------------------------------------------------------- random block
+// Seeded complex Gaussian entries from a counter-based generator (splitmix64 of (seed, index)) +
+// Box-Muller: the same block for the same seed on every GPU and run (R14: U0/V0 unspecified by P:181).
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__global__ void k_fill_random(int64_t count, uint64_t seed, double2* __restrict__ out, int rows, int cols, int ld) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h1 = splitmix64(seed ^ (2 * (uint64_t)e));
+    const uint64_t h2 = splitmix64(seed ^ (2 * (uint64_t)e + 1));
+    const double u1 = ((h1 >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    const double u2 = ((h2 >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    const double rr = sqrt(-2.0 * log(u1));
+    const int64_t r = e / cols, c = e % cols;
+    if (r < rows) out[r * ld + c] = make_double2(rr * cospi(2.0 * u2), rr * sinpi(2.0 * u2));
+  }
+}
+
+// ---------------------------------------------------------------------------- Gram
+// Gp[z][i][j] = sum_{k in slice z} conj(X[k][i]) Y[k][j]  (ri x rj; 32 x 32 output tile per CTA, DFMA)
+constexpr int kGT = 32;
+__global__ void __launch_bounds__(256) k_gram(int N, int ri, int rj, const double2* __restrict__ X, int ldx,
+                                             const double2* __restrict__ Y, int ldy, int KS,
+                                             double2* __restrict__ Gp) {
+  __shared__ double2 Xi[kGT][kGT + 1];
+  __shared__ double2 Xj[kGT][kGT + 1];
+  const int i0 = blockIdx.x * kGT, j0 = blockIdx.y * kGT, z = blockIdx.z;
+  const int k_begin = (int)((int64_t)N * z / KS), k_end = (int)((int64_t)N * (z + 1) / KS);
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  double2 acc[2][2];
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) acc[a][b] = make_double2(0.0, 0.0);
+  for (int k0 = k_begin; k0 < k_end; k0 += kGT) {
+    for (int e = threadIdx.x; e < kGT * kGT; e += 256) {
+      const int kk = e / kGT, c = e % kGT;
+      const int k = k0 + kk;
+      Xi[kk][c] = (k < k_end && i0 + c < ri) ? X[(size_t)k * ldx + i0 + c] : make_double2(0.0, 0.0);
+      Xj[kk][c] = (k < k_end && j0 + c < rj) ? Y[(size_t)k * ldy + j0 + c] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < kGT; ++kk) {
+      const double2 u0 = Xi[kk][ty], u1 = Xi[kk][ty + 16];
+      const double2 v0 = Xj[kk][tx], v1 = Xj[kk][tx + 16];
+      acc[0][0] = cfma(cconj(u0), v0, acc[0][0]);
+      acc[0][1] = cfma(cconj(u0), v1, acc[0][1]);
+      acc[1][0] = cfma(cconj(u1), v0, acc[1][0]);
+      acc[1][1] = cfma(cconj(u1), v1, acc[1][1]);
+    }
+    __syncthreads();
+  }
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) {
+      const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
+      if (i < ri && j < rj) Gp[((size_t)z * ri + i) * rj + j] = acc[a][b];
+    }
+}
+
+// out[e] = sum_{z < KS} parts[z * count + e]   (fixed order)
+__global__ void k_sum_parts(int64_t count, int KS, const double2* __restrict__ parts, double2* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int z = 0; z < KS; ++z) s = cadd(s, parts[(size_t)z * count + e]);
+    out[e] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------- small GEMM
+// Y[N x c] = alpha * X[N x r] M[r x c] + beta * Y   (64 x 32 output tile per CTA, DFMA)
+__global__ void __launch_bounds__(256) k_gemm_nm(int N, int r, int c, const double2* __restrict__ X, int ldx,
+                                                const double2* __restrict__ M, int ldm, double2* __restrict__ Y,
+                                                int ldy, double alpha, double beta) {
+  __shared__ double2 Xs[64][17];
+  __shared__ double2 Ms[16][33];
+  const int row0 = blockIdx.x * 64, col0 = blockIdx.y * 32;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 2 columns x 4 rows per thread
+  double2 acc[4][2];
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 2; ++b) acc[a][b] = make_double2(0.0, 0.0);
+  for (int k0 = 0; k0 < r; k0 += 16) {
+    for (int e = threadIdx.x; e < 64 * 16; e += 256) {
+      const int rr = e / 16, kk = e % 16;
+      const int row = row0 + rr, k = k0 + kk;
+      Xs[rr][kk] = (row < N && k < r) ? X[(size_t)row * ldx + k] : make_double2(0.0, 0.0);
+    }
+    for (int e = threadIdx.x; e < 16 * 32; e += 256) {
+      const int kk = e / 32, cc = e % 32;
+      const int k = k0 + kk, col = col0 + cc;
+      Ms[kk][cc] = (k < r && col < c) ? M[(size_t)k * ldm + col] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const double2 m0 = Ms[kk][tx], m1 = Ms[kk][tx + 16];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double2 x = Xs[ty + 16 * a][kk];
+        acc[a][0] = cfma(x, m0, acc[a][0]);
+        acc[a][1] = cfma(x, m1, acc[a][1]);
+      }
+    }
+    __syncthreads();
+  }
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 2; ++b) {
+      const int row = row0 + ty + 16 * a, col = col0 + tx + 16 * b;
+      if (row < N && col < c) {
+        double2* y = Y + (size_t)row * ldy + col;
+        const double2 old = beta != 0.0 ? *y : make_double2(0.0, 0.0);
+        *y = make_double2(alpha * acc[a][b].x + beta * old.x, alpha * acc[a][b].y + beta * old.y);
+      }
+    }
+}
+
+// ---------------------------------------------------------------------------- norms
+// parts[blockIdx] = sum of |X[k][j]|^2 over the block's elements (then summed in fixed order)
+__global__ void k_fro2_parts(int N, int c, const double2* __restrict__ X, int ldx, double* __restrict__ parts) {
+  __shared__ double red[32];
+  double s = 0.0;
+  const int64_t tot = (int64_t)N * c;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x)
+    s += cabs2(X[(e / c) * ldx + e % c]);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) parts[blockIdx.x] = v;
+  }
+}
+// ||T||_F^2 = sum over v in {-n..n}^d of |f(v)|^2 prod_i (n + 1 - |v_i|)   (T = [f(k-h)])
+__global__ void k_normT2_parts(int d, int n, int64_t box, const double2* __restrict__ grid, double* __restrict__ parts) {
+  __shared__ double red[32];
+  const int L = 2 * n + 2;
+  double s = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < box; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e;
+    double mult = 1.0;
+    for (int i = 0; i < d; ++i) {
+      const int v = (int)(r % L) - n;
+      r /= L;
+      mult *= (v > n) ? 0.0 : (double)(n + 1 - abs(v));
+    }
+    if (mult > 0.0) s += mult * cabs2(grid[e]);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) parts[blockIdx.x] = v;
+  }
+}
+__global__ void k_sum_doubles(int count, const double* __restrict__ parts, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < count; ++i) s += parts[i];
+    *out = s;
+  }
+}
+
+// ---------------------------------------------------------------------------- Cholesky with pivoting
+// One CTA. A (r x r, ld r) Hermitian PSD is overwritten: on exit its lower triangle holds L with
+// P^T A P = L L^H for the first `rank` columns. With pivot = 1 the largest remaining diagonal is
+// chosen at each step and the factorization stops at the first j where the trace of the remaining
+// Schur complement (= ||R(j:, j:)||_F^2 of the pivoted QR of the tall matrix) is
+// <= tol^2 * trace(A). Without pivoting it stops at a non-positive pivot. out[0] = rank, piv[r].
+__global__ void __launch_bounds__(512) k_chol_piv(int r, double2* __restrict__ A, int pivot, double tol,
+                                                  int* __restrict__ piv, int* __restrict__ rank_out) {
+  __shared__ double sval[512];
+  __shared__ int sidx[512];
+  __shared__ int s_p, s_stop;
+  __shared__ double s_tr0;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < r; i += nt) piv[i] = i;
+  // trace
+  double t = 0.0;
+  for (int i = tid; i < r; i += nt) t += A[(size_t)i * r + i].x;
+  sval[tid] = t;
+  __syncthreads();
+  for (int s = nt / 2; s > 0; s >>= 1) {
+    if (tid < s) sval[tid] += sval[tid + s];
+    __syncthreads();
+  }
+  if (tid == 0) s_tr0 = sval[0];
+  __syncthreads();
+  const double tr0 = s_tr0;
+  int rank = r;
+  for (int j = 0; j < r; ++j) {
+    // remaining trace and (optional) pivot = argmax remaining diagonal
+    double best = -1.0, tr = 0.0;
+    int bi = j;
+    for (int i = j + tid; i < r; i += nt) {
+      const double v = A[(size_t)i * r + i].x;
+      tr += v;
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+    sval[tid] = best;
+    sidx[tid] = bi;
+    __syncthreads();
+    for (int s = nt / 2; s > 0; s >>= 1) {
+      if (tid < s && (sval[tid + s] > sval[tid] || (sval[tid + s] == sval[tid] && sidx[tid + s] < sidx[tid]))) {
+        sval[tid] = sval[tid + s];
+        sidx[tid] = sidx[tid + s];
+      }
+      __syncthreads();
+    }
+    const int p = pivot ? sidx[0] : j;
+    __syncthreads();
+    sval[tid] = tr;
+    __syncthreads();
+    for (int s = nt / 2; s > 0; s >>= 1) {
+      if (tid < s) sval[tid] += sval[tid + s];
+      __syncthreads();
+    }
+    if (tid == 0) {
+      s_p = p;
+      const double trem = sval[0];
+      const double dj = A[(size_t)p * r + p].x;
+      s_stop = (pivot && trem <= tol * tol * tr0) || !(dj > 0.0);
+    }
+    __syncthreads();
+    if (s_stop) {
+      rank = j;
+      break;
+    }
+    if (p != j) {  // symmetric swap of rows/columns j and p (full rows: L part included)
+      for (int c = tid; c < r; c += nt) {
+        const double2 x = A[(size_t)j * r + c];
+        A[(size_t)j * r + c] = A[(size_t)p * r + c];
+        A[(size_t)p * r + c] = x;
+      }
+      __syncthreads();
+      for (int c = tid; c < r; c += nt) {
+        const double2 x = A[(size_t)c * r + j];
+        A[(size_t)c * r + j] = A[(size_t)c * r + p];
+        A[(size_t)c * r + p] = x;
+      }
+      if (tid == 0) {
+        const int x = piv[j];
+        piv[j] = piv[p];
+        piv[p] = x;
+      }
+      __syncthreads();
+    }
+    const double ljj = sqrt(A[(size_t)j * r + j].x);
+    const double inv = 1.0 / ljj;
+    __syncthreads();
+    if (tid == 0) A[(size_t)j * r + j] = make_double2(ljj, 0.0);
+    for (int i = j + 1 + tid; i < r; i += nt) A[(size_t)i * r + j] = cscale(A[(size_t)i * r + j], inv);
+    __syncthreads();
+    // trailing update of the full Hermitian block: A[i][k] -= L[i][j] conj(L[k][j])
+    const int w = r - j - 1;
+    for (int e = tid; e < w * w; e += nt) {
+      const int i = j + 1 + e / w, k = j + 1 + e % w;
+      const double2 li = A[(size_t)i * r + j], lk = A[(size_t)k * r + j];
+      double2 v = A[(size_t)i * r + k];
+      v.x -= li.x * lk.x + li.y * lk.y;
+      v.y -= li.y * lk.x - li.x * lk.y;
+      A[(size_t)i * r + k] = v;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *rank_out = rank;
+}
+
+// Rinv (k x k, ld ldr) = inverse of the upper-triangular R = L^H, L = lower triangle of A (ld r).
+// One thread per column c: back substitution R x = e_c.
+__global__ void k_trinv_from_lower(int r, int k, const double2* __restrict__ A, double2* __restrict__ Rinv, int ldr) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
+    for (int i = k - 1; i >= 0; --i) {
+      double2 s = make_double2(i == c ? 1.0 : 0.0, 0.0);
+      if (i < c) s = make_double2(0.0, 0.0);
+      if (i <= c) {
+        for (int q = i + 1; q <= c; ++q) {
+          // R[i][q] = conj(L[q][i])
+          const double2 Riq = cconj(A[(size_t)q * r + i]);
+          const double2 x = Rinv[(size_t)q * ldr + c];
+          s = csub(s, cmul(Riq, x));
+        }
+        s = cscale(s, 1.0 / A[(size_t)i * r + i].x);  // R[i][i] real positive
+      }
+      Rinv[(size_t)i * ldr + c] = s;
+    }
+  }
+}
+
+// Xout[:, j] = Xin[:, piv[j]] for j < k (column gather), row stride ld
+__global__ void k_gather_cols(int N, int k, const int* __restrict__ piv, const double2* __restrict__ Xin, int ldin,
+                              double2* __restrict__ Xout, int ldout) {
+  const int64_t tot = (int64_t)N * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / k;
+    const int j = (int)(e % k);
+    Xout[row * ldout + j] = Xin[row * ldin + piv[j]];
+  }
+}
+
+// ---------------------------------------------------------------------------- one-sided Jacobi SVD
+// One CTA. A (rows x cols, ld cols, rows >= cols) is overwritten by A V = U Sigma; V (cols x cols)
+// accumulates the rotations. Round-robin column pairs (one warp per pair), sweeps until every pair
+// satisfies |a_p^H a_q| <= eps * ||a_p|| ||a_q||. Then sigma_j = ||a_j||, U = a_j / sigma_j, sorted
+// descending (perm applied to U and V columns). Used for Q_k = U_Q Sigma V_Q^H (Alg. 3).
+__global__ void __launch_bounds__(1024) k_jacobi_svd(int rows, int cols, double2* __restrict__ A,
+                                                     double2* __restrict__ Vm, double* __restrict__ sigma,
+                                                     double2* __restrict__ Uout, double2* __restrict__ Vout,
+                                                     int* __restrict__ order, int max_sweeps) {
+  __shared__ int s_rot;
+  __shared__ int pairs[2][256];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int cp = cols + (cols & 1);  // even number of players (a virtual zero column if odd)
+  for (int e = tid; e < cols * cols; e += blockDim.x) Vm[e] = make_double2((e / cols) == (e % cols) ? 1.0 : 0.0, 0.0);
+  __syncthreads();
+  const double eps = 1e-15;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int round = 0; round < cp - 1; ++round) {
+      // tournament pairing: player 0 fixed, others rotate
+      for (int k = tid; k < cp / 2; k += blockDim.x) {
+        int a = (k == 0) ? 0 : 1 + (k - 1 + round) % (cp - 1);
+        int b = 1 + (cp - 2 - k + round) % (cp - 1);
+        pairs[0][k] = min(a, b);
+        pairs[1][k] = max(a, b);
+      }
+      __syncthreads();
+      for (int k = warp; k < cp / 2; k += nw) {
+        const int p = pairs[0][k], q = pairs[1][k];
+        if (q >= cols) continue;  // virtual column
+        double al = 0.0, be = 0.0;
+        double2 ga = make_double2(0.0, 0.0);
+        for (int i = lane; i < rows; i += 32) {
+          const double2 x = A[(size_t)i * cols + p], y = A[(size_t)i * cols + q];
+          al += cabs2(x);
+          be += cabs2(y);
+          ga = cadd(ga, cmulc(x, y));  // conj(a_p) a_q
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum2(ga);
+        const double ag = sqrt(cabs2(ga));
+        if (ag <= eps * sqrt(al * be) || ag == 0.0) continue;
+        if (lane == 0) s_rot = 1;
+        // rotation: [a_p a_q] <- [a_p a_q] J, J = [[c, -s e], [s conj(e), c]]... zeroing conj(a_p') a_q'
+        const double zeta = (be - al) / (2.0 * ag);
+        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+        const double2 ph = make_double2(ga.x / ag, ga.y / ag);  // e^{i phi}, ga = |ga| e^{i phi}
+        // a_p' = c a_p - s conj(ph) a_q ; a_q' = s ph a_p + c a_q
+        for (int i = lane; i < rows; i += 32) {
+          const double2 x = A[(size_t)i * cols + p], y = A[(size_t)i * cols + q];
+          const double2 phc = cconj(ph);
+          A[(size_t)i * cols + p] = csub(cscale(x, c), cscale(cmul(phc, y), s));
+          A[(size_t)i * cols + q] = cadd(cscale(cmul(ph, x), s), cscale(y, c));
+        }
+        for (int i = lane; i < cols; i += 32) {
+          const double2 x = Vm[(size_t)i * cols + p], y = Vm[(size_t)i * cols + q];
+          const double2 phc = cconj(ph);
+          Vm[(size_t)i * cols + p] = csub(cscale(x, c), cscale(cmul(phc, y), s));
+          Vm[(size_t)i * cols + q] = cadd(cscale(cmul(ph, x), s), cscale(y, c));
+        }
+      }
+      __syncthreads();
+    }
+    if (!s_rot) break;
+    __syncthreads();
+  }
+  // singular values and sort (descending, stable), U = A V columns normalized
+  for (int j = warp; j < cols; j += nw) {
+    double s2 = 0.0;
+    for (int i = lane; i < rows; i += 32) s2 += cabs2(A[(size_t)i * cols + j]);
+    s2 = warp_sum(s2);
+    if (lane == 0) sigma[j] = sqrt(s2);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int j = 0; j < cols; ++j) order[j] = j;
+    for (int a = 1; a < cols; ++a) {  // insertion sort on indices
+      const int key = order[a];
+      int b = a - 1;
+      while (b >= 0 && sigma[order[b]] < sigma[key]) {
+        order[b + 1] = order[b];
+        --b;
+      }
+      order[b + 1] = key;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < rows * cols; e += blockDim.x) {
+    const int i = e / cols, j = e % cols;
+    const int src = order[j];
+    const double sv = sigma[src];
+    const double2 a = A[(size_t)i * cols + src];
+    Uout[(size_t)i * cols + j] = sv > 0.0 ? cscale(a, 1.0 / sv) : make_double2(0.0, 0.0);
+  }
+  for (int e = tid; e < cols * cols; e += blockDim.x) {
+    const int i = e / cols, j = e % cols;
+    Vout[(size_t)i * cols + j] = Vm[(size_t)i * cols + order[j]];
+  }
+}
+
+// sigma_sorted[j] = sigma[order[j]]
+__global__ void k_permute_sigma(int cols, const double* __restrict__ sigma, const int* __restrict__ order,
+                                double* __restrict__ out) {
+  for (int j = threadIdx.x; j < cols; j += blockDim.x) out[j] = sigma[order[j]];
+}
+
+// ---------------------------------------------------------------------------- eig (one warp)
+// C (m x m, ld m) -> eigenvalues lam[m] and unit eigenvectors W (m x m, columns), via
+// Householder Hessenberg reduction, complex single-shift QR with Wilkinson shifts and deflation
+// (Schur form T = Z^H C Z), eigenvectors of T by back substitution, W = Z Y, normalized.
+// H and Z are in global memory (L1/L2), the warp updates rows/columns lane-parallel.
+__global__ void __launch_bounds__(32) k_eig(int m, double2* __restrict__ H, double2* __restrict__ Z,
+                                            double2* __restrict__ lam, double2* __restrict__ W,
+                                            int* __restrict__ status, int max_iter_per_eig) {
+  const int lane = threadIdx.x;
+  auto h = [&](int i, int j) -> double2& { return H[(size_t)i * m + j]; };
+  auto zz = [&](int i, int j) -> double2& { return Z[(size_t)i * m + j]; };
+  for (int e = lane; e < m * m; e += 32) Z[e] = make_double2((e / m) == (e % m) ? 1.0 : 0.0, 0.0);
+  __syncwarp();
+  // 1. Hessenberg reduction: for k, Householder on x = H[k+1:m, k]
+  for (int k = 0; k + 2 < m; ++k) {
+    double xn2 = 0.0;
+    for (int i = k + 1 + lane; i < m; i += 32) xn2 += cabs2(h(i, k));
+    xn2 = warp_sum(xn2);
+    const double xn = sqrt(xn2);
+    if (xn == 0.0) continue;
+    const double2 x0 = h(k + 1, k);
+    const double ax0 = sqrt(cabs2(x0));
+    const double2 ph = ax0 > 0.0 ? make_double2(x0.x / ax0, x0.y / ax0) : make_double2(1.0, 0.0);
+    // v = x + ph*||x|| e1, H = I - 2 v v^H / (v^H v)
+    const double2 v0 = cadd(x0, cscale(ph, xn));
+    __syncwarp();
+    if (lane == 0) h(k + 1, k) = v0;  // store v in place (column k below the subdiagonal)
+    __syncwarp();
+    double vn2 = 0.0;
+    for (int i = k + 1 + lane; i < m; i += 32) vn2 += cabs2(h(i, k));
+    vn2 = warp_sum(vn2);
+    const double tau = 2.0 / vn2;
+    // H <- P H: rows k+1..m-1, columns k+1..m-1 (column k handled below)
+    for (int j = k + 1; j < m; ++j) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int i = k + 1 + lane; i < m; i += 32) s = cadd(s, cmulc(h(i, k), h(i, j)));  // v^H col
+      s = warp_sum2(s);
+      s = cscale(s, tau);
+      for (int i = k + 1 + lane; i < m; i += 32) h(i, j) = csub(h(i, j), cmul(h(i, k), s));
+    }
+    __syncwarp();
+    // H <- H P: all rows, columns k+1..m-1
+    for (int i = 0; i < m; ++i) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int j = k + 1 + lane; j < m; j += 32) s = cadd(s, cmul(h(i, j), h(j, k)));  // row * v
+      s = warp_sum2(s);
+      s = cscale(s, tau);
+      for (int j = k + 1 + lane; j < m; j += 32) h(i, j) = csub(h(i, j), cmul(s, cconj(h(j, k))));
+    }
+    __syncwarp();
+    // Z <- Z P
+    for (int i = 0; i < m; ++i) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int j = k + 1 + lane; j < m; j += 32) s = cadd(s, cmul(zz(i, j), h(j, k)));
+      s = warp_sum2(s);
+      s = cscale(s, tau);
+      for (int j = k + 1 + lane; j < m; j += 32) zz(i, j) = csub(zz(i, j), cmul(s, cconj(h(j, k))));
+    }
+    __syncwarp();
+    // column k: H[k+1][k] = -ph ||x||, zeros below
+    const double2 newsub = cscale(ph, -xn);
+    for (int i = k + 1 + lane; i < m; i += 32) h(i, k) = (i == k + 1) ? newsub : make_double2(0.0, 0.0);
+    __syncwarp();
+  }
+  // 2. shifted QR on the Hessenberg matrix, active block [lo, hi]
+  double anorm = 0.0;
+  for (int e = lane; e < m * m; e += 32) anorm += cabs2(H[e]);
+  anorm = sqrt(warp_sum(anorm));
+  const double ulp = 2.220446049250313e-16;
+  int hi = m - 1, iter = 0, total = 0;
+  while (hi > 0) {
+    // find lo: smallest l such that subdiagonals lo+1..hi are not negligible
+    int lo = hi;
+    while (lo > 0) {
+      const double s = sqrt(cabs2(h(lo - 1, lo - 1))) + sqrt(cabs2(h(lo, lo)));
+      if (sqrt(cabs2(h(lo, lo - 1))) <= ulp * (s > 0.0 ? s : anorm)) break;
+      --lo;
+    }
+    __syncwarp();
+    if (lo > 0 && lane == 0) h(lo, lo - 1) = make_double2(0.0, 0.0);  // negligible: split
+    __syncwarp();
+    if (lo == hi) {  // deflate one eigenvalue
+      --hi;
+      iter = 0;
+      continue;
+    }
+    if (++iter > max_iter_per_eig || ++total > 30 * m * max_iter_per_eig) {
+      if (lane == 0) set_status(status, PRONY_ERR_NOT_CONVERGED);
+      break;
+    }
+    // Wilkinson shift from the trailing 2x2 of the active block; exceptional shift every 10 its
+    const double2 a = h(hi - 1, hi - 1), b = h(hi - 1, hi), c = h(hi, hi - 1), dd = h(hi, hi);
+    double2 mu;
+    if (iter % 10 == 0) {
+      mu = cadd(dd, make_double2(0.75 * sqrt(cabs2(c)), 0.0));
+    } else {
+      const double2 tr2 = cscale(cadd(a, dd), 0.5);
+      const double2 diff = cscale(csub(a, dd), 0.5);
+      const double2 disc = cadd(cmul(diff, diff), cmul(b, c));
+      // complex sqrt
+      const double r = sqrt(sqrt(cabs2(disc)));
+      const double th = 0.5 * atan2(disc.y, disc.x);
+      const double2 sq = make_double2(r * cos(th), r * sin(th));
+      const double2 m1 = cadd(tr2, sq), m2 = csub(tr2, sq);
+      mu = (cabs2(csub(m1, dd)) < cabs2(csub(m2, dd))) ? m1 : m2;
+    }
+    // implicit single-shift QR sweep via Givens rotations on [lo, hi]
+    for (int k = lo; k < hi; ++k) {
+      double2 x, y;
+      if (k == lo) {
+        x = csub(h(lo, lo), mu);
+        y = h(lo + 1, lo);
+      } else {
+        x = h(k, k - 1);
+        y = h(k + 1, k - 1);
+      }
+      const double nx = sqrt(cabs2(x) + cabs2(y));
+      if (nx == 0.0) continue;
+      // G = [[cc, s], [-conj(s), cc]] with cc real: G [x; y] = [nx'; 0]
+      const double ax = sqrt(cabs2(x));
+      double cc;
+      double2 s;
+      if (ax == 0.0) {
+        cc = 0.0;
+        s = cscale(cconj(y), 1.0 / sqrt(cabs2(y)));
+      } else {
+        cc = ax / nx;
+        const double2 ph = make_double2(x.x / ax, x.y / ax);
+        s = cscale(cmul(ph, cconj(y)), 1.0 / nx);
+      }
+      __syncwarp();
+      // rows k, k+1 (columns from max(lo, k-1) .. m-1)
+      for (int j = max(lo, k - 1) + lane; j < m; j += 32) {
+        const double2 u = h(k, j), v = h(k + 1, j);
+        h(k, j) = cadd(cscale(u, cc), cmul(s, v));
+        h(k + 1, j) = csub(cscale(v, cc), cmul(cconj(s), u));
+      }
+      __syncwarp();
+      // columns k, k+1 (rows 0 .. min(k+2, hi))
+      const int rmax = min(k + 2, hi);
+      for (int i = lane; i <= rmax; i += 32) {
+        const double2 u = h(i, k), v = h(i, k + 1);
+        h(i, k) = cadd(cscale(u, cc), cmul(cconj(s), v));
+        h(i, k + 1) = csub(cscale(v, cc), cmul(s, u));
+      }
+      for (int i = lane; i < m; i += 32) {
+        const double2 u = zz(i, k), v = zz(i, k + 1);
+        zz(i, k) = cadd(cscale(u, cc), cmul(cconj(s), v));
+        zz(i, k + 1) = csub(cscale(v, cc), cmul(s, u));
+      }
+      __syncwarp();
+      if (k > lo && lane == 0) h(k + 1, k - 1) = make_double2(0.0, 0.0);
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  // zero below the diagonal (numerically negligible after convergence)
+  for (int e = lane; e < m * m; e += 32)
+    if ((e / m) > (e % m)) H[e] = make_double2(0.0, 0.0);
+  __syncwarp();
+  for (int i = lane; i < m; i += 32) lam[i] = h(i, i);
+  __syncwarp();
+  // 3. eigenvectors of T (upper triangular): for each k, y_k = 1, y_i = -(sum_{j=i+1..k} T_ij y_j)/(T_ii - T_kk)
+  //    computed into W's column k (as Y), then W = Z Y in place column by column (Y kept in H's lower part? no:
+  //    use W as Y storage, then multiply).
+  const double small = ulp * (anorm > 0.0 ? anorm : 1.0);
+  for (int k = lane; k < m; k += 32) {
+    for (int i = m - 1; i > k; --i) W[(size_t)i * m + k] = make_double2(0.0, 0.0);
+    W[(size_t)k * m + k] = make_double2(1.0, 0.0);
+    const double2 lk = h(k, k);
+    for (int i = k - 1; i >= 0; --i) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int j = i + 1; j <= k; ++j) s = cadd(s, cmul(h(i, j), W[(size_t)j * m + k]));
+      double2 den = csub(h(i, i), lk);
+      if (sqrt(cabs2(den)) < small) den = make_double2(small, 0.0);
+      W[(size_t)i * m + k] = cscale(cdiv(s, den), -1.0);
+    }
+  }
+  __syncwarp();
+  // W = Z Y: Y is upper triangular (column k nonzero in rows 0..k); compute column by column from
+  // the last to the first, writing into H (free now) then copy with normalization
+  for (int k = 0; k < m; ++k) {
+    for (int i = lane; i < m; i += 32) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int j = 0; j <= k; ++j) s = cadd(s, cmul(zz(i, j), W[(size_t)j * m + k]));
+      h(i, k) = s;
+    }
+  }
+  __syncwarp();
+  for (int k = 0; k < m; ++k) {
+    double nn = 0.0;
+    for (int i = lane; i < m; i += 32) nn += cabs2(h(i, k));
+    nn = sqrt(warp_sum(nn));
+    const double inv = nn > 0.0 ? 1.0 / nn : 0.0;
+    for (int i = lane; i < m; i += 32) W[(size_t)i * m + k] = cscale(h(i, k), inv);
+  }
+}
+
+// ---------------------------------------------------------------------------- W^-1 S_l W diagonals
+// One CTA. LU with partial pivoting of W (m x m, in the scratch `LU`), then for every l:
+// X = W^-1 (S_l W) column by column, z[j][l] = X[j][j]. Also t = (-arg z / 2 pi) mod 1 (R4).
+__global__ void __launch_bounds__(256) k_diag_pencil(int d, int m, const double2* __restrict__ W,
+                                                    const double2* __restrict__ S, double2* __restrict__ LU,
+                                                    int* __restrict__ pv, double2* __restrict__ col,
+                                                    double2* __restrict__ z, double* __restrict__ t,
+                                                    int* __restrict__ status) {
+  __shared__ double sval[256];
+  __shared__ int sidx[256];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < m * m; e += nt) LU[e] = W[e];
+  for (int i = tid; i < m; i += nt) pv[i] = i;
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {
+    double best = -1.0;
+    int bi = j;
+    for (int i = j + tid; i < m; i += nt) {
+      const double v = cabs2(LU[(size_t)i * m + j]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+    sval[tid] = best;
+    sidx[tid] = bi;
+    __syncthreads();
+    for (int s = nt / 2; s > 0; s >>= 1) {
+      if (tid < s && sval[tid + s] > sval[tid]) {
+        sval[tid] = sval[tid + s];
+        sidx[tid] = sidx[tid + s];
+      }
+      __syncthreads();
+    }
+    const int p = sidx[0];
+    if (!(sval[0] > 0.0)) {
+      if (tid == 0) set_status(status, PRONY_ERR_SINGULAR);
+      return;
+    }
+    __syncthreads();
+    if (p != j) {
+      for (int c = tid; c < m; c += nt) {
+        const double2 x = LU[(size_t)j * m + c];
+        LU[(size_t)j * m + c] = LU[(size_t)p * m + c];
+        LU[(size_t)p * m + c] = x;
+      }
+      if (tid == 0) {
+        const int x = pv[j];
+        pv[j] = pv[p];
+        pv[p] = x;
+      }
+    }
+    __syncthreads();
+    const double2 piv = LU[(size_t)j * m + j];
+    for (int i = j + 1 + tid; i < m; i += nt) LU[(size_t)i * m + j] = cdiv(LU[(size_t)i * m + j], piv);
+    __syncthreads();
+    const int w = m - j - 1;
+    for (int e = tid; e < w * w; e += nt) {
+      const int i = j + 1 + e / w, k = j + 1 + e % w;
+      LU[(size_t)i * m + k] = csub(LU[(size_t)i * m + k], cmul(LU[(size_t)i * m + j], LU[(size_t)j * m + k]));
+    }
+    __syncthreads();
+  }
+  // z[jj][l] = e_jj^T W^-1 S_l W e_jj: solve W x = S_l w_jj (w_jj = column jj of W), take x[jj]
+  for (int l = 0; l < d; ++l) {
+    for (int jj = 0; jj < m; ++jj) {
+      // col = P (S_l w_jj)
+      for (int i = tid; i < m; i += nt) {
+        const int src = pv[i];
+        double2 s = make_double2(0.0, 0.0);
+        for (int k = 0; k < m; ++k) s = cadd(s, cmul(S[((size_t)l * m + src) * m + k], W[(size_t)k * m + jj]));
+        col[i] = s;
+      }
+      __syncthreads();
+      if (tid < 32) {  // forward (unit L) and backward (U) substitution, one warp
+        for (int i = 0; i < m; ++i) {
+          double2 s = make_double2(0.0, 0.0);
+          for (int k = tid; k < i; k += 32) s = cadd(s, cmul(LU[(size_t)i * m + k], col[k]));
+          s = warp_sum2(s);
+          if (tid == 0) col[i] = csub(col[i], s);
+          __syncwarp();
+        }
+        for (int i = m - 1; i >= jj; --i) {
+          double2 s = make_double2(0.0, 0.0);
+          for (int k = i + 1 + tid; k < m; k += 32) s = cadd(s, cmul(LU[(size_t)i * m + k], col[k]));
+          s = warp_sum2(s);
+          if (tid == 0) col[i] = cdiv(csub(col[i], s), LU[(size_t)i * m + i]);
+          __syncwarp();
+        }
+        if (tid == 0) {
+          const double2 zz = col[jj];
+          z[(size_t)jj * d + l] = zz;
+          if (t) {
+            double v = -atan2(zz.y, zz.x) * 0.15915494309189533577;
+            v = v - floor(v);
+            if (v >= 1.0) v = 0.0;
+            t[(size_t)jj * d + l] = v;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// C = sum_l mu_l S_l
+__global__ void k_combine(int d, int m, const double2* __restrict__ mu, const double2* __restrict__ S,
+                          double2* __restrict__ C) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * m; e += gridDim.x * blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int l = 0; l < d; ++l) s = cadd(s, cmul(mu[l], S[(size_t)l * m * m + e]));
+    C[e] = s;
+  }
+}
+
+}  // namespace prony

@@ -1,0 +1,40 @@
+// dense.cuh — small dense linear algebra kernels of NEXT-1 (dense.cu) and the block-power SVD /
+// diagonalization drivers (svd.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace prony {
+
+__global__ void k_fill_random(int64_t count, uint64_t seed, double2* out, int rows, int cols, int ld);
+__global__ void k_gram(int N, int ri, int rj, const double2* X, int ldx, const double2* Y, int ldy, int KS,
+                       double2* Gp);
+__global__ void k_sum_parts(int64_t count, int KS, const double2* parts, double2* out);
+__global__ void k_gemm_nm(int N, int r, int c, const double2* X, int ldx, const double2* M, int ldm, double2* Y,
+                          int ldy, double alpha, double beta);
+__global__ void k_fro2_parts(int N, int c, const double2* X, int ldx, double* parts);
+__global__ void k_normT2_parts(int d, int n, int64_t box, const double2* grid, double* parts);
+__global__ void k_sum_doubles(int count, const double* parts, double* out);
+__global__ void k_chol_piv(int r, double2* A, int pivot, double tol, int* piv, int* rank_out);
+__global__ void k_trinv_from_lower(int r, int k, const double2* A, double2* Rinv, int ldr);
+__global__ void k_gather_cols(int N, int k, const int* piv, const double2* Xin, int ldin, double2* Xout, int ldout);
+__global__ void k_jacobi_svd(int rows, int cols, double2* A, double2* Vm, double* sigma, double2* Uout, double2* Vout,
+                             int* order, int max_sweeps);
+__global__ void k_permute_sigma(int cols, const double* sigma, const int* order, double* out);
+__global__ void k_eig(int m, double2* H, double2* Z, double2* lam, double2* W, int* status, int max_iter_per_eig);
+__global__ void k_diag_pencil(int d, int m, const double2* W, const double2* S, double2* LU, int* pv, double2* col,
+                              double2* z, double* t, int* status);
+__global__ void k_combine(int d, int m, const double2* mu, const double2* S, double2* C);
+
+size_t svd_workspace_bytes(int d, int n, int N, int m);
+int block_power_svd(int d, int n, int N, const double2* grid, int m, double tol, int max_iter, uint64_t seed,
+                    double2* U, double2* V, double* sigma, int* rank_out, int* iters_out, double* resid_out, void* ws,
+                    int sm_count, cudaStream_t st);
+size_t diag_workspace_bytes(int d, int m);
+int diagonalize_launch(int d, int m, const double2* S, const double2* mu, double2* z, double* t, double2* W,
+                       void* ws, int32_t* status, cudaStream_t st);
+
+}  // namespace prony

@@ -61,8 +61,10 @@ def test_validation_before_any_cuda_call(pb):
     assert L.prony_ls_solve(0, 3, null, null, null, null, null, null, 0, null, null) == pb.PRONY_ERR_INVALID
     sz = ctypes.c_size_t()
     assert L.prony_workspace_size(0, 9, 4, 3, ctypes.byref(sz)) == pb.PRONY_ERR_INVALID
-    assert L.prony_build_pencil(2, 4, 3, null, 0, null, null, null, null, null, null, 0, null,
+    assert L.prony_build_pencil(2, 4, 3, null, 0, 0.0, 1, null, null, null, null, null, null, null, 0, null,
                                 null) == pb.PRONY_ERR_INVALID
+    assert L.prony_diagonalize(0, 3, null, null, null, null, null, null, 0, null, null) == pb.PRONY_ERR_INVALID
+    assert L.prony_toeplitz_apply(2, 4, null, 3, 0, null, 1, 1, null, 1, null, 0, null) == pb.PRONY_ERR_INVALID
 
 
 def test_misaligned_pointer_rejected(pb):
@@ -76,6 +78,7 @@ def test_misaligned_pointer_rejected(pb):
 
 
 def test_no_cpu_fallback_without_gpu(pb):
+    """Every compute entry point refuses CPU tensors (there is no CPU path)."""
     import torch
     if torch.cuda.is_available():
         pytest.skip("GPU present")
