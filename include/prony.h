@@ -218,7 +218,9 @@ int prony_toeplitz_apply(int d, int n, const prony_c128* grid, int ell, int conj
 /*
  * prony_pencil_host — one full pencil (prony_project over [0, dN) + prony_vandermonde_ls over
  * [0, N)) from HOST inputs to HOST outputs: copies grid, U, V, sigma, z host->device, runs the
- * device path on `stream`, copies S, G, b, c, t device->host and synchronizes `stream`.
+ * device path, copies S, G, b, c, t device->host and synchronizes `stream`. Internally a second
+ * stream (created and destroyed by the call, ordered after prior work on `stream`) carries the copy
+ * of U — first needed by the final reduction — and the LS step, so both overlap the projection.
  * Host buffers should be page-locked for full PCIe bandwidth (not required).
  *   host inputs : grid (L^d), U, V (N x m), sigma (m), z (m x d)
  *   host outputs: S (d x m x m), G (m x m), b (m), c (m), t (m x d); any output may be NULL

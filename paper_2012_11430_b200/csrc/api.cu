@@ -63,7 +63,7 @@ size_t ws_ls(int d, int n, int m, int sms) { return ls_workspace_bytes(d, n, m, 
 
 // device copies used by prony_pencil_host, carved from the front of its workspace
 struct HostLayout {
-  size_t grid, U, V, sigma, z, S, G, b, c, t, status, inner, total;
+  size_t grid, U, V, sigma, z, S, G, b, c, t, status, inner, inner_ls, total;
 };
 
 HostLayout host_layout(int d, int n, int m, int64_t N, int sms) {
@@ -87,8 +87,10 @@ HostLayout host_layout(int d, int n, int m, int64_t N, int sms) {
   h.c = take(m * sizeof(double2));
   h.t = take((size_t)m * d * sizeof(double));
   h.status = take(sizeof(int32_t));
-  h.inner = off;
-  off += std::max(ws_project(d, n, N, m, sms), ws_ls(d, n, m, sms));
+  h.inner = off;  // projection and LS run concurrently: separate scratch
+  off += align_up(ws_project(d, n, N, m, sms), 256);
+  h.inner_ls = off;
+  off += ws_ls(d, n, m, sms);
   h.total = off;
   return h;
 }
@@ -178,7 +180,7 @@ int prony_project_ex(int d, int n, int m, const prony_c128* grid, const prony_c1
   ProjPlan pl{};
   project_plan(g, sms, &pl);
   return project_launch(g, pl, (const double2*)grid, (const double2*)U, (const double2*)V, sigma, (double2*)S,
-                        workspace, sms, (cudaStream_t)stream, info);
+                        workspace, sms, (cudaStream_t)stream, info, nullptr);
 }
 
 int prony_vandermonde_ls(int d, int n, int m, const prony_c128* z, const prony_c128* grid, int64_t col_begin,
@@ -252,32 +254,70 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
   char* w = (char*)workspace;
   int64_t box = 1;
   for (int i = 0; i < d; ++i) box *= (2 * (int64_t)n + 2);
-  auto h2d = [&](size_t off, const void* src, size_t bytes) {
-    return cudaMemcpyAsync(w + off, src, bytes, cudaMemcpyHostToDevice, st) == cudaSuccess;
+  // Two streams, created for this call only: `st` carries grid/V/sigma -> the projection; `s2` carries
+  // U (needed only by k_reduce, so its copy overlaps k_project) and z -> the LS step (overlaps too).
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_grid = nullptr, ev_u = nullptr, ev_done = nullptr;
+  auto cleanup = [&]() {
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_grid) cudaEventDestroy(ev_grid);
+    if (ev_u) cudaEventDestroy(ev_u);
+    if (ev_done) cudaEventDestroy(ev_done);
+    if (s2) cudaStreamDestroy(s2);
   };
-  auto d2h = [&](void* dst, size_t off, size_t bytes) {
-    return dst == nullptr || cudaMemcpyAsync(dst, w + off, bytes, cudaMemcpyDeviceToHost, st) == cudaSuccess;
-  };
-  if (!h2d(h.grid, grid, box * sizeof(double2)) || !h2d(h.U, U, N * m * sizeof(double2)) ||
-      !h2d(h.V, V, N * m * sizeof(double2)) || !h2d(h.sigma, sigma, m * sizeof(double)) ||
-      !h2d(h.z, z, (size_t)m * d * sizeof(double2)))
+  if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ev_grid, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ev_u, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) != cudaSuccess) {
+    cleanup();
     return PRONY_ERR_CUDA;
-  if (cudaMemsetAsync(w + h.status, 0, sizeof(int32_t), st) != cudaSuccess) return PRONY_ERR_CUDA;
+  }
+  auto ok = [](cudaError_t e) { return e == cudaSuccess; };
+  bool good = ok(cudaEventRecord(ev_in, st)) && ok(cudaStreamWaitEvent(s2, ev_in, 0)) &&
+              ok(cudaMemsetAsync(w + h.status, 0, sizeof(int32_t), st)) &&
+              ok(cudaMemcpyAsync(w + h.grid, grid, box * sizeof(double2), cudaMemcpyHostToDevice, st)) &&
+              ok(cudaEventRecord(ev_grid, st)) &&
+              ok(cudaMemcpyAsync(w + h.V, V, N * m * sizeof(double2), cudaMemcpyHostToDevice, st)) &&
+              ok(cudaMemcpyAsync(w + h.sigma, sigma, m * sizeof(double), cudaMemcpyHostToDevice, st)) &&
+              ok(cudaMemcpyAsync(w + h.U, U, N * m * sizeof(double2), cudaMemcpyHostToDevice, s2)) &&
+              ok(cudaEventRecord(ev_u, s2)) &&
+              ok(cudaMemcpyAsync(w + h.z, z, (size_t)m * d * sizeof(double2), cudaMemcpyHostToDevice, s2)) &&
+              ok(cudaStreamWaitEvent(s2, ev_grid, 0));
+  if (!good) {
+    cleanup();
+    return PRONY_ERR_CUDA;
+  }
   int32_t* dst = (int32_t*)(w + h.status);
-  rc = prony_project(d, n, m, (const prony_c128*)(w + h.grid), (const prony_c128*)(w + h.U),
-                     (const prony_c128*)(w + h.V), (const double*)(w + h.sigma), 0, (int64_t)d * N,
-                     PRONY_UNITS_L_MAJOR, (prony_c128*)(w + h.S), w + h.inner, h.total - h.inner, dst, stream);
-  if (rc) return rc;
-  rc = prony_vandermonde_ls(d, n, m, (const prony_c128*)(w + h.z), (const prony_c128*)(w + h.grid), 0, N, nullptr,
-                            (prony_c128*)(w + h.G), (prony_c128*)(w + h.b), (prony_c128*)(w + h.c),
-                            (double*)(w + h.t), w + h.inner, h.total - h.inner, dst, stream);
-  if (rc) return rc;
-  if (!d2h(S, h.S, (size_t)d * m * m * sizeof(double2)) || !d2h(G, h.G, (size_t)m * m * sizeof(double2)) ||
-      !d2h(b, h.b, m * sizeof(double2)) || !d2h(c, h.c, m * sizeof(double2)) ||
-      !d2h(t, h.t, (size_t)m * d * sizeof(double)) || !d2h(status_out, h.status, sizeof(int32_t)))
-    return PRONY_ERR_CUDA;
-  if (cudaStreamSynchronize(st) != cudaSuccess) return PRONY_ERR_CUDA;
-  return PRONY_OK;
+  ProjGeom g{};
+  g.d = d;
+  g.n = n;
+  g.m = m;
+  g.N = (int)N;
+  unit_rows(d, N, 0, (int64_t)d * N, PRONY_UNITS_L_MAJOR, &g);
+  ProjPlan pl{};
+  project_plan(g, sms, &pl);
+  rc = project_launch(g, pl, (const double2*)(w + h.grid), (const double2*)(w + h.U), (const double2*)(w + h.V),
+                      (const double*)(w + h.sigma), (double2*)(w + h.S), w + h.inner, sms, st, nullptr, ev_u);
+  if (rc == PRONY_OK)
+    rc = ls_launch(d, n, m, (int)N, (const double2*)(w + h.z), (const double2*)(w + h.grid), 0, N, nullptr,
+                   (double2*)(w + h.G), (double2*)(w + h.b), (double2*)(w + h.c), (double*)(w + h.t),
+                   w + h.inner_ls, dst, sms, s2, nullptr);
+  if (rc != PRONY_OK) {
+    cudaStreamSynchronize(s2);
+    cleanup();
+    return rc;
+  }
+  auto d2h = [&](void* dstp, size_t off, size_t bytes, cudaStream_t s) {
+    return dstp == nullptr || cudaMemcpyAsync(dstp, w + off, bytes, cudaMemcpyDeviceToHost, s) == cudaSuccess;
+  };
+  good = d2h(G, h.G, (size_t)m * m * sizeof(double2), s2) && d2h(b, h.b, m * sizeof(double2), s2) &&
+         d2h(c, h.c, m * sizeof(double2), s2) && d2h(t, h.t, (size_t)m * d * sizeof(double), s2) &&
+         ok(cudaEventRecord(ev_done, s2)) && d2h(S, h.S, (size_t)d * m * m * sizeof(double2), st) &&
+         ok(cudaStreamWaitEvent(st, ev_done, 0)) && d2h(status_out, h.status, sizeof(int32_t), st) &&
+         ok(cudaStreamSynchronize(st));
+  cleanup();
+  return good ? PRONY_OK : PRONY_ERR_CUDA;
 }
 
 int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t seed, double tol, int max_iter,

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(512) k_chol_piv(int r, double2* __restrict__ A
                                                   int* __restrict__ piv, int* __restrict__ rank_out) {
   __shared__ double sval[512];
   __shared__ int sidx[512];
-  __shared__ int s_p, s_stop;
+  __shared__ int s_stop;
   __shared__ double s_tr0;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int i = tid; i < r; i += nt) piv[i] = i;
@@ -257,7 +257,6 @@ __global__ void __launch_bounds__(512) k_chol_piv(int r, double2* __restrict__ A
       __syncthreads();
     }
     if (tid == 0) {
-      s_p = p;
       const double trem = sval[0];
       const double dj = A[(size_t)p * r + p].x;
       s_stop = (pivot && trem <= tol * tol * tr0) || !(dj > 0.0);

@@ -81,7 +81,6 @@ __global__ void k_prep(int d, int n, int N, int m, int ldv, int NP, int64_t box,
 constexpr int kConsumerWarps = PRONY_CONSUMER_WARPS;    // 12 (3 warpgroups) or 8 (2 warpgroups)
 constexpr int kThreads = 32 * (kConsumerWarps + 4);     // + the producer warpgroup
 constexpr int kReduceThreads = 512;
-constexpr int kProducerThreads = 128;
 constexpr int kGatherThreads = 96;  // producer threads doing the A gather (warp 3 issues the B bulk copies)
 #ifndef PRONY_CONSUMER_REGS
 #define PRONY_CONSUMER_REGS (PRONY_CONSUMER_WARPS == 12 ? 160 : 232)
@@ -606,7 +605,7 @@ static int launch_reduce_t(const RedParams& r, dim3 rgrid, cudaStream_t st, int 
 
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
                    const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
-                   prony_exec_info* info) {
+                   prony_exec_info* info, cudaEvent_t wait_before_reduce) {
   const WsLayout wl = ws_layout(g.d, g.n, g.N, g.m, sm_count);
   char* w = (char*)ws;
   int32_t* ptab = (int32_t*)(w + wl.ptab);
@@ -698,6 +697,8 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
       return PRONY_ERR_RANGE;
   }
   if (lrc != PRONY_OK) return lrc;
+  // U is first read by k_reduce: a caller may still be copying it on another stream
+  if (wait_before_reduce && cudaStreamWaitEvent(st, wait_before_reduce, 0) != cudaSuccess) return PRONY_ERR_CUDA;
   switch (pl.shape.rWN * 16 + pl.shape.rNT) {
 #define PRONY_RCASE(nt, wn) \
   case wn * 16 + nt:        \
