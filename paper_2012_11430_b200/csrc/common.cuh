@@ -11,6 +11,23 @@ namespace prony {
 
 constexpr int kWarp = 32;
 
+// Debug builds (-DPRONY_DEBUG, tools/ab_variants.py "debug"): index checks on the gather paths count
+// violations in a device counter (read with prony_debug_violations()) and clamp the access instead of
+// faulting. Release builds compile the checks away.
+#ifdef PRONY_DEBUG
+#define PRONY_CHECK_INDEX(idx, lo, hi)                          \
+  do {                                                          \
+    if ((idx) < (lo) || (idx) >= (hi)) {                        \
+      atomicAdd(&::prony::g_prony_violations, 1ull);            \
+      (idx) = (lo);                                             \
+    }                                                           \
+  } while (0)
+#else
+#define PRONY_CHECK_INDEX(idx, lo, hi) \
+  do {                                 \
+  } while (0)
+#endif
+
 __device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {

@@ -21,6 +21,10 @@
 
 namespace prony {
 
+#ifdef PRONY_DEBUG
+__device__ unsigned long long g_prony_violations = 0;  // gather-index violations (debug builds only)
+#endif
+
 // complex product formulation: 3 (Gauss/3M, default) or 4 (4M); env PRONY_CMUL=4m selects 4M
 static int cmul_mode() {
   const char* e = getenv("PRONY_CMUL");
@@ -186,7 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
           const int phc = __shfl_sync(0xffffffffu, ph, kc);
           const int pa = sPA[ra];
           const bool ok = (pa >= 0) && (h0 + kc < h_end);
-          const int idx = ok ? pa - phc : 0;
+          int idx = ok ? pa - phc : 0;
+          PRONY_CHECK_INDEX(idx, 0, p.box);
           cp_async16(st + (uint32_t)(T::A_C + 2 * (kc * T::LDA + ra)) * 8u, grid + idx, ok ? 16 : 0);
           if constexpr (MODE == 3)
             cp_async8(st + (uint32_t)(T::A_S + kc * T::LDAS + ra) * 8u, gsum + idx, ok ? 8 : 0);
@@ -649,6 +654,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   p.KC = pl.KC;
   p.nrb = nrb;
   p.counters = counters;
+  p.box = (int)box;
   const int L = 2 * g.n + 2;
   int64_t C0 = 0, s = 1;
   for (int i = 0; i < g.d; ++i) {
@@ -843,6 +849,7 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
     p.KC = pl.KC;
     p.nrb = nrb;
     p.counters = counters;
+    p.box = (int)box;
     p.kb[0] = 0;
     p.rows[0] = N;
     p.yoff[0] = 0;
@@ -875,3 +882,13 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
 }
 
 }  // namespace prony
+
+#ifdef PRONY_DEBUG
+// debug builds only (not part of the ABI in prony.h): gather-index violations seen so far
+extern "C" unsigned long long prony_debug_violations(void) {
+  unsigned long long v = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&v, prony::g_prony_violations, sizeof(v));
+  return v;
+}
+#endif

@@ -45,6 +45,7 @@ struct ProjParams {
   double2* Y;
   int* counters;  // [d][nrb] split-K arrival counters (zeroed per call)
   int N, m, NP, chunk_w, R_tot, KC, nrb;
+  int box;  // grid size (debug index checks)
   int kb[PRONY_MAX_D], rows[PRONY_MAX_D], yoff[PRONY_MAX_D], shift[PRONY_MAX_D];
 };
 

@@ -9,6 +9,7 @@ sys.path.insert(0, ROOT)
 from paper_2012_11430_b200 import _build  # noqa: E402
 
 VARIANTS = {
+    "debug": ["PRONY_DEBUG"],
     "w8": ["PRONY_CONSUMER_WARPS=8"],
     "w8r224": ["PRONY_CONSUMER_WARPS=8", "PRONY_CONSUMER_REGS=224", "PRONY_PRODUCER_REGS=40"],
     "base": [],
