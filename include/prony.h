@@ -94,7 +94,8 @@ typedef enum prony_workspace_kind {
   PRONY_WS_PENCIL_HOST = 2,  /* prony_pencil_host: device copies of inputs/outputs + both above */
   PRONY_WS_BUILD = 3,        /* prony_build_pencil */
   PRONY_WS_APPLY = 4,        /* prony_toeplitz_apply, any r */
-  PRONY_WS_DIAG = 5          /* prony_diagonalize */
+  PRONY_WS_DIAG = 5,         /* prony_diagonalize */
+  PRONY_WS_PROJECT_MU = 6    /* prony_project_mu */
 } prony_workspace_kind;
 
 /* unit orders of prony_project: units u in [0, d*N) */
@@ -201,6 +202,18 @@ int prony_vandermonde_ls_ex(int d, int n, int m, const prony_c128* z, const pron
  */
 int prony_ls_solve(int d, int m, const prony_c128* G, const prony_c128* b, const prony_c128* z, prony_c128* c,
                    double* t, void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream);
+
+/*
+ * prony_project_mu — C_mu = U* B_mu V Sigma^-1 with B_mu = sum_l mu_l T_l (the paper's B_mu
+ * preprocessing; NEXT-4): B_mu is itself the Toeplitz operator of the combined grid
+ * g_mu[x] = sum_l mu_l grid[x + L^(d-l)], so C_mu costs one projection instead of d. Equal to
+ * sum_l mu_l S_l in exact arithmetic (R8).
+ *   mu         device d prony_c128;  C device m x m (overwritten)
+ *   workspace  >= prony_workspace_size(PRONY_WS_PROJECT_MU)
+ */
+int prony_project_mu(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
+                     const double* sigma, const prony_c128* mu, prony_c128* C, void* workspace, size_t workspace_bytes,
+                     int32_t* dev_status, prony_stream_t stream);
 
 /*
  * prony_toeplitz_apply — Y = T_l X (l = 1..d), Y = T X (l = 0) or, with conj = 1 and l = 0,

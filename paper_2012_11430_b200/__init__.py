@@ -11,7 +11,7 @@ from .binding import (  # noqa: F401
     PRONY_ERR_UNIMPLEMENTED, PRONY_ERR_WORKSPACE, PRONY_OK, UNITS_L_MAJOR, UNITS_ROW_MAJOR, WS_LS,
     WS_PENCIL_HOST, WS_PROJECT, PronyError, alloc_workspace, build_pencil, device_info, lib, ls_solve,
     pencil_host, project, status_string, toeplitz_apply, vandermonde_ls, workspace_size,
-    WS_APPLY, WS_DIAG, diagonalize, PRONY_ERR_RANK, PRONY_ERR_NOT_CONVERGED, WS_BUILD,
+    WS_APPLY, WS_DIAG, WS_PROJECT_MU, project_mu, diagonalize, PRONY_ERR_RANK, PRONY_ERR_NOT_CONVERGED, WS_BUILD,
 )
 from . import sharding  # noqa: F401
 

@@ -23,14 +23,15 @@ PRONY_ERR_CUDA = 6
 PRONY_ERR_UNIMPLEMENTED = 7
 PRONY_ERR_WORKSPACE = 8
 
-WS_PROJECT, WS_LS, WS_PENCIL_HOST, WS_BUILD, WS_APPLY, WS_DIAG = 0, 1, 2, 3, 4, 5
+WS_PROJECT, WS_LS, WS_PENCIL_HOST, WS_BUILD, WS_APPLY, WS_DIAG, WS_PROJECT_MU = 0, 1, 2, 3, 4, 5, 6
 UNITS_L_MAJOR, UNITS_ROW_MAJOR = 0, 1
 MAX_D, MAX_M = 8, 128
 
 # every symbol include/prony.h declares (checked by tests/test_abi.py)
 EXPORTS = ("prony_abi_version", "prony_status_string", "prony_device_info", "prony_workspace_size",
            "prony_project", "prony_project_ex", "prony_vandermonde_ls", "prony_vandermonde_ls_ex", "prony_ls_solve",
-           "prony_toeplitz_apply", "prony_pencil_host", "prony_build_pencil", "prony_diagonalize")
+           "prony_toeplitz_apply", "prony_pencil_host", "prony_build_pencil", "prony_diagonalize",
+           "prony_project_mu")
 
 
 class ExecInfo(ctypes.Structure):
@@ -80,8 +81,10 @@ def lib() -> ctypes.CDLL:
         L.prony_build_pencil.argtypes = [i32, i32, i32, vp, ctypes.c_uint64, ctypes.c_double, i32, vp, vp, vp, vp, vp,
                                          vp, vp, sz, vp, vp]
         L.prony_diagonalize.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, sz, vp, vp]
+        L.prony_project_mu.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp]
         for f in ("prony_device_info", "prony_workspace_size", "prony_project", "prony_vandermonde_ls", "prony_ls_solve",
                   "prony_project_ex", "prony_vandermonde_ls_ex", "prony_toeplitz_apply", "prony_diagonalize",
+                  "prony_project_mu",
                   "prony_pencil_host", "prony_build_pencil"):
             getattr(L, f).restype = i32
         _lib = L
@@ -216,6 +219,21 @@ def ls_solve(G, b, z, d: int, m: int, want_t: bool = True, workspace=None, dev_s
                               _ptr(dev_status), _stream(stream))
     _check(rc, "prony_ls_solve")
     return c, t
+
+
+def project_mu(grid, U, V, sigma, mu, d: int, n: int, m: int, out=None, workspace=None, stream=None):
+    """C_mu = U* B_mu V Sigma^-1, B_mu = sum_l mu_l T_l: one projection on the combined grid."""
+    for t_, nm in ((grid, "grid"), (U, "U"), (V, "V"), (mu, "mu")):
+        _dev_tensor(t_, torch.complex128, nm)
+    _dev_tensor(sigma, torch.float64, "sigma")
+    if out is None:
+        out = torch.empty((m, m), dtype=torch.complex128, device=grid.device)
+    if workspace is None:
+        workspace = alloc_workspace(WS_PROJECT_MU, d, n, m, grid.device)
+    rc = lib().prony_project_mu(d, n, m, _ptr(grid), _ptr(U), _ptr(V), _ptr(sigma), _ptr(mu), _ptr(out),
+                                _ptr(workspace), workspace.numel(), None, _stream(stream))
+    _check(rc, "prony_project_mu")
+    return out
 
 
 def toeplitz_apply(grid, X, d: int, n: int, ell: int = 0, conj: bool = False, out=None, workspace=None,

@@ -60,6 +60,12 @@ void unit_rows(int d, int64_t N, int64_t u0, int64_t u1, int order, ProjGeom* g)
 
 size_t ws_project(int d, int n, int64_t N, int m, int sms) { return project_workspace_bytes(d, n, (int)N, m, sms); }
 size_t ws_ls(int d, int n, int m, int sms) { return ls_workspace_bytes(d, n, m, sms); }
+size_t ws_project_mu(int d, int n, int64_t N, int m, int sms) {
+  int64_t box = 1;
+  for (int i = 0; i < d; ++i) box *= (2 * (int64_t)n + 2);
+  return align_up(ws_project(d, n, N, m, sms), 256) + align_up((size_t)box * sizeof(double2), 256) +
+         align_up((size_t)d * m * m * sizeof(double2), 256);
+}
 
 // device copies used by prony_pencil_host, carved from the front of its workspace
 struct HostLayout {
@@ -142,6 +148,7 @@ int prony_workspace_size(int kind, int d, int n, int m, size_t* bytes) {
       *bytes = std::max(svd_workspace_bytes(d, n, (int)N, m), ws_project(d, n, N, m, sms));
       return PRONY_OK;
     case PRONY_WS_DIAG: *bytes = diag_workspace_bytes(d, m); return PRONY_OK;
+    case PRONY_WS_PROJECT_MU: *bytes = ws_project_mu(d, n, N, m, sms); return PRONY_OK;
     case PRONY_WS_APPLY: *bytes = apply_workspace_bytes(d, n, (int)N); return PRONY_OK;
     default: return PRONY_ERR_INVALID;
   }
@@ -219,6 +226,45 @@ int prony_ls_solve(int d, int m, const prony_c128* G, const prony_c128* b, const
     return PRONY_ERR_INVALID;
   return ls_solve_launch(d, m, (const double2*)G, (const double2*)b, (const double2*)z, (double2*)c, t, workspace,
                          dev_status, (cudaStream_t)stream);
+}
+
+int prony_project_mu(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
+                     const double* sigma, const prony_c128* mu, prony_c128* C, void* workspace, size_t workspace_bytes,
+                     int32_t* dev_status, prony_stream_t stream) {
+  (void)dev_status;
+  int64_t N = 0;
+  int rc = validate_dnm(d, n, m, &N);
+  if (rc) return rc;
+  if (!grid || !U || !V || !sigma || !mu || !C || !workspace) return PRONY_ERR_INVALID;
+  if (!aligned16(grid) || !aligned16(U) || !aligned16(V) || !aligned16(mu) || !aligned16(C) || ((uintptr_t)sigma & 7u) ||
+      ((uintptr_t)workspace & 255u))
+    return PRONY_ERR_INVALID;
+  const int sms = sm_count_current();
+  if (sms <= 0) return PRONY_ERR_CUDA;
+  if (workspace_bytes < ws_project_mu(d, n, N, m, sms)) return PRONY_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)workspace;
+  const size_t off_g = align_up(ws_project(d, n, N, m, sms), 256);
+  int64_t box = 1;
+  for (int i = 0; i < d; ++i) box *= (2 * (int64_t)n + 2);
+  const size_t off_s = off_g + align_up((size_t)box * sizeof(double2), 256);
+  double2* gmu = (double2*)(w + off_g);
+  double2* Sd = (double2*)(w + off_s);
+  k_combine_grid<<<2 * sms, 256, 0, st>>>(d, n, box, (const double2*)grid, (const double2*)mu, gmu);
+  ProjGeom g{};
+  g.d = d;
+  g.n = n;
+  g.m = m;
+  g.N = (int)N;
+  g.kb[0] = 0;
+  g.rows[0] = (int)N;  // one segment: the l = 0 operator on the combined grid
+  ProjPlan pl{};
+  project_plan(g, sms, &pl);
+  rc = project_launch(g, pl, gmu, (const double2*)U, (const double2*)V, sigma, Sd, w, sms, st, nullptr, nullptr, 0);
+  if (rc) return rc;
+  if (cudaMemcpyAsync(C, Sd, (size_t)m * m * sizeof(double2), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return PRONY_ERR_CUDA;
+  return PRONY_OK;
 }
 
 int prony_toeplitz_apply(int d, int n, const prony_c128* grid, int ell, int conj, const prony_c128* X, int ldx, int r,

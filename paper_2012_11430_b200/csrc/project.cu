@@ -610,7 +610,7 @@ static int launch_reduce_t(const RedParams& r, dim3 rgrid, cudaStream_t st, int 
 
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
                    const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
-                   prony_exec_info* info, cudaEvent_t wait_before_reduce) {
+                   prony_exec_info* info, cudaEvent_t wait_before_reduce, int ell_base) {
   const WsLayout wl = ws_layout(g.d, g.n, g.N, g.m, sm_count);
   char* w = (char*)ws;
   int32_t* ptab = (int32_t*)(w + wl.ptab);
@@ -665,7 +665,8 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
     p.kb[l] = g.kb[l];
     p.rows[l] = g.rows[l];
     p.yoff[l] = pl.yoff[l];
-    p.shift[l] = (int)(ipow(L, g.d - 1 - l) + C0);  // s_l = L^(d-l) for l = 1..d
+    const int ell = l + ell_base;  // segment l holds T_ell (ell_base 1: S_1..S_d; 0: segment 0 is T)
+    p.shift[l] = (int)(C0 + (ell >= 1 ? ipow(L, g.d - ell) : 0));  // s_ell = L^(d-ell)
   }
   RedParams r{};
   r.Y = Y;
@@ -729,6 +730,23 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   }
   if (cudaGetLastError() != cudaSuccess) return PRONY_ERR_CUDA;
   return PRONY_OK;
+}
+
+// ---------------------------------------------------------------------------- B_mu (NEXT-4)
+// g_mu[x] = sum_l mu_l g[x + s_l]: B_mu = sum_l mu_l T_l is the Toeplitz operator
+// [g_mu[P(k) - P(h) + C0]], so C_mu = U* B_mu V Sigma^-1 is ONE projection on the combined grid.
+__global__ void k_combine_grid(int d, int n, int64_t box, const double2* __restrict__ grid,
+                               const double2* __restrict__ mu, double2* __restrict__ out) {
+  const int L = 2 * n + 2;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < box; x += (int64_t)gridDim.x * blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    int64_t sl = 1;
+    for (int l = d; l >= 1; --l) {  // s_l = L^(d-l)
+      if (x + sl < box) s = cadd(s, cmul(mu[l - 1], grid[x + sl]));
+      sl *= L;
+    }
+    out[x] = s;
+  }
 }
 
 // ---------------------------------------------------------------------------- Toeplitz apply

@@ -168,6 +168,19 @@ def test_project_spectrum_recovers_nodes(pb):
             assert np.min(np.abs(ev - zj)) < 1e-10
 
 
+# ------------------------------------------------------------------ NEXT-4: B_mu / C_mu in one projection
+@pytest.mark.parametrize("d,n,m,noise", [(2, 12, 9, 1e-6), (3, 5, 20, 0.0), (1, 30, 4, 1e-6), (4, 3, 7, 0.0)])
+def test_project_mu_equals_combination(pb, orc, d, n, m, noise):
+    """C_mu = U* (sum mu_l T_l) V Sigma^-1 equals sum_l mu_l S_l of the oracle."""
+    prob = problem(d, n, m, 3300 + d + n + m, noise, random_uv=True)
+    mu = orc.random_mu(d, 9)
+    C = pb.project_mu(dev(prob.grid), dev(prob.U), dev(prob.V), dev(prob.sigma), dev(mu), d, n, m)
+    torch.cuda.synchronize()
+    S_or = orc.project(prob.grid, prob.U, prob.V, prob.sigma, d, n)
+    want = np.tensordot(mu, S_or, axes=1)
+    assert rel(C, want) <= TOL
+
+
 # ------------------------------------------------------------------ Toeplitz apply (NEXT-1 operator)
 @pytest.mark.parametrize("d,n,r,noise", [(2, 7, 5, 1e-6), (3, 4, 130, 0.0), (1, 30, 3, 1e-3), (4, 3, 17, 1e-6)])
 def test_toeplitz_apply_dense_oracle(pb, orc, d, n, r, noise):
