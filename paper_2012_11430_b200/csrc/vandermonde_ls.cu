@@ -167,51 +167,44 @@ __global__ void k_ls_reduce(int m, int CB, const double2* __restrict__ Gpart, co
   }
 }
 
-// One CTA of kSolveThreads. The lower triangle of G lives packed in shared memory (L[i][k] at
-// i(i+1)/2 + k); right-looking Cholesky (column j: pivot, scale the column, rank-1 update of the
-// trailing triangle), then column-oriented forward / backward substitution.
+// One CTA of kSolveThreads. The lower triangle of G lives packed in shared memory (A[i][k] at
+// i(i+1)/2 + k). Right-looking Cholesky G = L L^H with lazily scaled columns: column j is never
+// rescaled in place, L[i][j] = A[i][j] / sqrt(d_j) with d_j the pivot (inv[j] = 1/sqrt(d_j)), so each
+// column costs ONE barrier (the trailing update reads column j and writes columns > j only).
+// Forward / backward substitution run in one warp with the right-hand side in registers.
+constexpr int kSolveMaxRowsPerLane = (PRONY_MAX_M + 31) / 32;
 __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const double2* __restrict__ G,
                                                          const double2* __restrict__ b,
                                                          const double2* __restrict__ z, double2* __restrict__ c,
                                                          double* __restrict__ t, int32_t* status) {
-  extern __shared__ __align__(16) double2 Ls[];  // m(m+1)/2 packed + y[m]
-  double2* y = Ls + (size_t)m * (m + 1) / 2;
+  extern __shared__ __align__(16) double2 As[];  // m(m+1)/2 packed
+  __shared__ double inv[PRONY_MAX_M];
   __shared__ int bad;
   const int tid = threadIdx.x;
   auto at = [](int i, int k) { return i * (i + 1) / 2 + k; };
   if (tid == 0) bad = 0;
-  for (int i = tid; i < m; i += kSolveThreads) {
-    for (int k = 0; k <= i; ++k) Ls[at(i, k)] = G[(size_t)i * m + k];
-    y[i] = b[i];
-  }
+  for (int i = tid; i < m; i += kSolveThreads)
+    for (int k = 0; k <= i; ++k) As[at(i, k)] = G[(size_t)i * m + k];
   __syncthreads();
   for (int j = 0; j < m; ++j) {
-    const double djj = Ls[at(j, j)].x;
-    if (!(djj > 0.0)) {  // uniform branch: every thread read the same value
+    const double dj = As[at(j, j)].x;  // final after the previous barrier
+    if (!(dj > 0.0)) {                 // uniform: every thread read the same value
       if (tid == 0) bad = 1;
       break;
     }
-    const double ljj = sqrt(djj);
-    const double inv = 1.0 / ljj;
-    __syncthreads();
-    if (tid == 0) Ls[at(j, j)] = make_double2(ljj, 0.0);
-    for (int i = j + 1 + tid; i < m; i += kSolveThreads) {
-      const double2 v = Ls[at(i, j)];
-      Ls[at(i, j)] = make_double2(v.x * inv, v.y * inv);
-    }
-    __syncthreads();
-    // trailing update: L[i][k] -= L[i][j] conj(L[k][j]), j < k <= i
+    const double invd = 1.0 / dj;  // L[i][j] conj(L[k][j]) = A[i][j] conj(A[k][j]) / d_j
+    if (tid == 0) inv[j] = sqrt(invd);
     const int r = m - j - 1;
     for (int ii = tid / 8; ii < r; ii += kSolveThreads / 8) {
       const int i = j + 1 + ii;
-      const double2 a = Ls[at(i, j)];
+      const double2 a = As[at(i, j)];
       for (int kk = tid % 8; kk <= ii; kk += 8) {
         const int k = j + 1 + kk;
-        const double2 bb = Ls[at(k, j)];
-        double2 v = Ls[at(i, k)];
-        v.x -= a.x * bb.x + a.y * bb.y;  // a conj(bb)
-        v.y -= a.y * bb.x - a.x * bb.y;
-        Ls[at(i, k)] = v;
+        const double2 bb = As[at(k, j)];
+        double2 v = As[at(i, k)];
+        v.x -= (a.x * bb.x + a.y * bb.y) * invd;
+        v.y -= (a.y * bb.x - a.x * bb.y) * invd;
+        As[at(i, k)] = v;
       }
     }
     __syncthreads();
@@ -220,34 +213,66 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const dou
   if (bad) {
     if (tid == 0) set_status(status, PRONY_ERR_SINGULAR);
     for (int i = tid; i < m; i += kSolveThreads) c[i] = make_double2(NAN, NAN);
-  } else {
-    // forward: L y = b (column oriented)
+  } else if (tid < 32) {
+    const int lane = tid;
+    double2 y[kSolveMaxRowsPerLane];
+#pragma unroll
+    for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
+      const int i = lane + 32 * q;
+      y[q] = i < m ? b[i] : make_double2(0.0, 0.0);
+    }
+    // forward: L y = b, column oriented: y_j /= L_jj; y_i -= L_ij y_j (i > j)
     for (int j = 0; j < m; ++j) {
-      const double ljj = Ls[at(j, j)].x;
-      const double2 yj = make_double2(y[j].x / ljj, y[j].y / ljj);
-      __syncthreads();
-      if (tid == 0) y[j] = yj;
-      for (int i = j + 1 + tid; i < m; i += kSolveThreads) {
-        const double2 a = Ls[at(i, j)];
-        y[i].x -= a.x * yj.x - a.y * yj.y;
-        y[i].y -= a.x * yj.y + a.y * yj.x;
+      const int qj = j >> 5, lj = j & 31;
+      double2 yj = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < kSolveMaxRowsPerLane; ++q)
+        if (q == qj) yj = y[q];
+      yj.x = __shfl_sync(0xffffffffu, yj.x, lj);
+      yj.y = __shfl_sync(0xffffffffu, yj.y, lj);
+      const double ij = inv[j];
+      yj = make_double2(yj.x * ij, yj.y * ij);
+#pragma unroll
+      for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
+        const int i = lane + 32 * q;
+        if (i == j) y[q] = yj;
+        if (i > j && i < m) {
+          const double2 a = As[at(i, j)];
+          const double2 l = make_double2(a.x * ij, a.y * ij);
+          y[q].x -= l.x * yj.x - l.y * yj.y;
+          y[q].y -= l.x * yj.y + l.y * yj.x;
+        }
       }
-      __syncthreads();
     }
-    // backward: L^H x = y, x overwrites y (column j of L^H is the conjugated row j of L)
+    // backward: L^H x = y: x_j = y_j / L_jj; y_i -= conj(L_ji) x_j (i < j)
     for (int j = m - 1; j >= 0; --j) {
-      const double ljj = Ls[at(j, j)].x;
-      const double2 xj = make_double2(y[j].x / ljj, y[j].y / ljj);
-      __syncthreads();
-      if (tid == 0) y[j] = xj;
-      for (int i = tid; i < j; i += kSolveThreads) {
-        const double2 a = cconj(Ls[at(j, i)]);
-        y[i].x -= a.x * xj.x - a.y * xj.y;
-        y[i].y -= a.x * xj.y + a.y * xj.x;
+      const int qj = j >> 5, lj = j & 31;
+      double2 xj = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < kSolveMaxRowsPerLane; ++q)
+        if (q == qj) xj = y[q];
+      xj.x = __shfl_sync(0xffffffffu, xj.x, lj);
+      xj.y = __shfl_sync(0xffffffffu, xj.y, lj);
+      const double ij = inv[j];
+      xj = make_double2(xj.x * ij, xj.y * ij);
+#pragma unroll
+      for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
+        const int i = lane + 32 * q;
+        if (i == j) y[q] = xj;
+        if (i < j) {
+          const double2 a = As[at(j, i)];
+          const double ii_ = inv[i];
+          const double2 l = make_double2(a.x * ii_, -a.y * ii_);  // conj(L_ji)
+          y[q].x -= l.x * xj.x - l.y * xj.y;
+          y[q].y -= l.x * xj.y + l.y * xj.x;
+        }
       }
-      __syncthreads();
     }
-    for (int i = tid; i < m; i += kSolveThreads) c[i] = cconj(y[i]);
+#pragma unroll
+    for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
+      const int i = lane + 32 * q;
+      if (i < m) c[i] = cconj(y[q]);
+    }
   }
   if (t) {
     const double inv2pi = 0.15915494309189533577;  // 1 / (2 pi)
@@ -289,7 +314,7 @@ int vls_cb(int64_t W, int m, int sm_count) {
   cb = std::max<int64_t>(1, std::min<int64_t>(cb, tiles));
   return (int)cb;
 }
-size_t solve_smem(int m) { return ((size_t)m * (m + 1) / 2 + m) * sizeof(double2); }
+size_t solve_smem(int m) { return (size_t)m * (m + 1) / 2 * sizeof(double2); }
 }  // namespace
 
 size_t ls_workspace_bytes(int d, int n, int m, int sm_count) {

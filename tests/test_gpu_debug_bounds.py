@@ -36,7 +36,7 @@ print("VIOLATIONS", L.prony_debug_violations())
 def test_gather_indices_in_bounds_debug_build():
     from paper_2012_11430_b200 import _build
     path = os.path.join(ROOT, "build", "libprony_debug.so")
-    if not os.path.exists(path):
+    if _build._stale(path):
         os.makedirs(os.path.dirname(path), exist_ok=True)
         _build.build_variant(path, ["PRONY_DEBUG"])
     env = dict(os.environ, PRONY_LIB=path, ROOT=ROOT)
