@@ -18,6 +18,8 @@
  *                        device, then prony_project (Algorithm 1 lines 1-3).
  *   prony_diagonalize    C_mu, its eigenvectors W, z = diag(W^-1 S_l W), t (Algorithm 1 lines 4-6).
  *   prony_toeplitz_apply T_l X, T X, T^H X with the implicit gather (the operator of the SVD).
+ *   prony_lanczos_svd    rank-revealing reduced SVD of T by Lanczos bidiagonalization with full
+ *                        reorthogonalization (Alg. 2) when m is unknown.
  *
  * Layout conventions (readings R1, R2):
  *   - complex numbers are prony_c128 {re, im} (== cuDoubleComplex == torch.complex128).
@@ -95,7 +97,8 @@ typedef enum prony_workspace_kind {
   PRONY_WS_BUILD = 3,        /* prony_build_pencil */
   PRONY_WS_APPLY = 4,        /* prony_toeplitz_apply, any r */
   PRONY_WS_DIAG = 5,         /* prony_diagonalize */
-  PRONY_WS_PROJECT_MU = 6    /* prony_project_mu */
+  PRONY_WS_PROJECT_MU = 6,   /* prony_project_mu */
+  PRONY_WS_LANCZOS = 7       /* prony_lanczos_svd; the m argument is max_rank (<= 255) */
 } prony_workspace_kind;
 
 /* unit orders of prony_project: units u in [0, d*N) */
@@ -281,6 +284,34 @@ int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t see
  */
 int prony_diagonalize(int d, int m, const prony_c128* S, const prony_c128* mu, prony_c128* z, double* t, prony_c128* W,
                       void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream);
+
+/*
+ * prony_lanczos_svd — Algorithm 2: Lanczos bidiagonalization T V_i = U_i B_i,
+ * T^H U_i = V_{i+1} B_{i,i+1}^T (eq_lanc_rec1/2) from a random p_1, with full
+ * reorthogonalization of every u_i / v_i against all previous ones (two classical Gram-Schmidt passes,
+ * P:170), stopping tests alpha <= tol_abs and beta <= tol_abs with tol_abs = tol * ||T||_F (P:172,
+ * reading R24: ||T||_F bounds ||T||_2 and has a closed form in the samples), the early-stop check of
+ * P:168 (a random vector orthogonalized against the basis that T^H resp. T does not annihilate
+ * restarts the recurrence with alpha resp. beta = 0), and the SVD of the bidiagonal factor: alpha stop
+ * -> B_{r,r+1} = Ubar_B [Sigma_B 0] Vbar_B^T, U = U_r Ubar_B, V = V_{r+1} Vbar_B(:,1:r);
+ * beta stop -> B_r = U_B Sigma_B V_B^T, U = U_r U_B, V = V_r V_B. The rank r is the
+ * dimension of the bidiagonal factor: no knowledge of m is needed.
+ * SYNCHRONOUS (the stopping tests read alpha_i, beta_i on the host every step).
+ *   grid        device L^d samples (as prony_project)
+ *   max_rank    1 <= max_rank <= 255, max_rank <= N: the basis buffers; the iteration stops there
+ *   tol         relative tolerance (>= 0): P:172 u ||T||_2 noise-free, the noise level for noisy data
+ *   seed        seeds p_1 and the early-stop test vectors (counter-based generator, R14)
+ *   ldo         columns of the outputs (1 <= ldo <= max_rank); the first min(r, ldo) are written
+ *   U, V        device N x ldo (row-major): leading left / right singular vectors
+ *   sigma       device ldo doubles, nonincreasing
+ *   rank_out    host int32: r;  steps_out nullable host int32: Lanczos steps taken
+ *   workspace   >= prony_workspace_size(PRONY_WS_LANCZOS, d, n, max_rank)
+ * Returns PRONY_OK, PRONY_ERR_NOT_CONVERGED (max_rank steps without a stop: outputs hold the
+ * rank-max_rank Lanczos approximation), PRONY_ERR_RANK (T = 0), or validation / CUDA errors.
+ */
+int prony_lanczos_svd(int d, int n, const prony_c128* grid, int max_rank, double tol, uint64_t seed, int ldo,
+                      prony_c128* U, prony_c128* V, double* sigma, int32_t* rank_out, int32_t* steps_out,
+                      void* workspace, size_t workspace_bytes, prony_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,7 @@ PRONY_ERR_CUDA = 6
 PRONY_ERR_UNIMPLEMENTED = 7
 PRONY_ERR_WORKSPACE = 8
 
-WS_PROJECT, WS_LS, WS_PENCIL_HOST, WS_BUILD, WS_APPLY, WS_DIAG, WS_PROJECT_MU = 0, 1, 2, 3, 4, 5, 6
+WS_PROJECT, WS_LS, WS_PENCIL_HOST, WS_BUILD, WS_APPLY, WS_DIAG, WS_PROJECT_MU, WS_LANCZOS = 0, 1, 2, 3, 4, 5, 6, 7
 UNITS_L_MAJOR, UNITS_ROW_MAJOR = 0, 1
 MAX_D, MAX_M = 8, 128
 
@@ -31,7 +31,7 @@ MAX_D, MAX_M = 8, 128
 EXPORTS = ("prony_abi_version", "prony_status_string", "prony_device_info", "prony_workspace_size",
            "prony_project", "prony_project_ex", "prony_vandermonde_ls", "prony_vandermonde_ls_ex", "prony_ls_solve",
            "prony_toeplitz_apply", "prony_pencil_host", "prony_build_pencil", "prony_diagonalize",
-           "prony_project_mu")
+           "prony_project_mu", "prony_lanczos_svd")
 
 
 class ExecInfo(ctypes.Structure):
@@ -82,6 +82,8 @@ def lib() -> ctypes.CDLL:
                                          vp, vp, sz, vp, vp]
         L.prony_diagonalize.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, sz, vp, vp]
         L.prony_project_mu.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp]
+        L.prony_lanczos_svd.argtypes = [i32, i32, vp, i32, ctypes.c_double, ctypes.c_uint64, i32, vp, vp, vp, vp, vp,
+                                        vp, sz, vp]
         for f in ("prony_device_info", "prony_workspace_size", "prony_project", "prony_vandermonde_ls", "prony_ls_solve",
                   "prony_project_ex", "prony_vandermonde_ls_ex", "prony_toeplitz_apply", "prony_diagonalize",
                   "prony_project_mu",
@@ -306,6 +308,34 @@ def build_pencil(grid, d: int, n: int, m: int, seed: int = 0, tol: float | None 
     if check and rc not in (PRONY_OK, PRONY_ERR_NOT_CONVERGED, PRONY_ERR_RANK):
         _check(rc, "prony_build_pencil")
     return {"S": S, "U": U, "V": V, "sigma": s, "rank": rank.value, "resid": resid.value, "status": rc}
+
+
+def lanczos_svd(grid, d: int, n: int, max_rank: int, tol: float | None = None, seed: int = 0, ldo: int | None = None,
+                workspace=None, stream=None, check: bool = True):
+    """Rank-revealing reduced SVD of T by Lanczos bidiagonalization with full reorthogonalization
+    (Alg. 2), m unknown. tol defaults to N eps_M (the noise-free tolerance of P:172/P:581).
+    Synchronous. Returns a dict with U, V (N, ldo), sigma (ldo,) [first min(rank, ldo) valid], rank,
+    steps, status (PRONY_OK / PRONY_ERR_NOT_CONVERGED when max_rank steps ran out)."""
+    _dev_tensor(grid, torch.complex128, "grid")
+    N = (n + 1) ** d
+    if tol is None:
+        tol = N * 2.220446049250313e-16
+    if ldo is None:
+        ldo = max_rank
+    dev = grid.device
+    U = torch.zeros((N, ldo), dtype=torch.complex128, device=dev)
+    V = torch.zeros((N, ldo), dtype=torch.complex128, device=dev)
+    s = torch.zeros(ldo, dtype=torch.float64, device=dev)
+    rank = ctypes.c_int32(0)
+    steps = ctypes.c_int32(0)
+    if workspace is None:
+        workspace = alloc_workspace(WS_LANCZOS, d, n, max_rank, dev)
+    rc = lib().prony_lanczos_svd(d, n, _ptr(grid), int(max_rank), float(tol), int(seed), int(ldo), _ptr(U), _ptr(V),
+                                 _ptr(s), ctypes.byref(rank), ctypes.byref(steps), _ptr(workspace), workspace.numel(),
+                                 _stream(stream))
+    if check and rc not in (PRONY_OK, PRONY_ERR_NOT_CONVERGED):
+        _check(rc, "prony_lanczos_svd")
+    return {"U": U, "V": V, "sigma": s, "rank": rank.value, "steps": steps.value, "status": rc}
 
 
 def diagonalize(S, mu, d: int, m: int, workspace=None, dev_status=None, stream=None):

@@ -136,6 +136,13 @@ int prony_device_info(int* sm_count, int* cc_major, int* cc_minor) {
 int prony_workspace_size(int kind, int d, int n, int m, size_t* bytes) {
   if (!bytes) return PRONY_ERR_INVALID;
   int64_t N = 0;
+  if (kind == PRONY_WS_LANCZOS) {
+    const int rc = validate_dnm(d, n, 1, &N);
+    if (rc) return rc;
+    if (m < 1 || m > kLanczosMaxRank || m > N) return PRONY_ERR_RANGE;
+    *bytes = lanczos_workspace_bytes(d, n, (int)N, m);
+    return PRONY_OK;
+  }
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
   const int sms = sm_count_current();
@@ -396,6 +403,28 @@ int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t see
   if (rc) return rc;
   if (cudaStreamSynchronize(st) != cudaSuccess) return PRONY_ERR_CUDA;
   return src;
+}
+
+int prony_lanczos_svd(int d, int n, const prony_c128* grid, int max_rank, double tol, uint64_t seed, int ldo,
+                      prony_c128* U, prony_c128* V, double* sigma, int32_t* rank_out, int32_t* steps_out,
+                      void* workspace, size_t workspace_bytes, prony_stream_t stream) {
+  int64_t N = 0;
+  int rc = validate_dnm(d, n, 1, &N);
+  if (rc) return rc;
+  if (!grid || !U || !V || !sigma || !rank_out || !workspace || !(tol >= 0.0)) return PRONY_ERR_INVALID;
+  if (max_rank < 1 || ldo < 1 || ldo > max_rank) return PRONY_ERR_INVALID;
+  if (max_rank > kLanczosMaxRank || max_rank > N) return PRONY_ERR_RANGE;
+  if (!aligned16(grid) || !aligned16(U) || !aligned16(V) || ((uintptr_t)sigma & 7u) || ((uintptr_t)workspace & 255u))
+    return PRONY_ERR_INVALID;
+  if (workspace_bytes < lanczos_workspace_bytes(d, n, (int)N, max_rank)) return PRONY_ERR_WORKSPACE;
+  const int sms = sm_count_current();
+  if (sms <= 0) return PRONY_ERR_CUDA;
+  int rank = 0, steps = 0;
+  rc = lanczos_svd(d, n, (int)N, (const double2*)grid, max_rank, tol, seed, (double2*)U, (double2*)V, sigma, ldo,
+                   &rank, &steps, workspace, sms, (cudaStream_t)stream);
+  *rank_out = rank;
+  if (steps_out) *steps_out = steps;
+  return rc;
 }
 
 int prony_diagonalize(int d, int m, const prony_c128* S, const prony_c128* mu, prony_c128* z, double* t, prony_c128* W,

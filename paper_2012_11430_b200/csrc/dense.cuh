@@ -34,6 +34,11 @@ int block_power_svd(int d, int n, int N, const double2* grid, int m, double tol,
                     double2* U, double2* V, double* sigma, int* rank_out, int* iters_out, double* resid_out, void* ws,
                     int sm_count, cudaStream_t st);
 size_t diag_workspace_bytes(int d, int m);
+constexpr int kLanczosMaxRank = 255;     // Jacobi pair table of the bidiagonal SVD
+constexpr double kLanczosTolFloor = 1e-10;  // relative rank tolerance floor (R24)
+size_t lanczos_workspace_bytes(int d, int n, int N, int kmax);
+int lanczos_svd(int d, int n, int N, const double2* grid, int kmax, double tol, uint64_t seed, double2* U, double2* V,
+                double* sigma, int ldo, int* rank_out, int* steps_out, void* ws, int sm_count, cudaStream_t st);
 int diagonalize_launch(int d, int m, const double2* S, const double2* mu, double2* z, double* t, double2* W,
                        void* ws, int32_t* status, cudaStream_t st);
 

@@ -65,6 +65,17 @@ def test_validation_before_any_cuda_call(pb):
                                 null) == pb.PRONY_ERR_INVALID
     assert L.prony_diagonalize(0, 3, null, null, null, null, null, null, 0, null, null) == pb.PRONY_ERR_INVALID
     assert L.prony_toeplitz_apply(2, 4, null, 3, 0, null, 1, 1, null, 1, null, 0, null) == pb.PRONY_ERR_INVALID
+    # lanczos: null grid -> INVALID; max_rank above the Jacobi limit or above N -> RANGE (pointers non-null)
+    assert L.prony_lanczos_svd(2, 4, null, 5, 0.0, 0, 5, null, null, null, null, null, null, 0,
+                               null) == pb.PRONY_ERR_INVALID
+    buf = (ctypes.c_double * 64)()
+    p = ctypes.c_void_p(ctypes.addressof(buf))
+    r = ctypes.c_int32()
+    assert L.prony_lanczos_svd(2, 4, p, 26, 0.0, 0, 5, p, p, p, ctypes.byref(r), None, p, 0,
+                               null) == pb.PRONY_ERR_RANGE
+    assert L.prony_lanczos_svd(2, 4, p, 5, 0.0, 0, 6, p, p, p, ctypes.byref(r), None, p, 0,
+                               null) == pb.PRONY_ERR_INVALID
+    assert L.prony_workspace_size(pb.WS_LANCZOS, 2, 20, 256, ctypes.byref(sz)) == pb.PRONY_ERR_RANGE
 
 
 def test_misaligned_pointer_rejected(pb):
