@@ -222,7 +222,8 @@ def run_ours(args, cfg):
     d, n, m, N = c.d, c.n, c.m, c.N
     tg = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     grid, U, V, sigma, z = tg(prob.grid), tg(prob.U), tg(prob.V), tg(prob.sigma), tg(prob.z)
-    pencil = sharding.DistributedPencil(d, n, m, dev, world, rank)
+    order_arg = {"l-major": 0, "row-major": 1, "shared": 2}[args.units]
+    pencil = sharding.DistributedPencil(d, n, m, dev, world, rank, unit_order=order_arg)
     order = pencil.order
     st = pencil.status
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -366,11 +367,15 @@ def run_ours(args, cfg):
             "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded planted exponential sum, complex Gaussian noise 1e-6)",
             "config": {"workload": f"{c.name}: d={d} n={n} N={N} m={m} noise={c.noise} (BASELINE configs[3])",
-                       "d": d, "n": n, "N": N, "m": m, "parallelism": f"dp{world} ({'l-major' if order == 0 else 'row-major'} units)",
+                       "d": d, "n": n, "N": N, "m": m, "parallelism": f"dp{world} ({['l-major', 'row-major', 'shared'][order]} units)",
                        "l2": "flushed (256 MiB write) before every timed step, outside the timed interval",
                        "pencils_per_step": 1, "comm": "1 x all_reduce(SUM) of packed [S,G,b] per step" if world > 1 else "none"},
             "tflops": F * value / 1e12,
             "pct_peak": (F * value / 1e12) / (peak * world) if peak else None,
+            "flop_accounting": ("tflops/pct_peak count the paper's d(8mN^2+8Nm^2)+8m^2N+8mN per pencil; with "
+                                "shared units one extended product T_E V ((n+2)^d rows) replaces the d products "
+                                "T_l V (d(n+1)^d rows), DESIGN.md F8; roofline.achieved counts the flops of the "
+                                "product k_project actually computes (8 m N rows), as a 4M ZGEMM would"),
             "roofline": {"bound": "tensor", "kernel": "k_project (complex FP64 DMMA, implicit Toeplitz gather)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                          "traffic": traffic,
@@ -404,6 +409,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--units", default="shared", choices=["shared", "l-major", "row-major"],
+                    help="prony_unit_order of the projection (shared: one extended product for all l, F8)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -101,10 +101,14 @@ typedef enum prony_workspace_kind {
   PRONY_WS_LANCZOS = 7       /* prony_lanczos_svd; the m argument is max_rank (<= 255) */
 } prony_workspace_kind;
 
-/* unit orders of prony_project: units u in [0, d*N) */
+/* unit orders of prony_project. L_MAJOR / ROW_MAJOR: units u in [0, d*N), one row k
+ * of one T_l each. SHARED: units u in [0, (n+2)^d), one row k' of the extended Toeplitz block
+ * T_E = [f(k'-h)]_{k' in {0..n+1}^d, h in I_n} each; since T_l[k,:] = T_E[k+e_l,:] (F8)
+ * one product T_E V serves all d pencils ((n+2)^d instead of d(n+1)^d rows of work). */
 typedef enum prony_unit_order {
-  PRONY_UNITS_L_MAJOR = 0,   /* u = (l-1)*N + k  (l-sharding when ranks divide d) */
-  PRONY_UNITS_ROW_MAJOR = 1  /* u = k*d + (l-1)  (row-block sharding, all l per rank) */
+  PRONY_UNITS_L_MAJOR = 0,    /* u = (l-1)*N + k  (l-sharding when ranks divide d) */
+  PRONY_UNITS_ROW_MAJOR = 1,  /* u = k*d + (l-1)  (row-block sharding, all l per rank) */
+  PRONY_UNITS_SHARED = 2      /* u = index of k' in {0..n+1}^d (lexicographic, last fastest) */
 } prony_unit_order;
 
 /*
@@ -150,9 +154,11 @@ int prony_workspace_size(int kind, int d, int n, int m, size_t* bytes);
  *   sigma       device, m doubles > 0: Sigma^-1 is applied as the column scale 1/sigma_j (R11).
  *   unit_begin, unit_end, unit_order
  *               the call contributes the rows k of T_l for the units u in [unit_begin,
- *               unit_end) of [0, d*N) (order: prony_unit_order). [0, d*N) gives the complete
- *               S_1..S_d; a partition of [0, d*N) over ranks gives partial pencils whose SUM
- *               is S (Sigma^-1 already applied), i.e. one all-reduce completes the pencil.
+ *               unit_end) of [0, U) (order: prony_unit_order; U = d*N for L_MAJOR / ROW_MAJOR,
+ *               (n+2)^d for SHARED). [0, U) gives the complete S_1..S_d; a partition of [0, U)
+ *               over ranks gives partial pencils whose SUM is S (Sigma^-1 already applied),
+ *               i.e. one all-reduce completes the pencil. SHARED is the fast order (the
+ *               library's own full-pencil calls use it).
  *   S           device, d x m x m prony_c128, OVERWRITTEN with this call's partial sum
  *               (rows of S_l with no unit in range are zero).
  *   workspace   device scratch of workspace_bytes >= prony_workspace_size(PRONY_WS_PROJECT).

@@ -127,12 +127,43 @@ def project(grid, U, V, sigma, d, n):
     return np.stack([project_rows(grid, U, V, sigma, d, n, ell) for ell in range(1, d + 1)])
 
 
+def _shared_runs(d, n, ell, unit_begin, unit_end):
+    """Unit order 2 (SHARED): unit u is the point k' of E = {0..n+1}^d with index u (lexicographic,
+    last coordinate fastest); it stands for row k = k' - e_l of T_l whenever that k lies in I_n
+    (F8). Returns the rows k of T_l covered by [unit_begin, unit_end) as (kb, ke) runs."""
+    runs = []
+    for u in range(unit_begin, unit_end):
+        c = []
+        r = u
+        for _ in range(d):
+            c.append(r % (n + 2))
+            r //= n + 2
+        c = c[::-1]                      # c[0] is the slowest coordinate (e_1 direction)
+        c[ell - 1] -= 1
+        if min(c) < 0 or max(c) > n:
+            continue
+        k = 0
+        for ci in c:
+            k = k * (n + 1) + ci
+        if runs and runs[-1][1] == k:
+            runs[-1][1] = k + 1
+        else:
+            runs.append([k, k + 1])
+    return runs
+
+
 def project_units(grid, U, V, sigma, d, n, unit_begin, unit_end, unit_order=0):
-    """Partial pencil over a unit sub-range of [0, dN) (DESIGN.md §6 sharding):
-    unit_order 0: u = (l-1) N + k ; 1: u = k d + (l-1). Returns (d, m, m)."""
+    """Partial pencil over a unit sub-range (DESIGN.md §6 sharding): unit_order 0: u = (l-1) N + k,
+    1: u = k d + (l-1) (units in [0, dN)); 2: u = a point of {0..n+1}^d standing for row k' - e_l of
+    every T_l (units in [0, (n+2)^d)). Each row is computed directly from T_l. Returns (d, m, m)."""
     N = N_of(d, n)
     m = U.shape[1]
     out = np.zeros((d, m, m), np.complex128)
+    if unit_order == 2:
+        for ell in range(1, d + 1):
+            for kb, ke in _shared_runs(d, n, ell, unit_begin, unit_end):
+                out[ell - 1] += project_rows(grid, U, V, sigma, d, n, ell, kb, ke)
+        return out
     for ell in range(1, d + 1):
         if unit_order == 0:
             kb = min(max(unit_begin - (ell - 1) * N, 0), N)

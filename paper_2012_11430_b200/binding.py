@@ -24,7 +24,7 @@ PRONY_ERR_UNIMPLEMENTED = 7
 PRONY_ERR_WORKSPACE = 8
 
 WS_PROJECT, WS_LS, WS_PENCIL_HOST, WS_BUILD, WS_APPLY, WS_DIAG, WS_PROJECT_MU, WS_LANCZOS = 0, 1, 2, 3, 4, 5, 6, 7
-UNITS_L_MAJOR, UNITS_ROW_MAJOR = 0, 1
+UNITS_L_MAJOR, UNITS_ROW_MAJOR, UNITS_SHARED = 0, 1, 2
 MAX_D, MAX_M = 8, 128
 
 # every symbol include/prony.h declares (checked by tests/test_abi.py)
@@ -139,16 +139,21 @@ def alloc_workspace(kind: int, d: int, n: int, m: int, device=None) -> torch.Ten
     return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device or "cuda")
 
 
+def unit_count(d: int, n: int, unit_order: int) -> int:
+    """Size of the unit space of prony_project: d N (L_MAJOR, ROW_MAJOR) or (n+2)^d (SHARED)."""
+    return (n + 2) ** d if unit_order == UNITS_SHARED else d * (n + 1) ** d
+
+
 def project(grid, U, V, sigma, d: int, n: int, m: int, unit_begin: int = 0, unit_end: int | None = None,
-            unit_order: int = UNITS_L_MAJOR, out=None, workspace=None, dev_status=None, stream=None, info=None):
-    """S_l = U* T_l V Sigma^-1 over units [unit_begin, unit_end) -> (d, m, m) complex128."""
-    N = (n + 1) ** d
+            unit_order: int = UNITS_SHARED, out=None, workspace=None, dev_status=None, stream=None, info=None):
+    """S_l = U* T_l V Sigma^-1 over units [unit_begin, unit_end) -> (d, m, m) complex128.
+    The default order SHARED computes all d pencils from one extended product (F8)."""
     _dev_tensor(grid, torch.complex128, "grid")
     _dev_tensor(U, torch.complex128, "U")
     _dev_tensor(V, torch.complex128, "V")
     _dev_tensor(sigma, torch.float64, "sigma")
     if unit_end is None:
-        unit_end = d * N
+        unit_end = unit_count(d, n, unit_order)
     if out is None:
         out = torch.empty((d, m, m), dtype=torch.complex128, device=grid.device)
     _dev_tensor(out, torch.complex128, "out")

@@ -42,7 +42,13 @@ int validate_dnm(int d, int n, int m, int64_t* N_out) {
 }
 
 // rows of T_l covered by units [u0, u1) in the given order
-void unit_rows(int d, int64_t N, int64_t u0, int64_t u1, int order, ProjGeom* g) {
+void unit_rows(int d, int n, int64_t N, int64_t u0, int64_t u1, int order, ProjGeom* g) {
+  if (order == PRONY_UNITS_SHARED) {
+    g->shared = 1;
+    g->e0 = (int)u0;
+    g->e1 = (int)u1;
+    return;
+  }
   for (int l = 0; l < d; ++l) {
     int64_t kb, ke;
     if (order == PRONY_UNITS_L_MAJOR) {
@@ -180,8 +186,10 @@ int prony_project_ex(int d, int n, int m, const prony_c128* grid, const prony_c1
   if (!aligned16(grid) || !aligned16(U) || !aligned16(V) || !aligned16(S) || ((uintptr_t)sigma & 7u) ||
       ((uintptr_t)workspace & 255u))
     return PRONY_ERR_INVALID;
-  if (unit_order != PRONY_UNITS_L_MAJOR && unit_order != PRONY_UNITS_ROW_MAJOR) return PRONY_ERR_INVALID;
-  if (unit_begin < 0 || unit_end < unit_begin || unit_end > (int64_t)d * N) return PRONY_ERR_RANGE;
+  if (unit_order != PRONY_UNITS_L_MAJOR && unit_order != PRONY_UNITS_ROW_MAJOR && unit_order != PRONY_UNITS_SHARED)
+    return PRONY_ERR_INVALID;
+  const int64_t units = unit_order == PRONY_UNITS_SHARED ? ext_rows(d, n) : (int64_t)d * N;
+  if (unit_begin < 0 || unit_end < unit_begin || unit_end > units) return PRONY_ERR_RANGE;
   const int sms = sm_count_current();
   if (sms <= 0) return PRONY_ERR_CUDA;
   if (workspace_bytes < ws_project(d, n, N, m, sms)) return PRONY_ERR_WORKSPACE;
@@ -190,7 +198,7 @@ int prony_project_ex(int d, int n, int m, const prony_c128* grid, const prony_c1
   g.n = n;
   g.m = m;
   g.N = (int)N;
-  unit_rows(d, N, unit_begin, unit_end, unit_order, &g);
+  unit_rows(d, n, N, unit_begin, unit_end, unit_order, &g);
   ProjPlan pl{};
   project_plan(g, sms, &pl);
   return project_launch(g, pl, (const double2*)grid, (const double2*)U, (const double2*)V, sigma, (double2*)S,
@@ -347,7 +355,7 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
   g.n = n;
   g.m = m;
   g.N = (int)N;
-  unit_rows(d, N, 0, (int64_t)d * N, PRONY_UNITS_L_MAJOR, &g);
+  unit_rows(d, n, N, 0, ext_rows(d, n), PRONY_UNITS_SHARED, &g);
   ProjPlan pl{};
   project_plan(g, sms, &pl);
   rc = project_launch(g, pl, (const double2*)(w + h.grid), (const double2*)(w + h.U), (const double2*)(w + h.V),
@@ -398,7 +406,7 @@ int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t see
   *rank_out = rank;
   if (resid_out) *resid_out = resid;
   if (src != PRONY_OK && src != PRONY_ERR_NOT_CONVERGED) return src;
-  rc = prony_project(d, n, m, grid, U, V, sigma, 0, (int64_t)d * N, PRONY_UNITS_L_MAJOR, S, workspace,
+  rc = prony_project(d, n, m, grid, U, V, sigma, 0, ext_rows(d, n), PRONY_UNITS_SHARED, S, workspace,
                      workspace_bytes, dev_status, stream);
   if (rc) return rc;
   if (cudaStreamSynchronize(st) != cudaSuccess) return PRONY_ERR_CUDA;

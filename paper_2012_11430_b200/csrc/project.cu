@@ -68,6 +68,42 @@ __global__ void k_prep(int d, int n, int N, int m, int ldv, int NP, int64_t box,
   }
 }
 
+// Shared-row tables (F8): for e in E = {0..n+1}^d with coordinates c (base n+2, last
+// fastest): etab[e] = sum_i c_i L^(d-1-i), so T_E[e,h] = grid[etab[e] - P(h) + C0]; and for each l,
+// umap[l][e] = index in I_n of k = c - e_l when that k lies in I_n (then T_l[k,:] = T_E[e,:]), else -1.
+__global__ void k_prep_ext(int d, int n, int64_t E, int32_t* __restrict__ etab, int32_t* __restrict__ umap) {
+  const int L = 2 * n + 2, Le = n + 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E + kPtabPad;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e >= E) {
+      etab[e] = 0;
+      continue;
+    }
+    int c[PRONY_MAX_D];
+    int64_t r = e;
+    for (int i = d - 1; i >= 0; --i) {
+      c[i] = (int)(r % Le);
+      r /= Le;
+    }
+    int P = 0, s = 1;
+    for (int i = d - 1; i >= 0; --i) {
+      P += c[i] * s;
+      s *= L;
+    }
+    etab[e] = P;
+    for (int l = 0; l < d; ++l) {  // S_{l+1}: shift e_{l+1} is coordinate l
+      int idx = 0;
+      bool ok = c[l] >= 1;
+      for (int i = 0; i < d; ++i) {
+        const int k = c[i] - (i == l ? 1 : 0);
+        ok = ok && k <= n;
+        idx = idx * (n + 1) + k;
+      }
+      umap[(int64_t)l * E + e] = ok ? idx : -1;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------- projection
 // Warp-specialized CTA of kThreads = 512 threads: warpgroups 0-2 are consumers (12 warps =
 // WM x WN, warp tile 16 rows x 8*nt_active columns, 3M/4M DMMA; setmaxnreg 152 registers),
@@ -153,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
     for (int e = tid; e < kBK * (T::LDB * 2 + T::LDBS); e += kThreads) smem[s * T::STAGE + T::B_C + e] = 0.0;
   int* sPA = reinterpret_cast<int*>(smem + T::PAT);
   for (int r = tid; r < BM; r += kThreads)
-    sPA[r] = (rb0 + r < rows) ? p.ptab[p.kb[l] + rb0 + r] + p.shift[l] : -1;  // -1: row outside
+    sPA[r] = (rb0 + r < rows) ? p.rtab[p.kb[l] + rb0 + r] + p.shift[l] : -1;  // -1: row outside
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full0 + 8u * s, kGatherThreads + 1);  // A-gather cp.async arrivals + B expect_tx
@@ -392,8 +428,10 @@ __global__ void __launch_bounds__(kReduceThreads, 1) k_reduce(RedParams p) {
     for (int e = tid; e < kRedSlab * T::NPU; e += kReduceThreads) {
       const int r = e / T::NPU, i = e % T::NPU;
       const int row = r0 + r;
-      const bool ok = row < rend && i < m;
-      const double2* src = p.U + (ok ? (size_t)(p.kb[l] + row) * m + i : 0);
+      int urow = p.kb[l] + row;
+      if (p.umap && row < rend) urow = __ldg(p.umap + (size_t)l * p.E + urow);  // -1: no T_l row here
+      const bool ok = row < rend && i < m && urow >= 0;
+      const double2* src = p.U + (ok ? (size_t)urow * m + i : 0);
       cp_async16(st + (uint32_t)(T::U_C + 2 * (r * T::LDU + i)) * 8u, src, ok ? 16 : 0);
     }
     cp_async_commit();
@@ -517,17 +555,23 @@ int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl) {
   const ProjShape sh = proj_shape(g.m);
   pl->shape = sh;
   int R_tot = 0, max_rows = 0, row_blocks = 0;
-  for (int l = 0; l < g.d; ++l) {
-    pl->yoff[l] = R_tot;
-    R_tot += g.rows[l];
-    max_rows = std::max(max_rows, g.rows[l]);
-    row_blocks += (g.rows[l] + sh.BM - 1) / sh.BM;
+  if (g.shared) {  // one product over rows [e0, e1) of T_E serves every l
+    R_tot = max_rows = g.e1 - g.e0;
+    row_blocks = (R_tot + sh.BM - 1) / sh.BM;
+    for (int l = 0; l < g.d; ++l) pl->yoff[l] = 0;
+  } else {
+    for (int l = 0; l < g.d; ++l) {
+      pl->yoff[l] = R_tot;
+      R_tot += g.rows[l];
+      max_rows = std::max(max_rows, g.rows[l]);
+      row_blocks += (g.rows[l] + sh.BM - 1) / sh.BM;
+    }
   }
   pl->R_tot = R_tot;
   pl->max_rows = max_rows;
   // split-K: chunk count KC minimizing waves x (chunk columns + pipeline fill), subject to
-  // KC * R_tot <= kYCap d N (workspace bound) and chunks of >= 64 columns.
-  const int64_t cap_rows = (int64_t)kYCap * g.d * g.N;
+  // KC * R_tot <= kYCap max(d N, |E|) (workspace bound) and chunks of >= 64 columns.
+  const int64_t cap_rows = (int64_t)kYCap * std::max<int64_t>((int64_t)g.d * g.N, ext_rows(g.d, g.n));
   int kc_max = (int)std::min<int64_t>(64, std::max<int64_t>(1, cap_rows / std::max(R_tot, 1)));
   kc_max = std::max(1, std::min(kc_max, std::max(1, g.N / 64)));
   double best = 1e30;
@@ -553,9 +597,11 @@ int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl) {
   return 0;
 }
 
+int64_t ext_rows(int d, int n) { return ipow(n + 2, d); }
+
 namespace {
 struct WsLayout {
-  size_t ptab, gsum, vsum, Y, Spart, counters, total;
+  size_t ptab, etab, umap, gsum, vsum, Y, Spart, counters, total;
 };
 WsLayout ws_layout(int d, int n, int N, int m, int sm_count) {
   const ProjShape sh = proj_shape(m);
@@ -568,14 +614,18 @@ WsLayout ws_layout(int d, int n, int N, int m, int sm_count) {
     off += align_up(bytes, 256);
     return o;
   };
+  const int64_t E = ext_rows(d, n);
   w.ptab = take((size_t)(N + kPtabPad) * sizeof(int32_t));
+  w.etab = take((size_t)(E + kPtabPad) * sizeof(int32_t));
+  w.umap = take((size_t)d * E * sizeof(int32_t));
   w.gsum = take((size_t)box * sizeof(double));
   w.vsum = take((size_t)N * sh.NP * sizeof(double));
-  w.Y = take((size_t)kYCap * d * N * sh.NP * sizeof(double2));  // Y partials (KC*R_tot <= kYCap*dN)
+  // Y partials: KC * R_tot <= kYCap * max(dN, |E|)
+  w.Y = take((size_t)kYCap * std::max<int64_t>((int64_t)d * N, E) * sh.NP * sizeof(double2));
   const int ib = (sh.NP + sh.BI - 1) / sh.BI;
   const int RP = std::max(1, sm_count / std::max(1, d * ib));
   w.Spart = take((size_t)d * RP * m * m * sizeof(double2));
-  w.counters = take((size_t)d * ((N + 15) / 16 + 1) * sizeof(int));  // split-K arrival counters
+  w.counters = take((size_t)d * ((std::max<int64_t>(N, E) + 15) / 16 + 1) * sizeof(int));  // split-K arrivals
   w.total = off;
   return w;
 }
@@ -614,11 +664,15 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   const WsLayout wl = ws_layout(g.d, g.n, g.N, g.m, sm_count);
   char* w = (char*)ws;
   int32_t* ptab = (int32_t*)(w + wl.ptab);
+  int32_t* etab = (int32_t*)(w + wl.etab);
+  int32_t* umap = (int32_t*)(w + wl.umap);
   double* gsum = (double*)(w + wl.gsum);
   double* vsum = (double*)(w + wl.vsum);
   double2* Y = (double2*)(w + wl.Y);
   double2* Spart = (double2*)(w + wl.Spart);
   int* counters = (int*)(w + wl.counters);
+  const int64_t E = ext_rows(g.d, g.n);
+  const int pslots = g.shared ? 1 : g.d;  // k_project row segments
 
   if (info) {
     info->launches = 0;
@@ -634,9 +688,10 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   int64_t box = 1;
   for (int i = 0; i < g.d; ++i) box *= (2 * (int64_t)g.n + 2);
   const int nrb = (pl.max_rows + pl.shape.BM - 1) / pl.shape.BM;
-  if (pl.KC > 1 && cudaMemsetAsync(counters, 0, (size_t)g.d * nrb * sizeof(int), st) != cudaSuccess)
+  if (pl.KC > 1 && cudaMemsetAsync(counters, 0, (size_t)pslots * nrb * sizeof(int), st) != cudaSuccess)
     return PRONY_ERR_CUDA;
   k_prep<<<2 * sm_count, 256, 0, st>>>(g.d, g.n, g.N, g.m, g.m, pl.shape.NP, box, grid, V, ptab, gsum, vsum);
+  if (g.shared) k_prep_ext<<<sm_count, 256, 0, st>>>(g.d, g.n, E, etab, umap);
 
   ProjParams p{};
   p.grid = grid;
@@ -645,6 +700,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   p.ldv = g.m;
   p.vsum = vsum;
   p.ptab = ptab;
+  p.rtab = g.shared ? etab : ptab;
   p.Y = Y;
   p.N = g.N;
   p.m = g.m;
@@ -668,9 +724,17 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
     const int ell = l + ell_base;  // segment l holds T_ell (ell_base 1: S_1..S_d; 0: segment 0 is T)
     p.shift[l] = (int)(C0 + (ell >= 1 ? ipow(L, g.d - ell) : 0));  // s_ell = L^(d-ell)
   }
+  if (g.shared) {  // one segment: rows [e0, e1) of T_E = [f(k'-h)]
+    p.kb[0] = g.e0;
+    p.rows[0] = pl.R_tot;
+    p.yoff[0] = 0;
+    p.shift[0] = (int)C0;
+  }
   RedParams r{};
   r.Y = Y;
   r.U = U;
+  r.umap = g.shared ? umap : nullptr;
+  r.E = (int)E;
   r.Spart = Spart;
   r.m = g.m;
   r.NP = pl.shape.NP;
@@ -678,11 +742,11 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   r.R_tot = pl.R_tot;
   r.RP = pl.RP;
   for (int l = 0; l < g.d; ++l) {
-    r.kb[l] = g.kb[l];
-    r.rows[l] = g.rows[l];
+    r.kb[l] = g.shared ? g.e0 : g.kb[l];
+    r.rows[l] = g.shared ? pl.R_tot : g.rows[l];
     r.yoff[l] = pl.yoff[l];
   }
-  dim3 grd((pl.max_rows + pl.shape.BM - 1) / pl.shape.BM, pl.KC, g.d);
+  dim3 grd((pl.max_rows + pl.shape.BM - 1) / pl.shape.BM, pl.KC, pslots);
   dim3 rgrd(pl.RP, g.d, (pl.shape.NP + pl.shape.BI - 1) / pl.shape.BI);
   const int NT = pl.shape.NT, WN = pl.shape.WN;
   const int mode = cmul_mode();
@@ -720,7 +784,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   const int64_t tot = (int64_t)g.d * g.m * g.m;
   k_finalize<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256, 0, st>>>(g.d, g.m, pl.RP, Spart, sigma, S);
   if (info) {
-    info->launches = 4;
+    info->launches = g.shared ? 5 : 4;  // k_prep (+ k_prep_ext), k_project, k_reduce, k_finalize
     info->main_grid[0] = (int)grd.x;
     info->main_grid[1] = (int)grd.y;
     info->main_grid[2] = (int)grd.z;
@@ -858,6 +922,7 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
     p.ldv = ldx;
     p.vsum = vsum;
     p.ptab = ptab;
+    p.rtab = ptab;
     p.Y = Y;
     p.N = N;
     p.m = wcols;

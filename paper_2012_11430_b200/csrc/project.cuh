@@ -8,6 +8,7 @@
 
 namespace prony {
 
+int64_t ext_rows(int d, int n);  // |E| = (n+2)^d
 constexpr int kPtabPad = 4;   // P table padded so the last k-step may read P(h) for h < N+4
 constexpr int kMaxNP = 128;   // padded width of Y rows handled by k_reduce
 constexpr int kYCap = 4;      // split-K bound: KC * (rows in range) <= kYCap * d * N
@@ -20,11 +21,16 @@ struct ProjShape {
   int NP;
 };
 
-// rows of T_l covered by a call: for l = 1..d (index l-1), rows [kb, kb+rows) of I_n
+// rows of T_l covered by a call: for l = 1..d (index l-1), rows [kb, kb+rows) of I_n.
+// shared = 1 (PRONY_UNITS_SHARED): the call covers rows [e0, e1) of the extended block
+// T_E = [f(k'-h)], k' in E = {0..n+1}^d (lexicographic, last fastest), and every S_l takes its rows
+// from the same product: T_l[k,:] = T_E[k+e_l,:] (F8), so k_project runs once for all l.
 struct ProjGeom {
   int d, n, m, N;
   int kb[PRONY_MAX_D];
   int rows[PRONY_MAX_D];
+  int shared;
+  int e0, e1;
 };
 
 struct ProjPlan {
@@ -42,6 +48,7 @@ struct ProjParams {
   int ldv;  // row stride of V (elements)
   const double* vsum;
   const int32_t* ptab;
+  const int32_t* rtab;  // row table: ptab (per-l rows of I_n) or etab (rows of E, shared mode)
   double2* Y;
   int* counters;  // [d][nrb] split-K arrival counters (zeroed per call)
   int N, m, NP, chunk_w, R_tot, KC, nrb;
@@ -52,8 +59,9 @@ struct ProjParams {
 struct RedParams {
   const double2* Y;
   const double2* U;
+  const int32_t* umap;  // shared mode: umap[l*E + e] = row of U paired with row e of Y_E for S_l, or -1
   double2* Spart;
-  int m, NP, KC, R_tot, RP;
+  int m, NP, KC, R_tot, RP, E;
   int kb[PRONY_MAX_D], rows[PRONY_MAX_D], yoff[PRONY_MAX_D];
 };
 

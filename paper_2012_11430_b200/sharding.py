@@ -2,8 +2,9 @@
 
 S_l = sum_g U[R_g]^* T_l[R_g, :] V Sigma^-1 is linear in any partition of the rows k of T_l
 and of l, and G = sum_g A[:, K_g] A[:, K_g]^H, b likewise over the columns k. So each rank
-takes a contiguous, equal slice of the unit space [0, dN) (l-major or row-major order, see
-prony_unit_order) and of the columns [0, N), computes partial S (Sigma^-1 already applied),
+takes a contiguous, equal slice of the unit space (default: the SHARED order, rows k' of the
+extended block T_E, each standing for row k' - e_l of every T_l; or [0, dN) l-major / row-major,
+see prony_unit_order) and of the columns [0, N), computes partial S (Sigma^-1 already applied),
 G and b with its own GPU, and ONE all_reduce(SUM) of the packed [S_1..S_d, G, b]
 ((d+1) m^2 + m complex128, 470 KB at d=2, m=100) over NCCL completes the pencil on every
 rank; the m x m Cholesky solve for c then runs locally (prony_ls_solve).
@@ -22,9 +23,15 @@ def split_range(total: int, parts: int, idx: int) -> tuple[int, int]:
     return total * idx // parts, total * (idx + 1) // parts
 
 
-def unit_range(d: int, n: int, world: int, rank: int) -> tuple[int, int]:
-    N = (n + 1) ** d
-    return split_range(d * N, world, rank)
+UNITS_L_MAJOR, UNITS_ROW_MAJOR, UNITS_SHARED = 0, 1, 2
+
+
+def unit_count(d: int, n: int, order: int) -> int:
+    return (n + 2) ** d if order == UNITS_SHARED else d * (n + 1) ** d
+
+
+def unit_range(d: int, n: int, world: int, rank: int, order: int = UNITS_SHARED) -> tuple[int, int]:
+    return split_range(unit_count(d, n, order), world, rank)
 
 
 def column_range(d: int, n: int, world: int, rank: int) -> tuple[int, int]:
@@ -33,9 +40,9 @@ def column_range(d: int, n: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def default_unit_order(d: int, world: int) -> int:
-    """l-major when the ranks divide d (pure l-sharding, e.g. cfg3 on 3 GPUs), else row-major
-    (every rank touches all l: V tiles and grid windows shared across l, balanced rows)."""
-    return 0 if world > 1 and d % world == 0 else 1
+    """SHARED for every world size: one extended product serves all l ((n+2)^d rows of work instead
+    of d (n+1)^d), and a contiguous slice of it is a balanced row block on every rank."""
+    return UNITS_SHARED
 
 
 def pack(S: torch.Tensor, G: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
@@ -71,7 +78,7 @@ class DistributedPencil:
         self.d, self.n, self.m = d, n, m
         self.world, self.rank = world, rank
         self.order = default_unit_order(d, world) if unit_order is None else unit_order
-        self.u0, self.u1 = unit_range(d, n, world, rank)
+        self.u0, self.u1 = unit_range(d, n, world, rank, self.order)
         self.c0, self.c1 = column_range(d, n, world, rank)
         self.ws_p = pb.alloc_workspace(pb.WS_PROJECT, d, n, m, device)
         self.ws_l = pb.alloc_workspace(pb.WS_LS, d, n, m, device)

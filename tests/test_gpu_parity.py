@@ -89,13 +89,14 @@ def test_project_edge_shapes(pb, orc, d, n, m, noise):
         assert rel(S[l], S_or[l]) <= TOL
 
 
-@pytest.mark.parametrize("order", [0, 1])
+@pytest.mark.parametrize("order", [0, 1, 2])
 def test_project_unit_ranges_partition(pb, orc, order):
     """Partial pencils over unit sub-ranges match the oracle and sum to the full pencil."""
     prob = problem(3, 6, 10, 77, 1e-6, random_uv=True)
     c = prob.cfg
     N = c.N
-    cuts = [0, 5, 343, 344, 700, 3 * N - 1, 3 * N]
+    E = (c.n + 2) ** c.d
+    cuts = [0, 5, 343, 344, 700, 3 * N - 1, 3 * N] if order < 2 else [0, 5, 63, 64, 300, E - 1, E]
     acc = torch.zeros((c.d, c.m, c.m), dtype=torch.complex128, device="cuda")
     for a, b in zip(cuts, cuts[1:]):
         S = run_project(pb, prob, unit_begin=a, unit_end=b, unit_order=order)
@@ -125,7 +126,8 @@ def test_project_cmul_modes(pb, orc, mode, d, n, m, monkeypatch):
         assert rel(S[l], S_or[l]) <= 1e-13
 
 
-@pytest.mark.parametrize("u0,u1,order", [(0, 100, 0), (4096 + 7, 4096 + 300, 0), (11, 913, 1), (0, 8192, 1)])
+@pytest.mark.parametrize("u0,u1,order", [(0, 100, 0), (4096 + 7, 4096 + 300, 0), (11, 913, 1), (0, 8192, 1),
+                                          (0, 100, 2), (3999, 4225, 2)])
 def test_project_small_ranges_many_chunks(pb, orc, u0, u1, order):
     """Small unit ranges over a long K (N = 4096) make the planner split K into many chunks:
     exercises the split-K arrival counters and the last-arriver fixup of k_project."""

@@ -32,7 +32,7 @@ def _worker(rank, world, port, d, n, m, order, out_path):
     import oracle
     import workload as W
     prob = W.make_problem(W.custom_config(d, n, m, 1e-6, 97), with_svd=True)
-    u0, u1 = sharding.unit_range(d, n, world, rank)
+    u0, u1 = sharding.unit_range(d, n, world, rank, order)
     c0, c1 = sharding.column_range(d, n, world, rank)
     S = oracle.project_units(prob.grid, prob.U, prob.V, prob.sigma, d, n, u0, u1, order)
     A = oracle.vandermonde(prob.z, d, n, c0, c1)
@@ -44,7 +44,7 @@ def _worker(rank, world, port, d, n, m, order, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("d,n,m,order", [(3, 4, 6, 1), (3, 4, 6, 0), (2, 9, 5, 1)])
+@pytest.mark.parametrize("d,n,m,order", [(3, 4, 6, 1), (3, 4, 6, 0), (2, 9, 5, 1), (2, 9, 5, 2), (3, 4, 6, 2)])
 def test_allreduce_pencil_world2_gloo(tmp_path, oracle_mod, d, n, m, order):
     import workload as W
     out = str(tmp_path / "res.npz")
@@ -70,11 +70,26 @@ def test_split_range_partitions(total, parts):
 
 
 def test_default_unit_order():
-    assert sharding.default_unit_order(3, 3) == 0   # l-sharding when ranks divide d
-    assert sharding.default_unit_order(2, 2) == 0
-    assert sharding.default_unit_order(3, 2) == 1   # row-major otherwise (cfg3 on 2/4 GPUs)
-    assert sharding.default_unit_order(2, 8) == 1
-    assert sharding.default_unit_order(2, 1) == 1
+    for d, world in [(3, 3), (2, 2), (3, 2), (2, 8), (2, 1)]:
+        assert sharding.default_unit_order(d, world) == sharding.UNITS_SHARED
+    assert sharding.unit_count(2, 200, sharding.UNITS_SHARED) == 202 ** 2
+    assert sharding.unit_count(2, 200, sharding.UNITS_L_MAJOR) == 2 * 201 ** 2
+
+
+@pytest.mark.parametrize("d,n", [(1, 6), (2, 3), (3, 2)])
+def test_shared_units_cover_every_row_once(oracle_mod, d, n):
+    """Unit order 2: over [0, (n+2)^d) every row k of every T_l is covered exactly once (so a partition
+    of the units over ranks sums to the full pencil), and splitting the range splits the runs."""
+    N = (n + 1) ** d
+    E = (n + 2) ** d
+    for ell in range(1, d + 1):
+        runs = oracle_mod._shared_runs(d, n, ell, 0, E)
+        rows = [k for a, b in runs for k in range(a, b)]
+        assert rows == list(range(N))
+        cut = E // 3
+        left = oracle_mod._shared_runs(d, n, ell, 0, cut)
+        right = oracle_mod._shared_runs(d, n, ell, cut, E)
+        assert [k for a, b in left + right for k in range(a, b)] == list(range(N))
 
 
 def test_pack_unpack_roundtrip():
