@@ -366,7 +366,7 @@ def run_ours(args, cfg):
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded planted exponential sum, complex Gaussian noise 1e-6)",
-            "config": {"workload": f"{c.name}: d={d} n={n} N={N} m={m} noise={c.noise} (BASELINE configs[3])",
+            "config": {"workload": f"{c.name}: d={d} n={n} N={N} m={m} noise={c.noise} (BASELINE configs[{int(c.name[3:]) - 1}])",
                        "d": d, "n": n, "N": N, "m": m, "parallelism": f"dp{world} ({['l-major', 'row-major', 'shared'][order]} units)",
                        "l2": "flushed (256 MiB write) before every timed step, outside the timed interval",
                        "pencils_per_step": 1, "comm": "1 x all_reduce(SUM) of packed [S,G,b] per step" if world > 1 else "none"},

@@ -162,7 +162,9 @@ int prony_workspace_size(int kind, int d, int n, int m, size_t* bytes);
  *   S           device, d x m x m prony_c128, OVERWRITTEN with this call's partial sum
  *               (rows of S_l with no unit in range are zero).
  *   workspace   device scratch of workspace_bytes >= prony_workspace_size(PRONY_WS_PROJECT).
- *   dev_status  nullable device int32 (no device-side failure modes in this call).
+ *   dev_status  nullable device int32: PRONY_ERR_SINGULAR when a sigma_j is not finite and positive or
+ *               sigma_min <= N eps_M sigma_max (the scale guard of SURVEY §8(b) / P:581); S is still
+ *               written (the column scale 1/sigma_j is applied regardless).
  *   stream      CUDA stream for all launches.
  */
 int prony_project(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,

@@ -178,7 +178,6 @@ int prony_project_ex(int d, int n, int m, const prony_c128* grid, const prony_c1
                      const double* sigma, int64_t unit_begin, int64_t unit_end, int unit_order, prony_c128* S,
                      void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream,
                      prony_exec_info* info) {
-  (void)dev_status;
   int64_t N = 0;
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
@@ -202,7 +201,7 @@ int prony_project_ex(int d, int n, int m, const prony_c128* grid, const prony_c1
   ProjPlan pl{};
   project_plan(g, sms, &pl);
   return project_launch(g, pl, (const double2*)grid, (const double2*)U, (const double2*)V, sigma, (double2*)S,
-                        workspace, sms, (cudaStream_t)stream, info, nullptr);
+                        workspace, sms, (cudaStream_t)stream, info, nullptr, 1, dev_status);
 }
 
 int prony_vandermonde_ls(int d, int n, int m, const prony_c128* z, const prony_c128* grid, int64_t col_begin,
@@ -246,7 +245,6 @@ int prony_ls_solve(int d, int m, const prony_c128* G, const prony_c128* b, const
 int prony_project_mu(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
                      const double* sigma, const prony_c128* mu, prony_c128* C, void* workspace, size_t workspace_bytes,
                      int32_t* dev_status, prony_stream_t stream) {
-  (void)dev_status;
   int64_t N = 0;
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
@@ -275,7 +273,8 @@ int prony_project_mu(int d, int n, int m, const prony_c128* grid, const prony_c1
   g.rows[0] = (int)N;  // one segment: the l = 0 operator on the combined grid
   ProjPlan pl{};
   project_plan(g, sms, &pl);
-  rc = project_launch(g, pl, gmu, (const double2*)U, (const double2*)V, sigma, Sd, w, sms, st, nullptr, nullptr, 0);
+  rc = project_launch(g, pl, gmu, (const double2*)U, (const double2*)V, sigma, Sd, w, sms, st, nullptr, nullptr, 0,
+                      dev_status);
   if (rc) return rc;
   if (cudaMemcpyAsync(C, Sd, (size_t)m * m * sizeof(double2), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
     return PRONY_ERR_CUDA;
@@ -359,7 +358,8 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
   ProjPlan pl{};
   project_plan(g, sms, &pl);
   rc = project_launch(g, pl, (const double2*)(w + h.grid), (const double2*)(w + h.U), (const double2*)(w + h.V),
-                      (const double*)(w + h.sigma), (double2*)(w + h.S), w + h.inner, sms, st, nullptr, ev_u);
+                      (const double*)(w + h.sigma), (double2*)(w + h.S), w + h.inner, sms, st, nullptr, ev_u, 1,
+                      dst);
   if (rc == PRONY_OK)
     rc = ls_launch(d, n, m, (int)N, (const double2*)(w + h.z), (const double2*)(w + h.grid), 0, N, nullptr,
                    (double2*)(w + h.G), (double2*)(w + h.b), (double2*)(w + h.c), (double*)(w + h.t),

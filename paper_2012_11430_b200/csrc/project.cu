@@ -505,9 +505,24 @@ __global__ void __launch_bounds__(kReduceThreads, 1) k_reduce(RedParams p) {
   }
 }
 
-// S[l][i][j] = (sum_{p < RP} S_part[l][p][i][j]) / sigma_j   (fixed order)
+// S[l][i][j] = (sum_{p < RP} S_part[l][p][i][j]) / sigma_j   (fixed order).
+// Scale guard (SPEC compute_S "sigma_m below underflow guard"): a sigma that is not
+// finite and positive, or below N eps_M sigma_max (the rank rule of P:581), reports PRONY_ERR_SINGULAR
+// in the status word; S is still written.
 __global__ void k_finalize(int d, int m, int RP, const double2* __restrict__ Spart, const double* __restrict__ sigma,
-                           double2* __restrict__ S) {
+                           double2* __restrict__ S, int N, int32_t* __restrict__ status) {
+  if (status && blockIdx.x == 0 && threadIdx.x == 0) {
+    double smax = 0.0;
+    bool bad = false;
+    for (int j = 0; j < m; ++j) {
+      const double sj = sigma[j];
+      if (!(sj > 0.0) || !isfinite(sj)) bad = true;
+      else smax = fmax(smax, sj);
+    }
+    for (int j = 0; j < m && !bad; ++j)
+      if (sigma[j] <= (double)N * 2.220446049250313e-16 * smax) bad = true;
+    if (bad) set_status(status, PRONY_ERR_SINGULAR);
+  }
   const int64_t total = (int64_t)d * m * m;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int l = (int)(e / ((int64_t)m * m));
@@ -660,7 +675,7 @@ static int launch_reduce_t(const RedParams& r, dim3 rgrid, cudaStream_t st, int 
 
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
                    const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
-                   prony_exec_info* info, cudaEvent_t wait_before_reduce, int ell_base) {
+                   prony_exec_info* info, cudaEvent_t wait_before_reduce, int ell_base, int32_t* dev_status) {
   const WsLayout wl = ws_layout(g.d, g.n, g.N, g.m, sm_count);
   char* w = (char*)ws;
   int32_t* ptab = (int32_t*)(w + wl.ptab);
@@ -782,7 +797,8 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   }
   if (lrc != PRONY_OK) return lrc;
   const int64_t tot = (int64_t)g.d * g.m * g.m;
-  k_finalize<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256, 0, st>>>(g.d, g.m, pl.RP, Spart, sigma, S);
+  k_finalize<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256, 0, st>>>(g.d, g.m, pl.RP, Spart, sigma, S,
+                                                                                  g.N, dev_status);
   if (info) {
     info->launches = g.shared ? 5 : 4;  // k_prep (+ k_prep_ext), k_project, k_reduce, k_finalize
     info->main_grid[0] = (int)grd.x;

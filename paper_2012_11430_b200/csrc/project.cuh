@@ -70,7 +70,8 @@ int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl);
 size_t project_workspace_bytes(int d, int n, int N, int m, int sm_count);
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
                    const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
-                   prony_exec_info* info, cudaEvent_t wait_before_reduce = nullptr, int ell_base = 1);
+                   prony_exec_info* info, cudaEvent_t wait_before_reduce = nullptr, int ell_base = 1,
+                   int32_t* dev_status = nullptr);
 __global__ void k_combine_grid(int d, int n, int64_t box, const double2* grid, const double2* mu, double2* out);
 
 size_t apply_workspace_bytes(int d, int n, int N);

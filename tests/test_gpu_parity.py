@@ -451,3 +451,21 @@ def test_accuracy_table_on_device(pb, orc):
         rows[eps] = errs
     for i in range(3):
         assert 300 < rows[1e-6][i] / rows[1e-9][i] < 3000
+
+
+@pytest.mark.parametrize("bad", ["tiny", "zero", "nan"])
+def test_project_sigma_guard(pb, orc, bad):
+    """Scale guard (SURVEY §8(b) conventions; SPEC compute_S errors): sigma_min <= N eps sigma_max,
+    a zero or a non-finite sigma -> PRONY_ERR_SINGULAR in the device status word; a healthy sigma -> 0."""
+    prob = problem(2, 6, 4, 31, random_uv=True)
+    c = prob.cfg
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    run_project(pb, prob, dev_status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    sigma = prob.sigma.copy()
+    sigma[-1] = {"tiny": sigma[0] * c.N * 1e-17, "zero": 0.0, "nan": np.nan}[bad]
+    st.zero_()
+    pb.project(dev(prob.grid), dev(prob.U), dev(prob.V), dev(sigma), c.d, c.n, c.m, dev_status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == pb.PRONY_ERR_SINGULAR
