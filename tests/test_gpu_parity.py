@@ -79,14 +79,41 @@ def test_project_configs_full_oracle(pb, orc, name):
     (2, 11, 64, 0.0),      # m = 64 (WN = 1, NT = 8 -> WN = 2 path)
     (2, 12, 100, 1e-6),    # m = 100 (WN = 2, NT = 7), N = 169
     (2, 11, 128, 0.0),     # m = 128 = PRONY_MAX_M (NT = 8, WN = 2)
+    (6, 1, 5, 1e-6),       # d = 6: E = 729 > dN = 384
+    (8, 1, 3, 0.0),        # d = 8 = PRONY_MAX_D, N = 256, E = 6561
+    (1, 3, 4, 0.0),        # d = 1, N = 4 = m (full rank), E = N + 1
 ])
-def test_project_edge_shapes(pb, orc, d, n, m, noise):
+@pytest.mark.parametrize("order", [2, 0])
+def test_project_edge_shapes(pb, orc, d, n, m, noise, order):
     prob = problem(d, n, m, 1000 + d * 100 + n + m, noise, random_uv=True)
-    S = run_project(pb, prob)
+    S = run_project(pb, prob, unit_order=order)
     torch.cuda.synchronize()
     S_or = orc.project(prob.grid, prob.U, prob.V, prob.sigma, d, n)
     for l in range(d):
         assert rel(S[l], S_or[l]) <= TOL
+
+
+def test_project_shared_random_partitions(pb, orc):
+    """Random partitions of the SHARED unit space [0, (n+2)^d) over 2-9 'ranks' sum to the full pencil
+    (the multi-GPU decomposition), each partial equal to the oracle's rows of T_l it stands for."""
+    rng = np.random.default_rng(2024)
+    for d, n, m in [(2, 20, 12), (3, 7, 9)]:
+        prob = problem(d, n, m, 300 + d, 1e-6, random_uv=True)
+        E = (n + 2) ** d
+        full = orc.project(prob.grid, prob.U, prob.V, prob.sigma, d, n)
+        for parts in (2, 5, 9):
+            cuts = np.sort(rng.choice(np.arange(1, E), size=parts - 1, replace=False))
+            cuts = [0, *cuts.tolist(), E]
+            acc = torch.zeros((d, m, m), dtype=torch.complex128, device="cuda")
+            for a, b in zip(cuts, cuts[1:]):
+                S = run_project(pb, prob, unit_begin=a, unit_end=b, unit_order=2)
+                acc += S
+                if parts == 2:
+                    S_or = orc.project_units(prob.grid, prob.U, prob.V, prob.sigma, d, n, a, b, 2)
+                    for l in range(d):
+                        assert rel(S[l], S_or[l]) <= TOL
+            for l in range(d):
+                assert rel(acc[l], full[l]) <= TOL
 
 
 @pytest.mark.parametrize("order", [0, 1, 2])
