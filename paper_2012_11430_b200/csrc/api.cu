@@ -314,41 +314,6 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
   char* w = (char*)workspace;
   int64_t box = 1;
   for (int i = 0; i < d; ++i) box *= (2 * (int64_t)n + 2);
-  // Two streams, created for this call only: `st` carries grid/V/sigma -> the projection; `s2` carries
-  // U (needed only by k_reduce, so its copy overlaps k_project) and z -> the LS step (overlaps too).
-  cudaStream_t s2 = nullptr;
-  cudaEvent_t ev_in = nullptr, ev_grid = nullptr, ev_u = nullptr, ev_done = nullptr;
-  auto cleanup = [&]() {
-    if (ev_in) cudaEventDestroy(ev_in);
-    if (ev_grid) cudaEventDestroy(ev_grid);
-    if (ev_u) cudaEventDestroy(ev_u);
-    if (ev_done) cudaEventDestroy(ev_done);
-    if (s2) cudaStreamDestroy(s2);
-  };
-  if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ev_grid, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ev_u, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) != cudaSuccess) {
-    cleanup();
-    return PRONY_ERR_CUDA;
-  }
-  auto ok = [](cudaError_t e) { return e == cudaSuccess; };
-  bool good = ok(cudaEventRecord(ev_in, st)) && ok(cudaStreamWaitEvent(s2, ev_in, 0)) &&
-              ok(cudaMemsetAsync(w + h.status, 0, sizeof(int32_t), st)) &&
-              ok(cudaMemcpyAsync(w + h.grid, grid, box * sizeof(double2), cudaMemcpyHostToDevice, st)) &&
-              ok(cudaEventRecord(ev_grid, st)) &&
-              ok(cudaMemcpyAsync(w + h.V, V, N * m * sizeof(double2), cudaMemcpyHostToDevice, st)) &&
-              ok(cudaMemcpyAsync(w + h.sigma, sigma, m * sizeof(double), cudaMemcpyHostToDevice, st)) &&
-              ok(cudaMemcpyAsync(w + h.U, U, N * m * sizeof(double2), cudaMemcpyHostToDevice, s2)) &&
-              ok(cudaEventRecord(ev_u, s2)) &&
-              ok(cudaMemcpyAsync(w + h.z, z, (size_t)m * d * sizeof(double2), cudaMemcpyHostToDevice, s2)) &&
-              ok(cudaStreamWaitEvent(s2, ev_grid, 0));
-  if (!good) {
-    cleanup();
-    return PRONY_ERR_CUDA;
-  }
-  int32_t* dst = (int32_t*)(w + h.status);
   ProjGeom g{};
   g.d = d;
   g.n = n;
@@ -357,24 +322,67 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
   unit_rows(d, n, N, 0, ext_rows(d, n), PRONY_UNITS_SHARED, &g);
   ProjPlan pl{};
   project_plan(g, sms, &pl);
+  // Streams created for this call only: `st` carries grid, the V rows of split-K chunk 0 and sigma ->
+  // k_prep -> chunk 0 of the projection; `s2` carries the rest of V (after chunk 0's rows: the link is
+  // not shared) -> its Vsum rows -> chunks 1..KC-1, then U (needed only by k_reduce); `s3` carries z ->
+  // the LS step. So only chunk 0's V rows are copied before the first DMMA.
+  const bool split = pl.KC > 1;
+  const int64_t v0 = split ? std::min<int64_t>(pl.chunk_w, N) : N;
+  cudaStream_t s2 = nullptr, s3 = nullptr;
+  cudaEvent_t ev[7] = {};  // in, grid, v0, u, done, split a, split b
+  auto cleanup = [&]() {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    if (s2) cudaStreamDestroy(s2);
+    if (s3) cudaStreamDestroy(s3);
+  };
+  bool good = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking) == cudaSuccess;
+  for (int i = 0; i < 7 && good; ++i) good = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!good) {
+    cleanup();
+    return PRONY_ERR_CUDA;
+  }
+  cudaEvent_t ev_in = ev[0], ev_grid = ev[1], ev_v0 = ev[2], ev_u = ev[3], ev_done = ev[4];
+  auto ok = [](cudaError_t e) { return e == cudaSuccess; };
+  const size_t vrow = (size_t)m * sizeof(double2);
+  good = ok(cudaEventRecord(ev_in, st)) && ok(cudaStreamWaitEvent(s2, ev_in, 0)) &&
+         ok(cudaStreamWaitEvent(s3, ev_in, 0)) && ok(cudaMemsetAsync(w + h.status, 0, sizeof(int32_t), st)) &&
+         ok(cudaMemcpyAsync(w + h.grid, grid, box * sizeof(double2), cudaMemcpyHostToDevice, st)) &&
+         ok(cudaEventRecord(ev_grid, st)) &&
+         ok(cudaMemcpyAsync(w + h.V, V, v0 * vrow, cudaMemcpyHostToDevice, st)) &&
+         ok(cudaMemcpyAsync(w + h.sigma, sigma, m * sizeof(double), cudaMemcpyHostToDevice, st)) &&
+         ok(cudaEventRecord(ev_v0, st)) && ok(cudaStreamWaitEvent(s2, ev_v0, 0)) &&
+         (v0 == N || ok(cudaMemcpyAsync(w + h.V + v0 * vrow, (const char*)V + v0 * vrow, (N - v0) * vrow,
+                                        cudaMemcpyHostToDevice, s2))) &&
+         ok(cudaMemcpyAsync(w + h.U, U, N * vrow, cudaMemcpyHostToDevice, s2)) && ok(cudaEventRecord(ev_u, s2)) &&
+         ok(cudaStreamWaitEvent(s3, ev_grid, 0)) &&
+         ok(cudaMemcpyAsync(w + h.z, z, (size_t)m * d * sizeof(double2), cudaMemcpyHostToDevice, s3));
+  if (!good) {
+    cleanup();
+    return PRONY_ERR_CUDA;
+  }
+  int32_t* dst = (int32_t*)(w + h.status);
+  ProjSplit sp{s2, ev[5], ev[6]};
   rc = project_launch(g, pl, (const double2*)(w + h.grid), (const double2*)(w + h.U), (const double2*)(w + h.V),
                       (const double*)(w + h.sigma), (double2*)(w + h.S), w + h.inner, sms, st, nullptr, ev_u, 1,
-                      dst);
+                      dst, split ? &sp : nullptr);
   if (rc == PRONY_OK)
     rc = ls_launch(d, n, m, (int)N, (const double2*)(w + h.z), (const double2*)(w + h.grid), 0, N, nullptr,
                    (double2*)(w + h.G), (double2*)(w + h.b), (double2*)(w + h.c), (double*)(w + h.t),
-                   w + h.inner_ls, dst, sms, s2, nullptr);
+                   w + h.inner_ls, dst, sms, s3, nullptr);
   if (rc != PRONY_OK) {
     cudaStreamSynchronize(s2);
+    cudaStreamSynchronize(s3);
     cleanup();
     return rc;
   }
   auto d2h = [&](void* dstp, size_t off, size_t bytes, cudaStream_t s) {
     return dstp == nullptr || cudaMemcpyAsync(dstp, w + off, bytes, cudaMemcpyDeviceToHost, s) == cudaSuccess;
   };
-  good = d2h(G, h.G, (size_t)m * m * sizeof(double2), s2) && d2h(b, h.b, m * sizeof(double2), s2) &&
-         d2h(c, h.c, m * sizeof(double2), s2) && d2h(t, h.t, (size_t)m * d * sizeof(double), s2) &&
-         ok(cudaEventRecord(ev_done, s2)) && d2h(S, h.S, (size_t)d * m * m * sizeof(double2), st) &&
+  good = d2h(G, h.G, (size_t)m * m * sizeof(double2), s3) && d2h(b, h.b, m * sizeof(double2), s3) &&
+         d2h(c, h.c, m * sizeof(double2), s3) && d2h(t, h.t, (size_t)m * d * sizeof(double), s3) &&
+         ok(cudaEventRecord(ev_done, s3)) && d2h(S, h.S, (size_t)d * m * m * sizeof(double2), st) &&
          ok(cudaStreamWaitEvent(st, ev_done, 0)) && d2h(status_out, h.status, sizeof(int32_t), st) &&
          ok(cudaStreamSynchronize(st));
   cleanup();

@@ -34,7 +34,7 @@ static int cmul_mode() {
 // ---------------------------------------------------------------------------- prep
 __global__ void k_prep(int d, int n, int N, int m, int ldv, int NP, int64_t box, const double2* __restrict__ grid,
                        const double2* __restrict__ V, int32_t* __restrict__ ptab, double* __restrict__ gsum,
-                       double* __restrict__ vsum) {
+                       double* __restrict__ vsum, int vrows) {
   const int L = 2 * n + 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -55,7 +55,7 @@ __global__ void k_prep(int d, int n, int N, int m, int ldv, int NP, int64_t box,
     const double2 v = grid[e];
     gsum[e] = v.x + v.y;
   }
-  const int64_t nv = (int64_t)N * NP;
+  const int64_t nv = (int64_t)vrows * NP;  // Vsum rows [0, vrows) (the rest: k_vsum)
   for (int64_t e = t0; e < nv; e += stride) {
     const int64_t h = e / NP;
     const int c = (int)(e % NP);
@@ -65,6 +65,21 @@ __global__ void k_prep(int d, int n, int N, int m, int ldv, int NP, int64_t box,
       s = v.x + v.y;
     }
     vsum[e] = s;
+  }
+}
+
+// Vsum rows [r0, r1) (the part of V that arrives after k_prep ran, prony_pencil_host)
+__global__ void k_vsum(int r0, int r1, int m, int ldv, int NP, const double2* __restrict__ V, double* __restrict__ vsum) {
+  const int64_t nv = (int64_t)(r1 - r0) * NP;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nv; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = r0 + e / NP;
+    const int c = (int)(e % NP);
+    double sv = 0.0;
+    if (c < m) {
+      const double2 v = V[h * ldv + c];
+      sv = v.x + v.y;
+    }
+    vsum[h * NP + c] = sv;
   }
 }
 
@@ -177,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
   const int rows = p.rows[l];
   const int rb0 = blockIdx.x * BM;
   if (rb0 >= rows) return;  // whole CTA exits together
-  const int chunk = blockIdx.y;
+  const int chunk = blockIdx.y + p.chunk_base;
   const int h_begin = chunk * p.chunk_w;
   const int h_end = min(h_begin + p.chunk_w, p.N);
   const int KT = (h_end - h_begin + kBK - 1) / kBK;
@@ -675,7 +690,8 @@ static int launch_reduce_t(const RedParams& r, dim3 rgrid, cudaStream_t st, int 
 
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
                    const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
-                   prony_exec_info* info, cudaEvent_t wait_before_reduce, int ell_base, int32_t* dev_status) {
+                   prony_exec_info* info, cudaEvent_t wait_before_reduce, int ell_base, int32_t* dev_status,
+                   const ProjSplit* sp) {
   const WsLayout wl = ws_layout(g.d, g.n, g.N, g.m, sm_count);
   char* w = (char*)ws;
   int32_t* ptab = (int32_t*)(w + wl.ptab);
@@ -705,7 +721,10 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   const int nrb = (pl.max_rows + pl.shape.BM - 1) / pl.shape.BM;
   if (pl.KC > 1 && cudaMemsetAsync(counters, 0, (size_t)pslots * nrb * sizeof(int), st) != cudaSuccess)
     return PRONY_ERR_CUDA;
-  k_prep<<<2 * sm_count, 256, 0, st>>>(g.d, g.n, g.N, g.m, g.m, pl.shape.NP, box, grid, V, ptab, gsum, vsum);
+  const bool split = sp && pl.KC > 1;
+  const int vrows0 = split ? std::min(pl.chunk_w, g.N) : g.N;
+  k_prep<<<2 * sm_count, 256, 0, st>>>(g.d, g.n, g.N, g.m, g.m, pl.shape.NP, box, grid, V, ptab, gsum, vsum,
+                                       vrows0);
   if (g.shared) k_prep_ext<<<sm_count, 256, 0, st>>>(g.d, g.n, E, etab, umap);
 
   ProjParams p{};
@@ -765,22 +784,40 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   dim3 rgrd(pl.RP, g.d, (pl.shape.NP + pl.shape.BI - 1) / pl.shape.BI);
   const int NT = pl.shape.NT, WN = pl.shape.WN;
   const int mode = cmul_mode();
-  int lrc = PRONY_OK;
-  switch (WN * 16 + NT) {
+  auto launch_main = [&](const ProjParams& pp, dim3 gg, cudaStream_t ss, prony_exec_info* inf) -> int {
+    switch (WN * 16 + NT) {
 #define PRONY_CASE(nt, wn) \
   case wn * 16 + nt:       \
-    lrc = launch_project_t<nt, wn>(p, grd, st, mode, info); \
-    break;
+    return launch_project_t<nt, wn>(pp, gg, ss, mode, inf);
 #if PRONY_CONSUMER_WARPS == 12
-    PRONY_CASE(1, 2) PRONY_CASE(1, 3) PRONY_CASE(2, 3) PRONY_CASE(3, 3) PRONY_CASE(4, 3) PRONY_CASE(5, 3)
-    PRONY_CASE(4, 4)
+      PRONY_CASE(1, 2) PRONY_CASE(1, 3) PRONY_CASE(2, 3) PRONY_CASE(3, 3) PRONY_CASE(4, 3) PRONY_CASE(5, 3)
+      PRONY_CASE(4, 4)
 #else
-    PRONY_CASE(1, 2) PRONY_CASE(2, 2) PRONY_CASE(3, 2) PRONY_CASE(4, 2) PRONY_CASE(5, 2) PRONY_CASE(6, 2)
-    PRONY_CASE(7, 2) PRONY_CASE(8, 2)
+      PRONY_CASE(1, 2) PRONY_CASE(2, 2) PRONY_CASE(3, 2) PRONY_CASE(4, 2) PRONY_CASE(5, 2) PRONY_CASE(6, 2)
+      PRONY_CASE(7, 2) PRONY_CASE(8, 2)
 #endif
 #undef PRONY_CASE
-    default:
-      return PRONY_ERR_RANGE;
+      default:
+        return PRONY_ERR_RANGE;
+    }
+  };
+  int lrc = PRONY_OK;
+  if (split) {
+    // chunk 0 (V rows [0, chunk_w), already resident) on st; chunks 1..KC-1 on s_rest once the rest of V
+    // (enqueued there by the caller) and its Vsum rows are in; the fixup counts arrivals across both
+    if (cudaEventRecord(sp->ev_a, st) != cudaSuccess || cudaStreamWaitEvent(sp->s_rest, sp->ev_a, 0) != cudaSuccess)
+      return PRONY_ERR_CUDA;
+    lrc = launch_main(p, dim3(grd.x, 1, grd.z), st, info);
+    if (lrc != PRONY_OK) return lrc;
+    k_vsum<<<2 * sm_count, 256, 0, sp->s_rest>>>(vrows0, g.N, g.m, g.m, pl.shape.NP, V, vsum);
+    ProjParams pr = p;
+    pr.chunk_base = 1;
+    lrc = launch_main(pr, dim3(grd.x, pl.KC - 1, grd.z), sp->s_rest, nullptr);
+    if (lrc != PRONY_OK) return lrc;
+    if (cudaEventRecord(sp->ev_b, sp->s_rest) != cudaSuccess || cudaStreamWaitEvent(st, sp->ev_b, 0) != cudaSuccess)
+      return PRONY_ERR_CUDA;
+  } else {
+    lrc = launch_main(p, grd, st, info);
   }
   if (lrc != PRONY_OK) return lrc;
   // U is first read by k_reduce: a caller may still be copying it on another stream
@@ -800,7 +837,8 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   k_finalize<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256, 0, st>>>(g.d, g.m, pl.RP, Spart, sigma, S,
                                                                                   g.N, dev_status);
   if (info) {
-    info->launches = g.shared ? 5 : 4;  // k_prep (+ k_prep_ext), k_project, k_reduce, k_finalize
+    info->launches = (g.shared ? 5 : 4) + (split ? 2 : 0);  // k_prep (+ k_prep_ext), k_project, k_reduce,
+                                                            // k_finalize (+ k_vsum, 2nd k_project)
     info->main_grid[0] = (int)grd.x;
     info->main_grid[1] = (int)grd.y;
     info->main_grid[2] = (int)grd.z;
@@ -930,7 +968,7 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
     project_plan(gg, sm_count, &pl);
     const int nrb = (pl.max_rows + pl.shape.BM - 1) / pl.shape.BM;
     if (pl.KC > 1 && cudaMemsetAsync(counters, 0, (size_t)nrb * sizeof(int), st) != cudaSuccess) return PRONY_ERR_CUDA;
-    k_prep<<<2 * sm_count, 256, 0, st>>>(d, n, N, wcols, ldx, pl.shape.NP, box, g, X + c0, ptab, gsum, vsum);
+    k_prep<<<2 * sm_count, 256, 0, st>>>(d, n, N, wcols, ldx, pl.shape.NP, box, g, X + c0, ptab, gsum, vsum, N);
     ProjParams p{};
     p.grid = g;
     p.gsum = gsum;

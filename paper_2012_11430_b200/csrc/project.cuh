@@ -53,6 +53,7 @@ struct ProjParams {
   int* counters;  // [d][nrb] split-K arrival counters (zeroed per call)
   int N, m, NP, chunk_w, R_tot, KC, nrb;
   int box;  // grid size (debug index checks)
+  int chunk_base;  // first split-K chunk of this launch (blockIdx.y + chunk_base)
   int kb[PRONY_MAX_D], rows[PRONY_MAX_D], yoff[PRONY_MAX_D], shift[PRONY_MAX_D];
 };
 
@@ -65,13 +66,22 @@ struct RedParams {
   int kb[PRONY_MAX_D], rows[PRONY_MAX_D], yoff[PRONY_MAX_D];
 };
 
+// Copy/compute overlap for callers whose V arrives in two parts (prony_pencil_host): when KC > 1 the
+// caller has made V rows [0, chunk_w) resident in stream order on `st` and enqueues the rest on
+// `s_rest` BEFORE calling project_launch; split-K chunk 0 then runs on `st` while chunks 1..KC-1 (and
+// their Vsum rows) run on `s_rest`; `ev_a` / `ev_b` are caller-owned scratch events.
+struct ProjSplit {
+  cudaStream_t s_rest;
+  cudaEvent_t ev_a, ev_b;
+};
+
 ProjShape proj_shape(int m);
 int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl);
 size_t project_workspace_bytes(int d, int n, int N, int m, int sm_count);
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
                    const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
                    prony_exec_info* info, cudaEvent_t wait_before_reduce = nullptr, int ell_base = 1,
-                   int32_t* dev_status = nullptr);
+                   int32_t* dev_status = nullptr, const ProjSplit* split = nullptr);
 __global__ void k_combine_grid(int d, int n, int64_t box, const double2* grid, const double2* mu, double2* out);
 
 size_t apply_workspace_bytes(int d, int n, int N);
