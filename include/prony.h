@@ -65,7 +65,7 @@
 extern "C" {
 #endif
 
-#define PRONY_ABI_VERSION 1
+#define PRONY_ABI_VERSION 2  /* 2: PRONY_UNITS_SHARED, prony_lanczos_svd, PRONY_WS_LANCZOS */
 #define PRONY_MAX_D 8
 #define PRONY_MAX_M 128
 
