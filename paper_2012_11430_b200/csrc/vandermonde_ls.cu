@@ -167,48 +167,73 @@ __global__ void k_ls_reduce(int m, int CB, const double2* __restrict__ Gpart, co
   }
 }
 
-// One CTA of kSolveThreads. The lower triangle of G lives packed in shared memory (A[i][k] at
-// i(i+1)/2 + k). Right-looking Cholesky G = L L^H with lazily scaled columns: column j is never
-// rescaled in place, L[i][j] = A[i][j] / sqrt(d_j) with d_j the pivot (inv[j] = 1/sqrt(d_j)), so each
-// column costs ONE barrier (the trailing update reads column j and writes columns > j only).
+// One CTA of kSolveThreads. Right-looking Cholesky G = L L^H with lazily scaled columns: column j is
+// never rescaled, L[i][j] = A[i][j] / sqrt(d_j) with d_j the pivot (inv[j] = 1/sqrt(d_j)). The lower
+// triangle lives in registers (each thread owns <= kSolveOwn entries); per column the owners publish
+// column j to a double-buffered shared vector, ONE barrier, and every owner of an entry right of it
+// applies the rank-1 update. The factor is then stored packed (A[i][k] at i(i+1)/2 + k) for the
+// substitutions.
 // Forward / backward substitution run in one warp with the right-hand side in registers.
 constexpr int kSolveMaxRowsPerLane = (PRONY_MAX_M + 31) / 32;
+constexpr int kSolveOwn = (PRONY_MAX_M * (PRONY_MAX_M + 1) / 2 + kSolveThreads - 1) / kSolveThreads;
 __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const double2* __restrict__ G,
                                                          const double2* __restrict__ b,
                                                          const double2* __restrict__ z, double2* __restrict__ c,
                                                          double* __restrict__ t, int32_t* status) {
   extern __shared__ __align__(16) double2 As[];  // m(m+1)/2 packed
   __shared__ double inv[PRONY_MAX_M];
+  __shared__ double2 colbuf[2][PRONY_MAX_M];  // the pivot column, double-buffered
   __shared__ int bad;
   const int tid = threadIdx.x;
   auto at = [](int i, int k) { return i * (i + 1) / 2 + k; };
   if (tid == 0) bad = 0;
-  for (int i = tid; i < m; i += kSolveThreads)
-    for (int k = 0; k <= i; ++k) As[at(i, k)] = G[(size_t)i * m + k];
-  __syncthreads();
+  // each thread owns up to kSolveOwn entries of the lower triangle, kept in registers for the whole
+  // factorization: entry e = tid + kSolveThreads s of the packed order
+  const int T = m * (m + 1) / 2;
+  double2 val[kSolveOwn];
+  int oi[kSolveOwn], ok[kSolveOwn];
+#pragma unroll
+  for (int s = 0; s < kSolveOwn; ++s) {
+    const int e = tid + kSolveThreads * s;
+    oi[s] = -1;
+    ok[s] = -1;
+    val[s] = make_double2(0.0, 0.0);
+    if (e < T) {
+      int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while (i * (i + 1) / 2 > e) --i;
+      while ((i + 1) * (i + 2) / 2 <= e) ++i;
+      oi[s] = i;
+      ok[s] = e - i * (i + 1) / 2;
+      val[s] = G[(size_t)i * m + ok[s]];
+    }
+  }
   for (int j = 0; j < m; ++j) {
-    const double dj = As[at(j, j)].x;  // final after the previous barrier
-    if (!(dj > 0.0)) {                 // uniform: every thread read the same value
+    double2* buf = colbuf[j & 1];
+#pragma unroll
+    for (int s = 0; s < kSolveOwn; ++s)
+      if (ok[s] == j) buf[oi[s]] = val[s];  // publish column j (final: updated through column j-1)
+    __syncthreads();
+    const double dj = buf[j].x;  // uniform
+    if (!(dj > 0.0)) {
       if (tid == 0) bad = 1;
       break;
     }
     const double invd = 1.0 / dj;  // L[i][j] conj(L[k][j]) = A[i][j] conj(A[k][j]) / d_j
     if (tid == 0) inv[j] = sqrt(invd);
-    const int r = m - j - 1;
-    for (int ii = tid / 8; ii < r; ii += kSolveThreads / 8) {
-      const int i = j + 1 + ii;
-      const double2 a = As[at(i, j)];
-      for (int kk = tid % 8; kk <= ii; kk += 8) {
-        const int k = j + 1 + kk;
-        const double2 bb = As[at(k, j)];
-        double2 v = As[at(i, k)];
-        v.x -= (a.x * bb.x + a.y * bb.y) * invd;
-        v.y -= (a.y * bb.x - a.x * bb.y) * invd;
-        As[at(i, k)] = v;
+#pragma unroll
+    for (int s = 0; s < kSolveOwn; ++s) {
+      if (ok[s] > j) {
+        const double2 a = buf[oi[s]], bb = buf[ok[s]];
+        val[s].x -= (a.x * bb.x + a.y * bb.y) * invd;
+        val[s].y -= (a.y * bb.x - a.x * bb.y) * invd;
       }
     }
-    __syncthreads();
+    // no second barrier: column j+1 goes to the other buffer, and this buffer is rewritten only after
+    // the next iteration's barrier, which every thread reaches after its reads here
   }
+#pragma unroll
+  for (int s = 0; s < kSolveOwn; ++s)
+    if (oi[s] >= 0) As[at(oi[s], ok[s])] = val[s];  // lazily scaled factor for the substitutions
   __syncthreads();
   if (bad) {
     if (tid == 0) set_status(status, PRONY_ERR_SINGULAR);
