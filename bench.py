@@ -385,6 +385,8 @@ def run_ours(args, cfg):
                          "executed_tflops": achieved * cm * (8 * ((m + 7) // 8)) / m,
                          "executed_frac": (achieved * cm * (8 * ((m + 7) // 8)) / m) / peak if peak else None,
                          "cmul": "4M" if cm == 1.0 else "3M",
+                         # also against the planning figure 148 SM x 128 FP64 flop/clk x 1.965 GHz
+                         "planning_peak": 37.2, "executed_frac_vs_planning": (achieved * cm * (8 * ((m + 7) // 8)) / m) / 37.2,
                          "share_of_step": sum(proj_ms) / sum(step_ms),
                          "grid": list(infos_p[0].main_grid), "split_k": infos_p[0].split_k},
             "kernels_ms": {"k_project": statistics.mean(proj_ms), "k_vls": statistics.mean(vls_ms)},
