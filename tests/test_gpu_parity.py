@@ -356,6 +356,22 @@ def test_pencil_host_matches_device_path(pb, orc):
     assert W.torus_dist_inf(out["t"], prob.t).max() <= 1e-8
 
 
+@pytest.mark.parametrize("d,n,m,noise", [(1, 300, 9, 1e-6), (3, 9, 13, 0.0), (2, 40, 37, 1e-6), (2, 5, 3, 0.0)])
+def test_pencil_host_shapes(pb, orc, d, n, m, noise):
+    """prony_pencil_host over shapes whose plans split K into several chunks (the copy/compute overlap
+    path: chunk 0 on the caller's stream, chunks 1.. behind the rest of V) and a single-chunk one."""
+    prob = problem(d, n, m, 700 + d + n + m, noise, random_uv=True)
+    c = prob.cfg
+    out = pb.pencil_host(prob.grid, prob.U, prob.V, prob.sigma, prob.z, d, n, m)
+    assert out["status"] == 0
+    S_or = orc.project(prob.grid, prob.U, prob.V, prob.sigma, d, n)
+    for l in range(d):
+        assert rel(out["S"][l], S_or[l]) <= TOL
+    A_or = orc.vandermonde(prob.z, d, n)
+    G_or, b_or = orc.ls_products(A_or, prob.grid, d, n)
+    assert rel(out["G"], G_or) <= TOL and rel(out["b"], b_or) <= TOL
+
+
 def test_end_to_end_recovery_with_oracle_tail(pb, orc):
     """Algorithm 1 with the GPU pencil: S from the device, then the oracle's eig / diagonalization
     (NEXT-1 runs those on the device); t within 1e-8 of planted (noise-free cfg3)."""
