@@ -900,6 +900,118 @@ __global__ void k_copy_cols(int N, int w, int NP, const double2* __restrict__ Y0
   }
 }
 
+// ---------------------------------------------------------------------------- Toeplitz matvec (r = 1)
+// The Lanczos recurrence (NEXT-3, Alg. 2) applies T and T^H to ONE vector per step. On the DMMA path
+// that single column is padded to an 8-wide n-tile and the A gather (24 B per T element) bounds it
+// (8.1 ms at cfg4). This DFMA kernel uses the Toeplitz structure along the last coordinate instead:
+// with k = (k', a), h = (h', b) (a, b the last coordinate, k', h' the first d-1 coordinates),
+//   T[k, h] = g[L (Pp(k') - Pp(h')) + shift + a - b],   Pp = linear box offset of the prefix,
+// so for one (k', h') pair the (n+1) x (n+1) block is a 1-D Toeplitz block read from ONE window of
+// 2n+1 consecutive samples. CTA (k', slice s of h') stages window + x[h', :] in shared memory
+// (double-buffered cp.async) and each thread accumulates 4 consecutive outputs a with a sliding
+// register window (1 window load + 1 broadcast load per 4 complex MACs). Partial sums per slice are
+// reduced in fixed slice order (deterministic).
+constexpr int kMvThreads = 128;
+constexpr int kMvPerThread = 4;
+constexpr int kMvMaxBlocks = 4;  // a-blocks of kMvThreads * kMvPerThread outputs: n + 1 <= 2048
+constexpr int kMvMaxSlices = 16;
+
+__global__ void __launch_bounds__(kMvThreads) k_toeplitz_mv(int d, int n, int Mp, int S, const double2* __restrict__ g,
+                                                            int shift, const double2* __restrict__ x, int ldx,
+                                                            double2* __restrict__ ypart) {
+  extern __shared__ __align__(16) double2 mvs[];
+  const int A = n + 1, Wl = 2 * n + 1, L = 2 * n + 2;
+  const int WS = Wl + 4;  // window slot: 1 pad in front, 3 behind (reads of the 4-wide register window)
+  const int slot = WS + A;
+  const int kp = blockIdx.x, s = blockIdx.y, tid = threadIdx.x, nth = blockDim.x;
+  auto Pp = [&](int idx) {
+    int P = 0, mul = 1;
+    for (int i = d - 2; i >= 0; --i) {
+      P += (idx % A) * mul;
+      idx /= A;
+      mul *= L;
+    }
+    return P;
+  };
+  const int pk = Pp(kp);
+  const int hb = (int)((int64_t)Mp * s / S), he = (int)((int64_t)Mp * (s + 1) / S);
+  for (int e = tid; e < 2 * slot; e += nth) mvs[e] = make_double2(0.0, 0.0);  // pads stay zero
+  __syncthreads();
+  auto issue = [&](int hp, int buf) {
+    double2* w = mvs + buf * slot;
+    const int wbase = L * (pk - Pp(hp)) + shift - n;
+    const uint32_t sw = (uint32_t)__cvta_generic_to_shared(w + 1);
+    for (int j = tid; j < Wl; j += nth) cp_async16(sw + 16u * j, g + wbase + j, 16);
+    const uint32_t sx = (uint32_t)__cvta_generic_to_shared(w + WS);
+    for (int b = tid; b < A; b += nth) cp_async16(sx + 16u * b, x + (size_t)(hp * A + b) * ldx, 16);
+    cp_async_commit();
+  };
+  double2 acc[kMvMaxBlocks][kMvPerThread];
+#pragma unroll
+  for (int q = 0; q < kMvMaxBlocks; ++q)
+#pragma unroll
+    for (int r = 0; r < kMvPerThread; ++r) acc[q][r] = make_double2(0.0, 0.0);
+  if (hb < he) issue(hb, 0);
+  for (int hp = hb; hp < he; ++hp) {
+    const int buf = (hp - hb) & 1;
+    if (hp + 1 < he) {
+      issue(hp + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double2* w = mvs + buf * slot + 1;  // w[j] = g[wbase + j], j in [-1, Wl + 2] readable
+    const double2* xs = mvs + buf * slot + WS;
+#pragma unroll
+    for (int q = 0; q < kMvMaxBlocks; ++q) {
+      const int a0 = q * nth * kMvPerThread + kMvPerThread * tid;
+      if (a0 < A) {
+        // output a0 + r at column b reads w[a0 + r - b + n]
+        double2 w0 = w[a0 + n], w1 = w[a0 + n + 1], w2 = w[a0 + n + 2], w3 = w[a0 + n + 3];
+        double2 c0 = acc[q][0], c1 = acc[q][1], c2 = acc[q][2], c3 = acc[q][3];
+        for (int b = 0; b < A; ++b) {
+          const double2 xb = xs[b];
+          c0.x = fma(w0.x, xb.x, fma(-w0.y, xb.y, c0.x));
+          c0.y = fma(w0.x, xb.y, fma(w0.y, xb.x, c0.y));
+          c1.x = fma(w1.x, xb.x, fma(-w1.y, xb.y, c1.x));
+          c1.y = fma(w1.x, xb.y, fma(w1.y, xb.x, c1.y));
+          c2.x = fma(w2.x, xb.x, fma(-w2.y, xb.y, c2.x));
+          c2.y = fma(w2.x, xb.y, fma(w2.y, xb.x, c2.y));
+          c3.x = fma(w3.x, xb.x, fma(-w3.y, xb.y, c3.x));
+          c3.y = fma(w3.x, xb.y, fma(w3.y, xb.x, c3.y));
+          w3 = w2;
+          w2 = w1;
+          w1 = w0;
+          w0 = w[a0 + n - b - 1];
+        }
+        acc[q][0] = c0;
+        acc[q][1] = c1;
+        acc[q][2] = c2;
+        acc[q][3] = c3;
+      }
+    }
+    __syncthreads();  // the slot is refilled by the next iteration's issue
+  }
+  double2* yp = ypart + (size_t)s * Mp * A + (size_t)kp * A;
+#pragma unroll
+  for (int q = 0; q < kMvMaxBlocks; ++q)
+#pragma unroll
+    for (int r = 0; r < kMvPerThread; ++r) {
+      const int a = q * nth * kMvPerThread + kMvPerThread * tid + r;
+      if (a < A) yp[a] = acc[q][r];
+    }
+}
+
+// y[k * ldy] = sum_{s < S} ypart[s][k]   (fixed order)
+__global__ void k_mv_reduce(int N, int S, const double2* __restrict__ ypart, double2* __restrict__ y, int ldy) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    double2 a = ypart[k];
+    for (int s = 1; s < S; ++s) a = cadd(a, ypart[(size_t)s * N + k]);
+    y[(size_t)k * ldy] = a;
+  }
+}
+
 namespace {
 constexpr int kApplyMaxW = 120;  // columns per k_project pass (NT <= 5 over WN = 3 warps)
 struct ApplyLayout {
@@ -952,6 +1064,21 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
     s *= L;
   }
   const int shift = (int)(C0 + (ell >= 1 ? ipow(L, d - ell) : 0));
+  const char* emv = getenv("PRONY_APPLY");
+  if (r == 1 && d >= 2 && n + 1 >= 64 && n + 1 <= kMvMaxBlocks * kMvThreads * kMvPerThread &&
+      !(emv && emv[0] == 'd')) {
+    // single vector: DFMA Toeplitz matvec (k_toeplitz_mv) instead of the 8-wide DMMA tile
+    const int Mp = N / (n + 1);
+    const int S = std::max(1, std::min({kMvMaxSlices, Mp, (2 * sm_count * 4 + Mp - 1) / Mp}));
+    const size_t smem = (size_t)2 * ((2 * n + 1 + 4) + (n + 1)) * sizeof(double2);
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(k_toeplitz_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return PRONY_ERR_CUDA;
+    const int nth = std::min(kMvThreads, ((n + 1 + kMvPerThread - 1) / kMvPerThread + 31) / 32 * 32);
+    k_toeplitz_mv<<<dim3(Mp, S), nth, smem, st>>>(d, n, Mp, S, g, shift, X, ldx, Y);
+    k_mv_reduce<<<(N + 255) / 256, 256, 0, st>>>(N, S, Y, Yout, ldy);
+    return cudaGetLastError() == cudaSuccess ? PRONY_OK : PRONY_ERR_CUDA;
+  }
   const int npass = (r + kApplyMaxW - 1) / kApplyMaxW;
   const int mode = cmul_mode();
   for (int ps = 0; ps < npass; ++ps) {

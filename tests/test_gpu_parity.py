@@ -512,3 +512,52 @@ def test_project_sigma_guard(pb, orc, bad):
     pb.project(dev(prob.grid), dev(prob.U), dev(prob.V), dev(sigma), c.d, c.n, c.m, dev_status=st)
     torch.cuda.synchronize()
     assert int(st.item()) == pb.PRONY_ERR_SINGULAR
+
+
+def test_toeplitz_matvec_dfma_dense(pb, orc):
+    """The single-vector apply (DFMA Toeplitz matvec, taken for r = 1, d >= 2, n + 1 >= 64; NEXT-3's
+    operator) against the oracle's dense T_l and T^H, with a strided input column and output column."""
+    d, n = 2, 63
+    prob = problem(d, n, 3, 881, 1e-6, random_uv=True)
+    N = prob.cfg.N
+    rng = np.random.default_rng(9)
+    Xw = rng.standard_normal((N, 5)) + 1j * rng.standard_normal((N, 5))
+    Xd = dev(Xw)
+    grid = dev(prob.grid)
+    Yw = torch.zeros((N, 3), dtype=torch.complex128, device="cuda")
+    for ell in range(0, d + 1):
+        pb.toeplitz_apply(grid, Xd[:, 2:3], d, n, ell, out=Yw[:, 1:2])
+        T = orc.T_dense(prob.grid, d, n, ell)
+        assert rel(Yw[:, 1].cpu().numpy(), T @ Xw[:, 2]) <= 1e-13
+        del T
+    pb.toeplitz_apply(grid, Xd[:, 2:3], d, n, 0, conj=True, out=Yw[:, 1:2])
+    T = orc.T_dense(prob.grid, d, n, 0)
+    assert rel(Yw[:, 1].cpu().numpy(), T.conj().T @ Xw[:, 2]) <= 1e-13
+    Y = Yw.cpu().numpy()
+    assert np.all(Y[:, 0] == 0) and np.all(Y[:, 2] == 0)
+
+
+def test_toeplitz_matvec_dfma_d3_sampled(pb, orc, monkeypatch):
+    """d = 3, n = 63 (N = 262144): sampled rows of T_l x (l = 1..3) against the oracle (one row of T_l at
+    a time via oracle.project_rows with a one-hot U); T x and T^H x against the DMMA apply path."""
+    d, n = 3, 63
+    prob = problem(d, n, 2, 882, 0.0, random_uv=True)
+    N = prob.cfg.N
+    rng = np.random.default_rng(10)
+    x = rng.standard_normal((N, 1)) + 1j * rng.standard_normal((N, 1))
+    xd, grid = dev(x), dev(prob.grid)
+    rows = [0, 1, 63, 64, 4095, 4096, N // 2 + 17, N - 65, N - 1]
+    one = np.ones(1)
+    for ell in (1, 2, 3):
+        y = pb.toeplitz_apply(grid, xd, d, n, ell).cpu().numpy()[:, 0]
+        ref = []
+        for k in rows:
+            e = np.zeros((N, 1), complex)
+            e[k, 0] = 1.0
+            ref.append(orc.project_rows(prob.grid, e, x, one, d, n, ell, k, k + 1)[0, 0])
+        assert rel(y[rows], np.array(ref)) <= 1e-13
+    y0 = pb.toeplitz_apply(grid, xd, d, n, 0).cpu().numpy()
+    yh = pb.toeplitz_apply(grid, xd, d, n, 0, conj=True).cpu().numpy()
+    monkeypatch.setenv("PRONY_APPLY", "dmma")
+    assert rel(y0, pb.toeplitz_apply(grid, xd, d, n, 0).cpu().numpy()) <= 1e-13
+    assert rel(yh, pb.toeplitz_apply(grid, xd, d, n, 0, conj=True).cpu().numpy()) <= 1e-13
