@@ -914,7 +914,7 @@ __global__ void k_copy_cols(int N, int w, int NP, const double2* __restrict__ Y0
 constexpr int kMvThreads = 128;
 constexpr int kMvPerThread = 4;
 constexpr int kMvMaxBlocks = 4;  // a-blocks of kMvThreads * kMvPerThread outputs: n + 1 <= 2048
-constexpr int kMvMaxSlices = 16;
+constexpr int kMvMaxSlices = 64;
 
 __global__ void __launch_bounds__(kMvThreads) k_toeplitz_mv(int d, int n, int Mp, int S, const double2* __restrict__ g,
                                                             int shift, const double2* __restrict__ x, int ldx,
@@ -968,22 +968,40 @@ __global__ void __launch_bounds__(kMvThreads) k_toeplitz_mv(int d, int n, int Mp
       const int a0 = q * nth * kMvPerThread + kMvPerThread * tid;
       if (a0 < A) {
         // output a0 + r at column b reads w[a0 + r - b + n]
-        double2 w0 = w[a0 + n], w1 = w[a0 + n + 1], w2 = w[a0 + n + 2], w3 = w[a0 + n + 3];
+        // register window (v0..v3) = w[a0 + n - b + 0..3]; unrolled by 4 with the window rotated through
+        // the argument order instead of moved
+        double2 v0 = w[a0 + n], v1 = w[a0 + n + 1], v2 = w[a0 + n + 2], v3 = w[a0 + n + 3];
         double2 c0 = acc[q][0], c1 = acc[q][1], c2 = acc[q][2], c3 = acc[q][3];
-        for (int b = 0; b < A; ++b) {
-          const double2 xb = xs[b];
-          c0.x = fma(w0.x, xb.x, fma(-w0.y, xb.y, c0.x));
-          c0.y = fma(w0.x, xb.y, fma(w0.y, xb.x, c0.y));
-          c1.x = fma(w1.x, xb.x, fma(-w1.y, xb.y, c1.x));
-          c1.y = fma(w1.x, xb.y, fma(w1.y, xb.x, c1.y));
-          c2.x = fma(w2.x, xb.x, fma(-w2.y, xb.y, c2.x));
-          c2.y = fma(w2.x, xb.y, fma(w2.y, xb.x, c2.y));
-          c3.x = fma(w3.x, xb.x, fma(-w3.y, xb.y, c3.x));
-          c3.y = fma(w3.x, xb.y, fma(w3.y, xb.x, c3.y));
-          w3 = w2;
-          w2 = w1;
-          w1 = w0;
-          w0 = w[a0 + n - b - 1];
+        auto step = [&](const double2& p0, const double2& p1, const double2& p2, const double2& p3, double2 xb) {
+          c0.x = fma(p0.x, xb.x, fma(-p0.y, xb.y, c0.x));
+          c0.y = fma(p0.x, xb.y, fma(p0.y, xb.x, c0.y));
+          c1.x = fma(p1.x, xb.x, fma(-p1.y, xb.y, c1.x));
+          c1.y = fma(p1.x, xb.y, fma(p1.y, xb.x, c1.y));
+          c2.x = fma(p2.x, xb.x, fma(-p2.y, xb.y, c2.x));
+          c2.y = fma(p2.x, xb.y, fma(p2.y, xb.x, c2.y));
+          c3.x = fma(p3.x, xb.x, fma(-p3.y, xb.y, c3.x));
+          c3.y = fma(p3.x, xb.y, fma(p3.y, xb.x, c3.y));
+        };
+        int b = 0;
+        for (; b + 4 <= A; b += 4) {
+          const double2 x0 = xs[b], x1 = xs[b + 1], x2 = xs[b + 2], x3 = xs[b + 3];
+          const double2 u0 = w[a0 + n - b - 1], u1 = w[a0 + n - b - 2], u2 = w[a0 + n - b - 3],
+                        u3 = w[a0 + n - b - 4];
+          step(v0, v1, v2, v3, x0);
+          step(u0, v0, v1, v2, x1);
+          step(u1, u0, v0, v1, x2);
+          step(u2, u1, u0, v0, x3);
+          v3 = u0;
+          v2 = u1;
+          v1 = u2;
+          v0 = u3;
+        }
+        for (; b < A; ++b) {
+          step(v0, v1, v2, v3, xs[b]);
+          v3 = v2;
+          v2 = v1;
+          v1 = v0;
+          v0 = w[a0 + n - b - 1];
         }
         acc[q][0] = c0;
         acc[q][1] = c1;
@@ -1069,7 +1087,10 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
       !(emv && emv[0] == 'd')) {
     // single vector: DFMA Toeplitz matvec (k_toeplitz_mv) instead of the 8-wide DMMA tile
     const int Mp = N / (n + 1);
-    const int S = std::max(1, std::min({kMvMaxSlices, Mp, (2 * sm_count * 4 + Mp - 1) / Mp}));
+    // slices of h': enough CTAs for several full waves (short CTAs, small tail); env PRONY_MV_SLICES
+    const char* esl = getenv("PRONY_MV_SLICES");
+    int S = std::max(1, std::min({kMvMaxSlices, Mp, (40 * sm_count + Mp - 1) / Mp}));
+    if (esl) S = std::max(1, std::min({kMvMaxSlices, Mp, atoi(esl)}));
     const size_t smem = (size_t)2 * ((2 * n + 1 + 4) + (n + 1)) * sizeof(double2);
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(k_toeplitz_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
