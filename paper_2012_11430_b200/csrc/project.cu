@@ -555,21 +555,29 @@ __global__ void k_finalize(int d, int m, int RP, const double2* __restrict__ Spa
 }
 
 // ---------------------------------------------------------------------------- host side
-// k_project: 12 consumer warps = WM x WN. WM = 4 puts all column parts of one 16-row m-tile on the
-// same SM sub-partition (warp w -> SMSP w % 4 = wm), so every SMSP gets exactly ceil(m/8) n-tiles of
-// DMMA work per k-step (balanced for any m); NT <= 5 keeps the 3M accumulators within 160 registers.
+// k_project: 12 consumer warps = WM x WN. For m <= 80 (<= 10 n-tiles) WN = 2, WM = 6: each warp carries
+// ceil(ntot/2) <= 5 n-tiles (A-fragment reuse) and a CTA covers 96 rows per gathered column (measured:
+// cfg5 m = 30 6.9 ms vs 8.6 ms with WN = 3, cfg2 m = 20 -12%). Above that WN = 3, WM = 4 puts all column
+// parts of one 16-row m-tile on the same SM sub-partition (warp w -> SMSP w % 4 = wm), so every SMSP
+// gets exactly ceil(m/8) n-tiles of DMMA work per k-step; NT <= 5 keeps the 3M accumulators within 160
+// registers.
 // k_reduce: 16 warps, WN column warps with <= 4 n-tiles (3M accumulators within 128 registers).
 ProjShape proj_shape(int m) {
   ProjShape s;
   const int ntot = (m + 7) / 8;
   if (kConsumerWarps == 8) {
     s.WN = 2;  // WM = 4: warp w -> SMSP w % 4 = wm, balanced; NT <= 8 (3M accumulators in 240 regs)
-  } else if (ntot <= 2) {
-    s.WN = 2;
+  } else if (ntot <= 10) {
+    s.WN = 2;  // WM = 6, BM = 96: more n-tiles per warp (A-fragment reuse) and more rows per gathered column
   } else if (ntot <= 15) {
     s.WN = 3;
   } else {
     s.WN = 4;
+  }
+  const char* ewn = getenv("PRONY_PROJ_WN");  // experiments: force the column-warp count (2, 3, 4)
+  if (ewn && kConsumerWarps == 12 && ewn[0] >= '2' && ewn[0] <= '4') {
+    const int wn = ewn[0] - '0';
+    if ((ntot + wn - 1) / wn <= (wn == 4 ? 4 : 5)) s.WN = wn;
   }
   s.NT = (ntot + s.WN - 1) / s.WN;
   s.WM = kConsumerWarps / s.WN;  // k_project consumer warps along rows
@@ -790,8 +798,8 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   case wn * 16 + nt:       \
     return launch_project_t<nt, wn>(pp, gg, ss, mode, inf);
 #if PRONY_CONSUMER_WARPS == 12
-      PRONY_CASE(1, 2) PRONY_CASE(1, 3) PRONY_CASE(2, 3) PRONY_CASE(3, 3) PRONY_CASE(4, 3) PRONY_CASE(5, 3)
-      PRONY_CASE(4, 4)
+      PRONY_CASE(1, 2) PRONY_CASE(2, 2) PRONY_CASE(3, 2) PRONY_CASE(4, 2) PRONY_CASE(5, 2) PRONY_CASE(1, 3)
+      PRONY_CASE(2, 3) PRONY_CASE(3, 3) PRONY_CASE(4, 3) PRONY_CASE(5, 3) PRONY_CASE(4, 4)
 #else
       PRONY_CASE(1, 2) PRONY_CASE(2, 2) PRONY_CASE(3, 2) PRONY_CASE(4, 2) PRONY_CASE(5, 2) PRONY_CASE(6, 2)
       PRONY_CASE(7, 2) PRONY_CASE(8, 2)
@@ -1147,8 +1155,8 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
     lrc = launch_project_t<nt, wn>(p, grd, st, mode, nullptr); \
     break;
 #if PRONY_CONSUMER_WARPS == 12
-      PRONY_CASE(1, 2) PRONY_CASE(1, 3) PRONY_CASE(2, 3) PRONY_CASE(3, 3) PRONY_CASE(4, 3) PRONY_CASE(5, 3)
-      PRONY_CASE(4, 4)
+      PRONY_CASE(1, 2) PRONY_CASE(2, 2) PRONY_CASE(3, 2) PRONY_CASE(4, 2) PRONY_CASE(5, 2) PRONY_CASE(1, 3)
+      PRONY_CASE(2, 3) PRONY_CASE(3, 3) PRONY_CASE(4, 3) PRONY_CASE(5, 3) PRONY_CASE(4, 4)
 #else
       PRONY_CASE(1, 2) PRONY_CASE(2, 2) PRONY_CASE(3, 2) PRONY_CASE(4, 2) PRONY_CASE(5, 2) PRONY_CASE(6, 2)
       PRONY_CASE(7, 2) PRONY_CASE(8, 2)
