@@ -13,7 +13,8 @@
  *                        G = A conj(A)^T, b = A conj(f) of argmin_c ||A^T c - f||_2,
  *                        and, over the full column range, c = conj(G^-1 b) and
  *                        t_j = (-arg z_j / 2 pi) mod 1 (reading R4).
- *   prony_pencil_host    both of the above from HOST buffers (copies in, results out).
+ *   prony_pencil_host    both of the above from HOST buffers (copies in, results out);
+ *                        prony_pencil_host_part: one rank's partial share (multi-GPU end to end).
  *   prony_build_pencil   reduced SVD of T (block power method Alg. 3) on the
  *                        device, then prony_project (Algorithm 1 lines 1-3).
  *   prony_diagonalize    C_mu, its eigenvectors W, z = diag(W^-1 S_l W), t (Algorithm 1 lines 4-6).
@@ -65,7 +66,7 @@
 extern "C" {
 #endif
 
-#define PRONY_ABI_VERSION 2  /* 2: PRONY_UNITS_SHARED, prony_lanczos_svd, PRONY_WS_LANCZOS */
+#define PRONY_ABI_VERSION 3  /* 2: PRONY_UNITS_SHARED, prony_lanczos_svd, PRONY_WS_LANCZOS; 3: prony_pencil_host_part */
 #define PRONY_MAX_D 8
 #define PRONY_MAX_M 128
 
@@ -240,12 +241,12 @@ int prony_toeplitz_apply(int d, int n, const prony_c128* grid, int ell, int conj
                          prony_c128* Y, int ldy, void* workspace, size_t workspace_bytes, prony_stream_t stream);
 
 /*
- * prony_pencil_host — one full pencil (prony_project over [0, dN) + prony_vandermonde_ls over
- * [0, N)) from HOST inputs to HOST outputs: copies grid, U, V, sigma, z host->device, runs the
- * device path, copies S, G, b, c, t device->host and synchronizes `stream`. Internally a second
- * stream (created and destroyed by the call, ordered after prior work on `stream`) carries the copy
- * of U — first needed by the final reduction — and the LS step, so both overlap the projection.
- * Host buffers should be page-locked for full PCIe bandwidth (not required).
+ * prony_pencil_host — one full pencil (prony_project over all SHARED units + prony_vandermonde_ls over
+ * [0, N), c and t included) from HOST inputs to HOST outputs, synchronizing `stream` at the end. Only
+ * the grid and the V rows of split-K chunk 0 are copied before the first DMMA: two streams created
+ * and destroyed by the call (ordered after prior work on `stream`) carry the rest of V with the
+ * remaining chunks of the projection, then U (first needed by the final reduction), and z with the LS
+ * step. Host buffers should be page-locked for full PCIe bandwidth (not required).
  *   host inputs : grid (L^d), U, V (N x m), sigma (m), z (m x d)
  *   host outputs: S (d x m x m), G (m x m), b (m), c (m), t (m x d); any output may be NULL
  *   workspace   : DEVICE scratch >= prony_workspace_size(PRONY_WS_PENCIL_HOST)
@@ -256,6 +257,21 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
                       const double* sigma, const prony_c128* z, prony_c128* S, prony_c128* G, prony_c128* b,
                       prony_c128* c, double* t, void* workspace, size_t workspace_bytes, int32_t* status_out,
                       prony_stream_t stream);
+
+/*
+ * prony_pencil_host_part — one rank's share of a pencil from HOST inputs (multi-GPU end to end, P:259-267
+ * offload per rank): copies the grid, V, sigma, z and only the rows of U its SHARED unit range pairs
+ * with, runs prony_project over units [unit_begin, unit_end) of [0, (n+2)^d) and the LS products over
+ * columns [col_begin, col_end) of [0, N) (no solve), with the same copy/compute overlap as
+ * prony_pencil_host, and leaves the partial S (d x m x m), G (m x m), b (m) in DEVICE memory for the
+ * caller's all-reduce (then prony_ls_solve). Asynchronous and stream-ordered: host buffers must stay
+ * valid (and be page-locked for overlap) until `stream` reaches the end of the call's work.
+ *   workspace >= prony_workspace_size(PRONY_WS_PENCIL_HOST);  dev_status: as prony_project
+ */
+int prony_pencil_host_part(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
+                           const double* sigma, const prony_c128* z, int64_t unit_begin, int64_t unit_end,
+                           int64_t col_begin, int64_t col_end, prony_c128* S, prony_c128* G, prony_c128* b,
+                           void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream);
 
 /*
  * prony_build_pencil — Algorithm 1 lines 1-3 on the device: the reduced SVD T = U Sigma V*

@@ -12,7 +12,7 @@ from .binding import (  # noqa: F401
     WS_PENCIL_HOST, WS_PROJECT, PronyError, alloc_workspace, build_pencil, device_info, lib, ls_solve,
     pencil_host, project, status_string, toeplitz_apply, vandermonde_ls, workspace_size,
     WS_APPLY, WS_DIAG, WS_PROJECT_MU, project_mu, diagonalize, PRONY_ERR_RANK, PRONY_ERR_NOT_CONVERGED, WS_BUILD,
-    WS_LANCZOS, lanczos_svd,
+    WS_LANCZOS, lanczos_svd, pencil_host_part, UNITS_SHARED,
 )
 from . import sharding  # noqa: F401
 

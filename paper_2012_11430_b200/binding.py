@@ -31,7 +31,7 @@ MAX_D, MAX_M = 8, 128
 EXPORTS = ("prony_abi_version", "prony_status_string", "prony_device_info", "prony_workspace_size",
            "prony_project", "prony_project_ex", "prony_vandermonde_ls", "prony_vandermonde_ls_ex", "prony_ls_solve",
            "prony_toeplitz_apply", "prony_pencil_host", "prony_build_pencil", "prony_diagonalize",
-           "prony_project_mu", "prony_lanczos_svd")
+           "prony_project_mu", "prony_lanczos_svd", "prony_pencil_host_part")
 
 
 class ExecInfo(ctypes.Structure):
@@ -82,6 +82,8 @@ def lib() -> ctypes.CDLL:
                                          vp, vp, sz, vp, vp]
         L.prony_diagonalize.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, sz, vp, vp]
         L.prony_project_mu.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp]
+        L.prony_pencil_host_part.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, i64, i64, i64, i64, vp, vp, vp, vp, sz,
+                                             vp, vp]
         L.prony_lanczos_svd.argtypes = [i32, i32, vp, i32, ctypes.c_double, ctypes.c_uint64, i32, vp, vp, vp, vp, vp,
                                         vp, sz, vp]
         for f in ("prony_device_info", "prony_workspace_size", "prony_project", "prony_vandermonde_ls", "prony_ls_solve",
@@ -287,6 +289,27 @@ def pencil_host(grid, U, V, sigma, z, d: int, n: int, m: int, workspace=None, ou
     _check(rc, "prony_pencil_host")
     outputs["status"] = st.value
     return outputs
+
+
+def pencil_host_part(grid, U, V, sigma, z, d: int, n: int, m: int, unit_begin: int, unit_end: int, col_begin: int,
+                     col_end: int, S, G, b, workspace=None, dev_status=None, stream=None):
+    """One rank's partial pencil from HOST inputs (pinned CPU torch tensors for overlap): SHARED units
+    [unit_begin, unit_end), LS columns [col_begin, col_end); partial S, G, b land in the given DEVICE
+    tensors. Asynchronous on `stream`."""
+    def host_ptr(a):
+        if not (isinstance(a, torch.Tensor) and not a.is_cuda and a.is_contiguous()):
+            raise TypeError("host inputs must be contiguous CPU tensors")
+        return ctypes.c_void_p(a.data_ptr())
+
+    for name, x in (("S", S), ("G", G), ("b", b)):
+        _dev_tensor(x, torch.complex128, name)
+    if workspace is None:
+        workspace = alloc_workspace(WS_PENCIL_HOST, d, n, m, S.device)
+    rc = lib().prony_pencil_host_part(d, n, m, host_ptr(grid), host_ptr(U), host_ptr(V), host_ptr(sigma), host_ptr(z),
+                                      int(unit_begin), int(unit_end), int(col_begin), int(col_end), _ptr(S), _ptr(G),
+                                      _ptr(b), _ptr(workspace), workspace.numel(), _ptr(dev_status), _stream(stream))
+    _check(rc, "prony_pencil_host_part")
+    return S, G, b
 
 
 def build_pencil(grid, d: int, n: int, m: int, seed: int = 0, tol: float | None = None, max_iter: int = 4,

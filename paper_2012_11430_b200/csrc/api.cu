@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <climits>
 #include <cstring>
 
 #include "../../include/prony.h"
@@ -297,21 +298,59 @@ int prony_toeplitz_apply(int d, int n, const prony_c128* grid, int ell, int conj
                                ldy, workspace, sms, (cudaStream_t)stream);
 }
 
-int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
-                      const double* sigma, const prony_c128* z, prony_c128* S, prony_c128* G, prony_c128* b,
-                      prony_c128* c, double* t, void* workspace, size_t workspace_bytes, int32_t* status_out,
-                      prony_stream_t stream) {
-  int64_t N = 0;
-  int rc = validate_dnm(d, n, m, &N);
-  if (rc) return rc;
-  if (!grid || !U || !V || !sigma || !z || !workspace) return PRONY_ERR_INVALID;
-  if ((uintptr_t)workspace & 255u) return PRONY_ERR_INVALID;
-  const int sms = sm_count_current();
-  if (sms <= 0) return PRONY_ERR_CUDA;
-  const HostLayout h = host_layout(d, n, m, N, sms);
-  if (workspace_bytes < h.total) return PRONY_ERR_WORKSPACE;
-  cudaStream_t st = (cudaStream_t)stream;
-  char* w = (char*)workspace;
+}  // extern "C"
+
+namespace {
+
+// Rows of U that the SHARED units [e0, e1) pair with (over all l): k = k' - e_l for the k' of the slab
+// with k in I_n. For fixed l that row index is increasing in k', so the range is bounded by the first
+// and the last valid unit of the slab for each l.
+void shared_u_rows(int d, int n, int64_t e0, int64_t e1, int64_t* lo, int64_t* hi) {
+  const int Le = n + 2;
+  auto krow = [&](int64_t e, int l) -> int64_t {  // -1 if k' - e_l is outside I_n
+    int c[PRONY_MAX_D];
+    for (int i = d - 1; i >= 0; --i) {
+      c[i] = (int)(e % Le);
+      e /= Le;
+    }
+    c[l] -= 1;
+    int64_t k = 0;
+    for (int i = 0; i < d; ++i) {
+      if (c[i] < 0 || c[i] > n) return -1;
+      k = k * (n + 1) + c[i];
+    }
+    return k;
+  };
+  *lo = INT64_MAX;
+  *hi = -1;
+  for (int l = 0; l < d; ++l) {
+    for (int64_t e = e0; e < e1; ++e) {
+      const int64_t k = krow(e, l);
+      if (k >= 0) {
+        *lo = std::min(*lo, k);
+        break;
+      }
+    }
+    for (int64_t e = e1 - 1; e >= e0; --e) {
+      const int64_t k = krow(e, l);
+      if (k >= 0) {
+        *hi = std::max(*hi, k + 1);
+        break;
+      }
+    }
+  }
+  if (*hi < 0) *lo = *hi = 0;
+}
+
+// Host-input pencil on the device (prony_pencil_host / prony_pencil_host_part). Streams created for
+// this call only: `st` carries grid, the V rows of split-K chunk 0 and sigma -> k_prep -> chunk 0 of
+// the projection; `s2` carries the rest of V (after chunk 0's rows: the link is not shared) -> its Vsum
+// rows -> chunks 1..KC-1, then the U rows (needed only by k_reduce); `s3` carries z -> the LS step. So
+// only chunk 0's V rows are copied before the first DMMA. On return `st` is ordered after everything.
+int host_pencil(int d, int n, int m, int64_t N, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
+                const double* sigma, const prony_c128* z, int64_t e0, int64_t e1, int64_t c0, int64_t c1, bool solve,
+                double2* S_dev, double2* G_dev, double2* b_dev, double2* c_dev, double* t_dev, int32_t* dst,
+                char* w, const HostLayout& h, int sms, cudaStream_t st) {
   int64_t box = 1;
   for (int i = 0; i < d; ++i) box *= (2 * (int64_t)n + 2);
   ProjGeom g{};
@@ -319,15 +358,13 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
   g.n = n;
   g.m = m;
   g.N = (int)N;
-  unit_rows(d, n, N, 0, ext_rows(d, n), PRONY_UNITS_SHARED, &g);
+  unit_rows(d, n, N, e0, e1, PRONY_UNITS_SHARED, &g);
   ProjPlan pl{};
   project_plan(g, sms, &pl);
-  // Streams created for this call only: `st` carries grid, the V rows of split-K chunk 0 and sigma ->
-  // k_prep -> chunk 0 of the projection; `s2` carries the rest of V (after chunk 0's rows: the link is
-  // not shared) -> its Vsum rows -> chunks 1..KC-1, then U (needed only by k_reduce); `s3` carries z ->
-  // the LS step. So only chunk 0's V rows are copied before the first DMMA.
   const bool split = pl.KC > 1;
   const int64_t v0 = split ? std::min<int64_t>(pl.chunk_w, N) : N;
+  int64_t ulo = 0, uhi = N;
+  if (e0 != 0 || e1 != ext_rows(d, n)) shared_u_rows(d, n, e0, e1, &ulo, &uhi);
   cudaStream_t s2 = nullptr, s3 = nullptr;
   cudaEvent_t ev[7] = {};  // in, grid, v0, u, done, split a, split b
   auto cleanup = [&]() {
@@ -347,7 +384,7 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
   auto ok = [](cudaError_t e) { return e == cudaSuccess; };
   const size_t vrow = (size_t)m * sizeof(double2);
   good = ok(cudaEventRecord(ev_in, st)) && ok(cudaStreamWaitEvent(s2, ev_in, 0)) &&
-         ok(cudaStreamWaitEvent(s3, ev_in, 0)) && ok(cudaMemsetAsync(w + h.status, 0, sizeof(int32_t), st)) &&
+         ok(cudaStreamWaitEvent(s3, ev_in, 0)) &&
          ok(cudaMemcpyAsync(w + h.grid, grid, box * sizeof(double2), cudaMemcpyHostToDevice, st)) &&
          ok(cudaEventRecord(ev_grid, st)) &&
          ok(cudaMemcpyAsync(w + h.V, V, v0 * vrow, cudaMemcpyHostToDevice, st)) &&
@@ -355,38 +392,84 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
          ok(cudaEventRecord(ev_v0, st)) && ok(cudaStreamWaitEvent(s2, ev_v0, 0)) &&
          (v0 == N || ok(cudaMemcpyAsync(w + h.V + v0 * vrow, (const char*)V + v0 * vrow, (N - v0) * vrow,
                                         cudaMemcpyHostToDevice, s2))) &&
-         ok(cudaMemcpyAsync(w + h.U, U, N * vrow, cudaMemcpyHostToDevice, s2)) && ok(cudaEventRecord(ev_u, s2)) &&
-         ok(cudaStreamWaitEvent(s3, ev_grid, 0)) &&
+         (uhi <= ulo || ok(cudaMemcpyAsync(w + h.U + ulo * vrow, (const char*)U + ulo * vrow, (uhi - ulo) * vrow,
+                                           cudaMemcpyHostToDevice, s2))) &&
+         ok(cudaEventRecord(ev_u, s2)) && ok(cudaStreamWaitEvent(s3, ev_grid, 0)) &&
          ok(cudaMemcpyAsync(w + h.z, z, (size_t)m * d * sizeof(double2), cudaMemcpyHostToDevice, s3));
   if (!good) {
     cleanup();
     return PRONY_ERR_CUDA;
   }
-  int32_t* dst = (int32_t*)(w + h.status);
   ProjSplit sp{s2, ev[5], ev[6]};
-  rc = project_launch(g, pl, (const double2*)(w + h.grid), (const double2*)(w + h.U), (const double2*)(w + h.V),
-                      (const double*)(w + h.sigma), (double2*)(w + h.S), w + h.inner, sms, st, nullptr, ev_u, 1,
-                      dst, split ? &sp : nullptr);
+  int rc = project_launch(g, pl, (const double2*)(w + h.grid), (const double2*)(w + h.U), (const double2*)(w + h.V),
+                          (const double*)(w + h.sigma), S_dev, w + h.inner, sms, st, nullptr, ev_u, 1, dst,
+                          split ? &sp : nullptr);
   if (rc == PRONY_OK)
-    rc = ls_launch(d, n, m, (int)N, (const double2*)(w + h.z), (const double2*)(w + h.grid), 0, N, nullptr,
-                   (double2*)(w + h.G), (double2*)(w + h.b), (double2*)(w + h.c), (double*)(w + h.t),
-                   w + h.inner_ls, dst, sms, s3, nullptr);
+    rc = ls_launch(d, n, m, (int)N, (const double2*)(w + h.z), (const double2*)(w + h.grid), c0, c1, nullptr, G_dev,
+                   b_dev, solve ? c_dev : nullptr, solve ? t_dev : nullptr, w + h.inner_ls, dst, sms, s3, nullptr);
+  if (rc == PRONY_OK && !(ok(cudaEventRecord(ev_done, s3)) && ok(cudaStreamWaitEvent(st, ev_done, 0))))
+    rc = PRONY_ERR_CUDA;
   if (rc != PRONY_OK) {
     cudaStreamSynchronize(s2);
     cudaStreamSynchronize(s3);
-    cleanup();
-    return rc;
   }
-  auto d2h = [&](void* dstp, size_t off, size_t bytes, cudaStream_t s) {
-    return dstp == nullptr || cudaMemcpyAsync(dstp, w + off, bytes, cudaMemcpyDeviceToHost, s) == cudaSuccess;
-  };
-  good = d2h(G, h.G, (size_t)m * m * sizeof(double2), s3) && d2h(b, h.b, m * sizeof(double2), s3) &&
-         d2h(c, h.c, m * sizeof(double2), s3) && d2h(t, h.t, (size_t)m * d * sizeof(double), s3) &&
-         ok(cudaEventRecord(ev_done, s3)) && d2h(S, h.S, (size_t)d * m * m * sizeof(double2), st) &&
-         ok(cudaStreamWaitEvent(st, ev_done, 0)) && d2h(status_out, h.status, sizeof(int32_t), st) &&
-         ok(cudaStreamSynchronize(st));
   cleanup();
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
+                      const double* sigma, const prony_c128* z, prony_c128* S, prony_c128* G, prony_c128* b,
+                      prony_c128* c, double* t, void* workspace, size_t workspace_bytes, int32_t* status_out,
+                      prony_stream_t stream) {
+  int64_t N = 0;
+  int rc = validate_dnm(d, n, m, &N);
+  if (rc) return rc;
+  if (!grid || !U || !V || !sigma || !z || !workspace) return PRONY_ERR_INVALID;
+  if ((uintptr_t)workspace & 255u) return PRONY_ERR_INVALID;
+  const int sms = sm_count_current();
+  if (sms <= 0) return PRONY_ERR_CUDA;
+  const HostLayout h = host_layout(d, n, m, N, sms);
+  if (workspace_bytes < h.total) return PRONY_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)workspace;
+  int32_t* dst = (int32_t*)(w + h.status);
+  if (cudaMemsetAsync(dst, 0, sizeof(int32_t), st) != cudaSuccess) return PRONY_ERR_CUDA;
+  rc = host_pencil(d, n, m, N, grid, U, V, sigma, z, 0, ext_rows(d, n), 0, N, true, (double2*)(w + h.S),
+                   (double2*)(w + h.G), (double2*)(w + h.b), (double2*)(w + h.c), (double*)(w + h.t), dst, w, h, sms,
+                   st);
+  if (rc != PRONY_OK) return rc;
+  auto d2h = [&](void* dstp, size_t off, size_t bytes) {
+    return dstp == nullptr || cudaMemcpyAsync(dstp, w + off, bytes, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+  };
+  const bool good = d2h(S, h.S, (size_t)d * m * m * sizeof(double2)) && d2h(G, h.G, (size_t)m * m * sizeof(double2)) &&
+                    d2h(b, h.b, m * sizeof(double2)) && d2h(c, h.c, m * sizeof(double2)) &&
+                    d2h(t, h.t, (size_t)m * d * sizeof(double)) && d2h(status_out, h.status, sizeof(int32_t)) &&
+                    cudaStreamSynchronize(st) == cudaSuccess;
   return good ? PRONY_OK : PRONY_ERR_CUDA;
+}
+
+int prony_pencil_host_part(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
+                           const double* sigma, const prony_c128* z, int64_t unit_begin, int64_t unit_end,
+                           int64_t col_begin, int64_t col_end, prony_c128* S, prony_c128* G, prony_c128* b,
+                           void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream) {
+  int64_t N = 0;
+  int rc = validate_dnm(d, n, m, &N);
+  if (rc) return rc;
+  if (!grid || !U || !V || !sigma || !z || !S || !G || !b || !workspace) return PRONY_ERR_INVALID;
+  if (!aligned16(S) || !aligned16(G) || !aligned16(b) || ((uintptr_t)workspace & 255u)) return PRONY_ERR_INVALID;
+  if (unit_begin < 0 || unit_end < unit_begin || unit_end > ext_rows(d, n)) return PRONY_ERR_RANGE;
+  if (col_begin < 0 || col_end < col_begin || col_end > N) return PRONY_ERR_RANGE;
+  const int sms = sm_count_current();
+  if (sms <= 0) return PRONY_ERR_CUDA;
+  const HostLayout h = host_layout(d, n, m, N, sms);
+  if (workspace_bytes < h.total) return PRONY_ERR_WORKSPACE;
+  return host_pencil(d, n, m, N, grid, U, V, sigma, z, unit_begin, unit_end, col_begin, col_end, false, (double2*)S,
+                     (double2*)G, (double2*)b, nullptr, nullptr, dev_status, (char*)workspace, h, sms,
+                     (cudaStream_t)stream);
 }
 
 int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t seed, double tol, int max_iter,

@@ -34,6 +34,37 @@ def unit_range(d: int, n: int, world: int, rank: int, order: int = UNITS_SHARED)
     return split_range(unit_count(d, n, order), world, rank)
 
 
+def shared_u_rows(d: int, n: int, e0: int, e1: int) -> tuple[int, int]:
+    """Rows [lo, hi) of U that the SHARED units [e0, e1) pair with (k = k' - e_l in I_n, any l): the
+    range prony_pencil_host_part copies (mirrors its host-side computation)."""
+    def krow(e, ell):
+        c = []
+        for _ in range(d):
+            c.append(e % (n + 2))
+            e //= n + 2
+        c = c[::-1]
+        c[ell] -= 1
+        if min(c) < 0 or max(c) > n:
+            return -1
+        k = 0
+        for ci in c:
+            k = k * (n + 1) + ci
+        return k
+    lo, hi = None, -1
+    for ell in range(d):
+        for e in range(e0, e1):
+            k = krow(e, ell)
+            if k >= 0:
+                lo = k if lo is None else min(lo, k)
+                break
+        for e in range(e1 - 1, e0 - 1, -1):
+            k = krow(e, ell)
+            if k >= 0:
+                hi = max(hi, k + 1)
+                break
+    return (0, 0) if hi < 0 else (lo, hi)
+
+
 def column_range(d: int, n: int, world: int, rank: int) -> tuple[int, int]:
     N = (n + 1) ** d
     return split_range(N, world, rank)
@@ -109,4 +140,21 @@ class DistributedPencil:
             return self.S, res["c"], res["t"]
         Sr, Gr, br = allreduce_pencil(self.S, self.G, self.b)
         c, t = pb.ls_solve(Gr.contiguous(), br.contiguous(), z, d, m, dev_status=self.status, stream=main)
+        return Sr, c, t
+
+    def from_host(self, grid_h, U_h, V_h, sigma_h, z_h, z_dev, stream=None):
+        """End to end from HOST inputs (page-locked CPU tensors): this rank's partial pencil through
+        prony_pencil_host_part (grid, V and only the U rows its unit slab pairs with are copied; the copy
+        of V overlaps the projection), then the all-reduce and the local m x m solve. SHARED order only.
+        z_dev: the nodes on the device (the solve's t); the LS products read z from z_h."""
+        pb, d, n, m = self.pb, self.d, self.n, self.m
+        if self.order != UNITS_SHARED:
+            raise ValueError("from_host needs the SHARED unit order")
+        main = stream if stream is not None else torch.cuda.current_stream()
+        if not hasattr(self, "ws_h"):
+            self.ws_h = pb.alloc_workspace(pb.WS_PENCIL_HOST, d, n, m, self.S.device)
+        pb.pencil_host_part(grid_h, U_h, V_h, sigma_h, z_h, d, n, m, self.u0, self.u1, self.c0, self.c1, self.S,
+                            self.G, self.b, workspace=self.ws_h, dev_status=self.status, stream=main)
+        Sr, Gr, br = allreduce_pencil(self.S, self.G, self.b)
+        c, t = pb.ls_solve(Gr.contiguous(), br.contiguous(), z_dev, d, m, dev_status=self.status, stream=main)
         return Sr, c, t

@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _rank(rank, world, port, name, out):
+def _rank(rank, world, port, name, out, from_host=False):
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
 
@@ -36,7 +36,12 @@ def _rank(rank, world, port, name, out):
     c = prob.cfg
     tg = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
     pencil = sharding.DistributedPencil(c.d, c.n, c.m, torch.device("cuda", 0), world, rank)
-    S, cc, t = pencil(tg(prob.grid), tg(prob.U), tg(prob.V), tg(prob.sigma), tg(prob.z))
+    if from_host:  # end to end from pinned host inputs: prony_pencil_host_part per rank
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        S, cc, t = pencil.from_host(pin(prob.grid), pin(prob.U), pin(prob.V), pin(prob.sigma), pin(prob.z),
+                                    tg(prob.z))
+    else:
+        S, cc, t = pencil(tg(prob.grid), tg(prob.U), tg(prob.V), tg(prob.sigma), tg(prob.z))
     torch.cuda.synchronize()
     if rank == 0:
         np.savez(out, S=S.cpu().numpy(), c=cc.cpu().numpy(), t=t.cpu().numpy(), st=pencil.status.cpu().numpy())
@@ -44,13 +49,13 @@ def _rank(rank, world, port, name, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
-def test_distributed_pencil_two_ranks(tmp_path, name):
+@pytest.mark.parametrize("name,from_host", [("cfg2", False), ("cfg3", False), ("cfg2", True), ("cfg3", True)])
+def test_distributed_pencil_two_ranks(tmp_path, name, from_host):
     sys.path.insert(0, ROOT)
     import paper_2012_11430_b200 as pb
     import workload as W
     out = str(tmp_path / "r.npz")
-    mp.spawn(_rank, args=(2, _free_port(), name, out), nprocs=2, join=True)
+    mp.spawn(_rank, args=(2, _free_port(), name, out, from_host), nprocs=2, join=True)
     r = np.load(out)
     prob = W.make_problem(name)
     c = prob.cfg

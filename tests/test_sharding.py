@@ -99,3 +99,33 @@ def test_pack_unpack_roundtrip():
     b = torch.randn(m, dtype=torch.complex128)
     S2, G2, b2 = sharding.unpack(sharding.pack(S, G, b), d, m)
     assert torch.equal(S, S2) and torch.equal(G, G2) and torch.equal(b, b2)
+
+
+@pytest.mark.parametrize("d,n", [(1, 5), (2, 4), (3, 3), (2, 9)])
+def test_shared_u_rows_is_the_exact_range(d, n):
+    """The U rows a SHARED unit slab pairs with (what prony_pencil_host_part copies): brute force over the
+    slab's units and every l."""
+    import random
+    rng = random.Random(d * 10 + n)
+    E = (n + 2) ** d
+    for _ in range(60):
+        a = rng.randrange(0, E)
+        b = rng.randrange(a, E + 1)
+        rows = set()
+        for e in range(a, b):
+            c, r = [], e
+            for _ in range(d):
+                c.append(r % (n + 2))
+                r //= n + 2
+            c = c[::-1]
+            for ell in range(d):
+                cc = list(c)
+                cc[ell] -= 1
+                if min(cc) < 0 or max(cc) > n:
+                    continue
+                k = 0
+                for ci in cc:
+                    k = k * (n + 1) + ci
+                rows.add(k)
+        want = (min(rows), max(rows) + 1) if rows else (0, 0)
+        assert sharding.shared_u_rows(d, n, a, b) == want
