@@ -911,54 +911,65 @@ __global__ void k_copy_cols(int N, int w, int NP, const double2* __restrict__ Y0
 // ---------------------------------------------------------------------------- Toeplitz matvec (r = 1)
 // The Lanczos recurrence (NEXT-3, Alg. 2) applies T and T^H to ONE vector per step. On the DMMA path
 // that single column is padded to an 8-wide n-tile and the A gather (24 B per T element) bounds it
-// (8.1 ms at cfg4). This DFMA kernel uses the Toeplitz structure along the last coordinate instead:
-// with k = (k', a), h = (h', b) (a, b the last coordinate, k', h' the first d-1 coordinates),
-//   T[k, h] = g[L (Pp(k') - Pp(h')) + shift + a - b],   Pp = linear box offset of the prefix,
-// so for one (k', h') pair the (n+1) x (n+1) block is a 1-D Toeplitz block read from ONE window of
-// 2n+1 consecutive samples. CTA (k', slice s of h') stages window + x[h', :] in shared memory
-// (double-buffered cp.async) and each thread accumulates 4 consecutive outputs a with a sliding
-// register window (1 window load + 1 broadcast load per 4 complex MACs). Partial sums per slice are
-// reduced in fixed slice order (deterministic).
-constexpr int kMvThreads = 128;
+// (8.1 ms at cfg4). This DFMA kernel uses the multilevel Toeplitz structure instead. Split the
+// multi-index into an outer prefix (first d - q coordinates) and an inner block (last q coordinates,
+// A = (n+1)^q points): k = (k'', a), h = (h'', b) and
+//   T[k, h] = g[L^q (P''(k'') - P''(h'')) + shift + Pin(a) - Pin(b)],   Pin(a) = sum_i a_i L^(q-1-i),
+// so for one prefix pair the A x A block reads ONE window of 2 Pmax + 1 consecutive samples
+// (Pmax = Pin(n,..,n)). CTA (k'', slice s of h'') stages window + x[h'', :] in shared memory
+// (double-buffered cp.async); a thread owns 4 consecutive outputs inside one run of the last inner
+// coordinate and walks each run of b with a sliding register window (1 window load + 1 broadcast load
+// per 4 complex MACs). Partial sums per slice are reduced in fixed slice order (deterministic).
+constexpr int kMvThreads = 256;
 constexpr int kMvPerThread = 4;
-constexpr int kMvMaxBlocks = 4;  // a-blocks of kMvThreads * kMvPerThread outputs: n + 1 <= 2048
+constexpr int kMvMaxSlots = 4;  // output slots (4 outputs each) per thread
 constexpr int kMvMaxSlices = 64;
 
-__global__ void __launch_bounds__(kMvThreads) k_toeplitz_mv(int d, int n, int Mp, int S, const double2* __restrict__ g,
-                                                            int shift, const double2* __restrict__ x, int ldx,
+__global__ void __launch_bounds__(kMvThreads) k_toeplitz_mv(int d, int n, int q, int Mp, int S,
+                                                            const double2* __restrict__ g, int shift,
+                                                            const double2* __restrict__ x, int ldx,
                                                             double2* __restrict__ ypart) {
   extern __shared__ __align__(16) double2 mvs[];
-  const int A = n + 1, Wl = 2 * n + 1, L = 2 * n + 2;
-  const int WS = Wl + 4;  // window slot: 1 pad in front, 3 behind (reads of the 4-wide register window)
+  const int n1 = n + 1, L = 2 * n + 2;
+  int A = 1, Lq = 1, Pmax = 0;
+  for (int i = 0; i < q; ++i) {
+    A *= n1;
+    Pmax = Pmax * L + n;
+    Lq *= L;
+  }
+  const int runs = A / n1;             // runs of the last coordinate inside the inner block
+  const int tpr = (n1 + kMvPerThread - 1) / kMvPerThread;  // threads (slots) per run
+  const int nslot = runs * tpr;
+  const int Wl = 2 * Pmax + 1, WS = Wl + 4;  // window slot: 1 pad in front, 3 behind
   const int slot = WS + A;
   const int kp = blockIdx.x, s = blockIdx.y, tid = threadIdx.x, nth = blockDim.x;
-  auto Pp = [&](int idx) {
+  auto Pdig = [&](int idx, int ndig) {  // linear box offset of an (ndig)-digit base-(n+1) index
     int P = 0, mul = 1;
-    for (int i = d - 2; i >= 0; --i) {
-      P += (idx % A) * mul;
-      idx /= A;
+    for (int i = 0; i < ndig; ++i) {
+      P += (idx % n1) * mul;
+      idx /= n1;
       mul *= L;
     }
     return P;
   };
-  const int pk = Pp(kp);
+  const int pk = Pdig(kp, d - q);
   const int hb = (int)((int64_t)Mp * s / S), he = (int)((int64_t)Mp * (s + 1) / S);
   for (int e = tid; e < 2 * slot; e += nth) mvs[e] = make_double2(0.0, 0.0);  // pads stay zero
   __syncthreads();
   auto issue = [&](int hp, int buf) {
     double2* w = mvs + buf * slot;
-    const int wbase = L * (pk - Pp(hp)) + shift - n;
+    const int wbase = Lq * (pk - Pdig(hp, d - q)) + shift - Pmax;
     const uint32_t sw = (uint32_t)__cvta_generic_to_shared(w + 1);
     for (int j = tid; j < Wl; j += nth) cp_async16(sw + 16u * j, g + wbase + j, 16);
     const uint32_t sx = (uint32_t)__cvta_generic_to_shared(w + WS);
-    for (int b = tid; b < A; b += nth) cp_async16(sx + 16u * b, x + (size_t)(hp * A + b) * ldx, 16);
+    for (int b = tid; b < A; b += nth) cp_async16(sx + 16u * b, x + ((size_t)hp * A + b) * ldx, 16);
     cp_async_commit();
   };
-  double2 acc[kMvMaxBlocks][kMvPerThread];
+  double2 acc[kMvMaxSlots][kMvPerThread];
 #pragma unroll
-  for (int q = 0; q < kMvMaxBlocks; ++q)
+  for (int u = 0; u < kMvMaxSlots; ++u)
 #pragma unroll
-    for (int r = 0; r < kMvPerThread; ++r) acc[q][r] = make_double2(0.0, 0.0);
+    for (int r = 0; r < kMvPerThread; ++r) acc[u][r] = make_double2(0.0, 0.0);
   if (hb < he) issue(hb, 0);
   for (int hp = hb; hp < he; ++hp) {
     const int buf = (hp - hb) & 1;
@@ -972,14 +983,12 @@ __global__ void __launch_bounds__(kMvThreads) k_toeplitz_mv(int d, int n, int Mp
     const double2* w = mvs + buf * slot + 1;  // w[j] = g[wbase + j], j in [-1, Wl + 2] readable
     const double2* xs = mvs + buf * slot + WS;
 #pragma unroll
-    for (int q = 0; q < kMvMaxBlocks; ++q) {
-      const int a0 = q * nth * kMvPerThread + kMvPerThread * tid;
-      if (a0 < A) {
-        // output a0 + r at column b reads w[a0 + r - b + n]
-        // register window (v0..v3) = w[a0 + n - b + 0..3]; unrolled by 4 with the window rotated through
-        // the argument order instead of moved
-        double2 v0 = w[a0 + n], v1 = w[a0 + n + 1], v2 = w[a0 + n + 2], v3 = w[a0 + n + 3];
-        double2 c0 = acc[q][0], c1 = acc[q][1], c2 = acc[q][2], c3 = acc[q][3];
+    for (int u = 0; u < kMvMaxSlots; ++u) {
+      const int sl = tid + u * nth;
+      if (sl < nslot) {
+        const int rho = sl / tpr, j0 = kMvPerThread * (sl % tpr);
+        const int prho = L * Pdig(rho, q - 1);
+        double2 c0 = acc[u][0], c1 = acc[u][1], c2 = acc[u][2], c3 = acc[u][3];
         auto step = [&](const double2& p0, const double2& p1, const double2& p2, const double2& p3, double2 xb) {
           c0.x = fma(p0.x, xb.x, fma(-p0.y, xb.y, c0.x));
           c0.y = fma(p0.x, xb.y, fma(p0.y, xb.x, c0.y));
@@ -990,43 +999,51 @@ __global__ void __launch_bounds__(kMvThreads) k_toeplitz_mv(int d, int n, int Mp
           c3.x = fma(p3.x, xb.x, fma(-p3.y, xb.y, c3.x));
           c3.y = fma(p3.x, xb.y, fma(p3.y, xb.x, c3.y));
         };
-        int b = 0;
-        for (; b + 4 <= A; b += 4) {
-          const double2 x0 = xs[b], x1 = xs[b + 1], x2 = xs[b + 2], x3 = xs[b + 3];
-          const double2 u0 = w[a0 + n - b - 1], u1 = w[a0 + n - b - 2], u2 = w[a0 + n - b - 3],
-                        u3 = w[a0 + n - b - 4];
-          step(v0, v1, v2, v3, x0);
-          step(u0, v0, v1, v2, x1);
-          step(u1, u0, v0, v1, x2);
-          step(u2, u1, u0, v0, x3);
-          v3 = u0;
-          v2 = u1;
-          v1 = u2;
-          v0 = u3;
+        for (int beta = 0; beta < runs; ++beta) {
+          // outputs (rho, j0 + r), inputs (beta, bl): window index c + r - bl
+          const int c = prho - L * Pdig(beta, q - 1) + j0 + Pmax;
+          const double2* xr = xs + beta * n1;
+          double2 v0 = w[c], v1 = w[c + 1], v2 = w[c + 2], v3 = w[c + 3];
+          int bl = 0;
+          for (; bl + 4 <= n1; bl += 4) {
+            const double2 x0 = xr[bl], x1 = xr[bl + 1], x2 = xr[bl + 2], x3 = xr[bl + 3];
+            const double2 u0 = w[c - bl - 1], u1 = w[c - bl - 2], u2 = w[c - bl - 3], u3 = w[c - bl - 4];
+            step(v0, v1, v2, v3, x0);
+            step(u0, v0, v1, v2, x1);
+            step(u1, u0, v0, v1, x2);
+            step(u2, u1, u0, v0, x3);
+            v3 = u0;
+            v2 = u1;
+            v1 = u2;
+            v0 = u3;
+          }
+          for (; bl < n1; ++bl) {
+            step(v0, v1, v2, v3, xr[bl]);
+            v3 = v2;
+            v2 = v1;
+            v1 = v0;
+            v0 = w[c - bl - 1];
+          }
         }
-        for (; b < A; ++b) {
-          step(v0, v1, v2, v3, xs[b]);
-          v3 = v2;
-          v2 = v1;
-          v1 = v0;
-          v0 = w[a0 + n - b - 1];
-        }
-        acc[q][0] = c0;
-        acc[q][1] = c1;
-        acc[q][2] = c2;
-        acc[q][3] = c3;
+        acc[u][0] = c0;
+        acc[u][1] = c1;
+        acc[u][2] = c2;
+        acc[u][3] = c3;
       }
     }
     __syncthreads();  // the slot is refilled by the next iteration's issue
   }
   double2* yp = ypart + (size_t)s * Mp * A + (size_t)kp * A;
 #pragma unroll
-  for (int q = 0; q < kMvMaxBlocks; ++q)
+  for (int u = 0; u < kMvMaxSlots; ++u) {
+    const int sl = tid + u * nth;
+    if (sl < nslot) {
+      const int rho = sl / tpr, j0 = kMvPerThread * (sl % tpr);
 #pragma unroll
-    for (int r = 0; r < kMvPerThread; ++r) {
-      const int a = q * nth * kMvPerThread + kMvPerThread * tid + r;
-      if (a < A) yp[a] = acc[q][r];
+      for (int r = 0; r < kMvPerThread; ++r)
+        if (j0 + r < n1) yp[rho * n1 + j0 + r] = acc[u][r];
     }
+  }
 }
 
 // y[k * ldy] = sum_{s < S} ypart[s][k]   (fixed order)
@@ -1091,22 +1108,36 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
   }
   const int shift = (int)(C0 + (ell >= 1 ? ipow(L, d - ell) : 0));
   const char* emv = getenv("PRONY_APPLY");
-  if (r == 1 && d >= 2 && n + 1 >= 64 && n + 1 <= kMvMaxBlocks * kMvThreads * kMvPerThread &&
-      !(emv && emv[0] == 'd')) {
-    // single vector: DFMA Toeplitz matvec (k_toeplitz_mv) instead of the 8-wide DMMA tile
-    const int Mp = N / (n + 1);
-    // slices of h': enough CTAs for several full waves (short CTAs, small tail); env PRONY_MV_SLICES
+  // single vector: DFMA Toeplitz matvec with q inner coordinates (q = 1 when a run has >= 64 points,
+  // else 2 when d >= 3 and runs are short enough for one CTA's output slots)
+  int q = 0;
+  if (r == 1 && d >= 2 && !(emv && emv[0] == 'd')) {
+    const int n1 = n + 1, tpr = (n1 + kMvPerThread - 1) / kMvPerThread;
+    if (n1 >= 64 && tpr <= kMvMaxSlots * kMvThreads) q = 1;
+    else if (d >= 3 && n1 * tpr <= kMvMaxSlots * kMvThreads && n1 * n1 >= 64) q = 2;
+  }
+  if (q) {
+    int A = 1, Pmax = 0;
+    for (int i = 0; i < q; ++i) {
+      A *= (n + 1);
+      Pmax = Pmax * L + n;
+    }
+    const int Mp = N / A;
+    const int nslot = (A / (n + 1)) * ((n + 1 + kMvPerThread - 1) / kMvPerThread);
+    const int nth = std::min(kMvThreads, std::max(32, (std::min(nslot, kMvThreads) + 31) / 32 * 32));
     const char* esl = getenv("PRONY_MV_SLICES");
     int S = std::max(1, std::min({kMvMaxSlices, Mp, (40 * sm_count + Mp - 1) / Mp}));
     if (esl) S = std::max(1, std::min({kMvMaxSlices, Mp, atoi(esl)}));
-    const size_t smem = (size_t)2 * ((2 * n + 1 + 4) + (n + 1)) * sizeof(double2);
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(k_toeplitz_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return PRONY_ERR_CUDA;
-    const int nth = std::min(kMvThreads, ((n + 1 + kMvPerThread - 1) / kMvPerThread + 31) / 32 * 32);
-    k_toeplitz_mv<<<dim3(Mp, S), nth, smem, st>>>(d, n, Mp, S, g, shift, X, ldx, Y);
-    k_mv_reduce<<<(N + 255) / 256, 256, 0, st>>>(N, S, Y, Yout, ldy);
-    return cudaGetLastError() == cudaSuccess ? PRONY_OK : PRONY_ERR_CUDA;
+    const size_t smem = (size_t)2 * ((2 * Pmax + 1 + 4) + A) * sizeof(double2);
+    if (smem > 227 * 1024) q = 0;
+    if (q) {
+      if (smem > 48 * 1024 &&
+          cudaFuncSetAttribute(k_toeplitz_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return PRONY_ERR_CUDA;
+      k_toeplitz_mv<<<dim3(Mp, S), nth, smem, st>>>(d, n, q, Mp, S, g, shift, X, ldx, Y);
+      k_mv_reduce<<<(N + 255) / 256, 256, 0, st>>>(N, S, Y, Yout, ldy);
+      return cudaGetLastError() == cudaSuccess ? PRONY_OK : PRONY_ERR_CUDA;
+    }
   }
   const int npass = (r + kApplyMaxW - 1) / kApplyMaxW;
   const int mode = cmul_mode();

@@ -544,11 +544,12 @@ def test_project_sigma_guard(pb, orc, bad):
     assert int(st.item()) == pb.PRONY_ERR_SINGULAR
 
 
-def test_toeplitz_matvec_dfma_dense(pb, orc):
-    """The single-vector apply (DFMA Toeplitz matvec, taken for r = 1, d >= 2, n + 1 >= 64; NEXT-3's
-    operator) against the oracle's dense T_l and T^H, with a strided input column and output column."""
-    d, n = 2, 63
-    prob = problem(d, n, 3, 881, 1e-6, random_uv=True)
+@pytest.mark.parametrize("d,n", [(2, 63), (3, 9), (4, 7)])
+def test_toeplitz_matvec_dfma_dense(pb, orc, d, n):
+    """The single-vector apply (DFMA Toeplitz matvec: q = 1 inner coordinate for n + 1 >= 64, q = 2 for
+    shorter runs at d >= 3; NEXT-3's operator) against the oracle's dense T_l and T^H, with a strided
+    input column and output column."""
+    prob = problem(d, n, 3, 881 + d + n, 1e-6, random_uv=True)
     N = prob.cfg.N
     rng = np.random.default_rng(9)
     Xw = rng.standard_normal((N, 5)) + 1j * rng.standard_normal((N, 5))
@@ -567,18 +568,19 @@ def test_toeplitz_matvec_dfma_dense(pb, orc):
     assert np.all(Y[:, 0] == 0) and np.all(Y[:, 2] == 0)
 
 
-def test_toeplitz_matvec_dfma_d3_sampled(pb, orc, monkeypatch):
-    """d = 3, n = 63 (N = 262144): sampled rows of T_l x (l = 1..3) against the oracle (one row of T_l at
-    a time via oracle.project_rows with a one-hot U); T x and T^H x against the DMMA apply path."""
-    d, n = 3, 63
+@pytest.mark.parametrize("d,n", [(3, 63), (3, 20), (4, 12)])
+def test_toeplitz_matvec_dfma_sampled(pb, orc, monkeypatch, d, n):
+    """Large shapes (d = 3, n = 63: N = 262144, q = 1; cfg3 / cfg5 sizes, q = 2): sampled rows of T_l x
+    against the oracle (one row of T_l at a time via oracle.project_rows with a one-hot U); T x and
+    T^H x against the DMMA apply path."""
     prob = problem(d, n, 2, 882, 0.0, random_uv=True)
     N = prob.cfg.N
     rng = np.random.default_rng(10)
     x = rng.standard_normal((N, 1)) + 1j * rng.standard_normal((N, 1))
     xd, grid = dev(x), dev(prob.grid)
-    rows = [0, 1, 63, 64, 4095, 4096, N // 2 + 17, N - 65, N - 1]
+    rows = sorted({0, 1, n, n + 1, (n + 1) ** 2 - 1, (n + 1) ** 2, N // 2 + 17, N - n - 2, N - 1})
     one = np.ones(1)
-    for ell in (1, 2, 3):
+    for ell in sorted({1, 2, d}):
         y = pb.toeplitz_apply(grid, xd, d, n, ell).cpu().numpy()[:, 0]
         ref = []
         for k in rows:
