@@ -17,6 +17,8 @@ Parity status per function (DESIGN.md §4 lists the pins):
   project / project_columns / vandermonde / ls_products / cholesky_solve / T_dense:
       pinned (tests/test_oracle_pins.py)
   svd_reduced, eig, diagonalize, t_from_z, lstsq_qr, algorithm1: pinned (same file)
+  project_units / _shared_runs (unit orders 0, 1, 2): pinned (unit-range linearity in
+      test_oracle_pins.py; order 2 covers every row of every T_l exactly once, test_sharding.py)
 """
 from __future__ import annotations
 
