@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
         if (plane == 0) mbar_arrive_expect_tx(full0 + 8u * s, bytes_row * (uint32_t)nrows);
         __syncwarp();
         const uint32_t st = sbase + (uint32_t)(s * T::STAGE) * 8u;
-        if (kr < nrows) {
+        if (plane < 2 * kBK && kr < nrows) {
           const int h = h0 + kr;
           if (!sum_plane) {
             bulk_g2s(st + (uint32_t)(T::B_C + 2 * kr * T::LDB) * 8u, V + (size_t)h * p.ldv, (uint32_t)m * 16u,

@@ -12,8 +12,15 @@ int64_t ext_rows(int d, int n);  // |E| = (n+2)^d
 constexpr int kPtabPad = 4;   // P table padded so the last k-step may read P(h) for h < N+4
 constexpr int kMaxNP = 128;   // padded width of Y rows handled by k_reduce
 constexpr int kYCap = 4;      // split-K bound: KC * (rows in range) <= kYCap * d * N
-constexpr int kBK = 16;       // columns of T_l per pipeline stage of k_project
-constexpr int kStages = 3;    // cp.async ring depth of k_project (<= 227 KB smem)
+#ifndef PRONY_BK
+#define PRONY_BK 16
+#endif
+#ifndef PRONY_STAGES
+#define PRONY_STAGES 3
+#endif
+constexpr int kBK = PRONY_BK;          // columns of T_l per pipeline stage of k_project (8 or 16)
+constexpr int kStages = PRONY_STAGES;  // cp.async ring depth of k_project (<= 227 KB smem)
+static_assert(kBK == 8 || kBK == 16, "stage width: 8 or 16 columns (the P(h) lanes and B-row lanes)");
 
 struct ProjShape {
   int NT, WN, WM, BM;  // k_project consumer layout

@@ -18,6 +18,8 @@ VARIANTS = {
     "g2": ["PRONY_GATHER_UNROLL=2"],
     "kk2g2": ["PRONY_KK_UNROLL=2", "PRONY_GATHER_UNROLL=2"],
     "r152p40": ["PRONY_CONSUMER_REGS=152", "PRONY_PRODUCER_REGS=40"],
+    "bk8s6": ["PRONY_BK=8", "PRONY_STAGES=6"],
+    "bk8s5": ["PRONY_BK=8", "PRONY_STAGES=5"],
 }
 
 if __name__ == "__main__":
