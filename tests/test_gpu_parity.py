@@ -593,3 +593,45 @@ def test_toeplitz_matvec_dfma_sampled(pb, orc, monkeypatch, d, n):
     monkeypatch.setenv("PRONY_APPLY", "dmma")
     assert rel(y0, pb.toeplitz_apply(grid, xd, d, n, 0).cpu().numpy()) <= 1e-13
     assert rel(yh, pb.toeplitz_apply(grid, xd, d, n, 0, conj=True).cpu().numpy()) <= 1e-13
+
+
+def test_cuda_graph_capture_and_replay(pb, orc):
+    """prony.h promises stream-ordered, allocation-free calls that a CUDA graph can capture: one pencil
+    (projection + LS products + solve) captured once and replayed on new inputs copied into the same
+    buffers gives the oracle's pencil for those inputs."""
+    probs = [problem(2, 20, 9, 1500 + i, 1e-6, random_uv=True) for i in range(2)]
+    c = probs[0].cfg
+    d, n, m = c.d, c.n, c.m
+    bufs = {k: dev(getattr(probs[0], k)) for k in ("grid", "U", "V", "sigma", "z")}
+    ws_p = pb.alloc_workspace(pb.WS_PROJECT, d, n, m)
+    ws_l = pb.alloc_workspace(pb.WS_LS, d, n, m)
+    S = torch.empty((d, m, m), dtype=torch.complex128, device="cuda")
+    out = {"G": torch.empty((m, m), dtype=torch.complex128, device="cuda"),
+           "b": torch.empty(m, dtype=torch.complex128, device="cuda"),
+           "c": torch.empty(m, dtype=torch.complex128, device="cuda"),
+           "t": torch.empty((m, d), dtype=torch.float64, device="cuda")}
+    st = torch.cuda.Stream()
+
+    def pencil():
+        pb.project(bufs["grid"], bufs["U"], bufs["V"], bufs["sigma"], d, n, m, out=S, workspace=ws_p,
+                   stream=torch.cuda.current_stream())
+        pb.vandermonde_ls(bufs["z"], bufs["grid"], d, n, m, out=out, workspace=ws_l,
+                          stream=torch.cuda.current_stream())
+
+    with torch.cuda.stream(st):
+        pencil()  # warm-up (sets kernel attributes outside the capture)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=st):
+        pencil()
+    for prob in probs[::-1]:
+        for k in bufs:
+            bufs[k].copy_(torch.from_numpy(np.ascontiguousarray(getattr(prob, k))))
+        graph.replay()
+        torch.cuda.synchronize()
+        S_or = orc.project(prob.grid, prob.U, prob.V, prob.sigma, d, n)
+        for l in range(d):
+            assert rel(S[l], S_or[l]) <= TOL
+        A_or = orc.vandermonde(prob.z, d, n)
+        G_or, b_or = orc.ls_products(A_or, prob.grid, d, n)
+        assert rel(out["G"], G_or) <= TOL and rel(out["b"], b_or) <= TOL
