@@ -635,3 +635,43 @@ def test_cuda_graph_capture_and_replay(pb, orc):
         A_or = orc.vandermonde(prob.z, d, n)
         G_or, b_or = orc.ls_products(A_or, prob.grid, d, n)
         assert rel(out["G"], G_or) <= TOL and rel(out["b"], b_or) <= TOL
+
+
+def test_project_random_shapes_and_ranges(pb, orc):
+    """Seeded random sweep: d in 1..4, n, m (ragged tiles, m up to 40), random sub-ranges in all three
+    unit orders, noise or not — each partial pencil against the oracle's rows of T_l."""
+    rng = np.random.default_rng(4242)
+    for it in range(24):
+        d = int(rng.integers(1, 5))
+        n = int(rng.integers(2, {1: 60, 2: 14, 3: 6, 4: 4}[d]))
+        N = (n + 1) ** d
+        m = int(rng.integers(1, min(40, N) + 1))
+        prob = problem(d, n, m, 5000 + it, float(rng.choice([0.0, 1e-6])), random_uv=True)
+        order = int(rng.integers(0, 3))
+        U_tot = (n + 2) ** d if order == 2 else d * N
+        a = int(rng.integers(0, U_tot))
+        b = int(rng.integers(a, U_tot + 1))
+        S = run_project(pb, prob, unit_begin=a, unit_end=b, unit_order=order)
+        torch.cuda.synchronize()
+        S_or = orc.project_units(prob.grid, prob.U, prob.V, prob.sigma, d, n, a, b, order)
+        for l in range(d):
+            if np.linalg.norm(S_or[l]) == 0:
+                assert float(S[l].abs().max()) == 0.0, (it, d, n, m, order, a, b)
+            else:
+                assert rel(S[l], S_or[l]) <= TOL, (it, d, n, m, order, a, b)
+
+
+def test_workspace_too_small_is_rejected(pb):
+    """Every entry point checks workspace_bytes against prony_workspace_size before launching."""
+    prob = problem(2, 6, 4, 77, random_uv=True)
+    c = prob.cfg
+    small = torch.empty(256, dtype=torch.uint8, device="cuda")
+    with pytest.raises(pb.PronyError) as e:
+        run_project(pb, prob, workspace=small)
+    assert e.value.code == pb.PRONY_ERR_WORKSPACE
+    with pytest.raises(pb.PronyError) as e:
+        pb.vandermonde_ls(dev(prob.z), dev(prob.grid), c.d, c.n, c.m, workspace=small)
+    assert e.value.code == pb.PRONY_ERR_WORKSPACE
+    with pytest.raises(pb.PronyError) as e:
+        pb.toeplitz_apply(dev(prob.grid), dev(prob.U), c.d, c.n, 0, workspace=small)
+    assert e.value.code == pb.PRONY_ERR_WORKSPACE
