@@ -48,13 +48,16 @@
  *   PRONY_OK                 launched (or nothing to do for an empty range)
  *   PRONY_ERR_INVALID        null / misaligned pointer, d,n,m out of range, bad unit_order
  *   PRONY_ERR_RANGE          (2n+2)^d >= 2^31, m > PRONY_MAX_M, m > N, range outside [0, limit]
- *   PRONY_ERR_SINGULAR       (dev_status) G not Hermitian positive definite in the Cholesky
+ *   PRONY_ERR_SINGULAR       (dev_status) G not Hermitian positive definite in the Cholesky, a sigma below
+ *                            the scale guard (prony_project), W singular (prony_diagonalize)
+ *   PRONY_ERR_RANK           detected rank below m (prony_build_pencil) or T = 0 (prony_lanczos_svd)
+ *   PRONY_ERR_NOT_CONVERGED  iteration cap reached (block power, Lanczos, QR eigensolver); outputs written
  *   PRONY_ERR_CUDA           a CUDA launch / copy failed (cudaGetLastError() is left set)
- *   PRONY_ERR_UNIMPLEMENTED  prony_build_pencil (round 1)
+ *   PRONY_ERR_UNIMPLEMENTED  reserved (every entry point of this header is implemented)
  *   PRONY_ERR_WORKSPACE      workspace_bytes smaller than prony_workspace_size(...)
  *
  * Implementation limits (this build): 1 <= d <= PRONY_MAX_D, 1 <= m <= PRONY_MAX_M,
- * m <= N, (2n+2)^d < 2^31.
+ * m <= N, (2n+2)^d < 2^31, N * 8 ceil(m/8) < 2^31.
  */
 #ifndef PRONY_H
 #define PRONY_H
