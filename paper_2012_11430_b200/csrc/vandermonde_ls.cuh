@@ -9,7 +9,10 @@
 namespace prony {
 
 constexpr int kMaxM = PRONY_MAX_M;
-constexpr int kTile = 16;          // columns of A per smem tile of k_vls
+#ifndef PRONY_VLS_TILE
+#define PRONY_VLS_TILE 16
+#endif
+constexpr int kTile = PRONY_VLS_TILE;  // columns of A per smem tile of k_vls
 constexpr int kVlsThreads = 512;   // 16 warps (DMMA warp engine)
 constexpr int kSolveThreads = 512;
 

@@ -19,6 +19,8 @@ VARIANTS = {
     "kk2g2": ["PRONY_KK_UNROLL=2", "PRONY_GATHER_UNROLL=2"],
     "r152p40": ["PRONY_CONSUMER_REGS=152", "PRONY_PRODUCER_REGS=40"],
     "bk8s6": ["PRONY_BK=8", "PRONY_STAGES=6"],
+    "vt32": ["PRONY_VLS_TILE=32"],
+    "vt64": ["PRONY_VLS_TILE=64"],
     "bk8s5": ["PRONY_BK=8", "PRONY_STAGES=5"],
 }
 
