@@ -940,7 +940,9 @@ __global__ void __launch_bounds__(kMvThreads) k_toeplitz_mv(int d, int n, int q,
   const int runs = A / n1;             // runs of the last coordinate inside the inner block
   const int tpr = (n1 + kMvPerThread - 1) / kMvPerThread;  // threads (slots) per run
   const int nslot = runs * tpr;
-  const int Wl = 2 * Pmax + 1, WS = Wl + 4;  // window slot: 1 pad in front, 3 behind
+  // window slot: logical w(-1 .. Wl+2) (1 pad in front, 3 behind) stored 4-way interleaved, element e at
+  // ((e+1) % 4) Q + (e+1) / 4, so the 32 lanes of a warp (outputs 4 apart) read 32 consecutive 16-B words
+  const int Wl = 2 * Pmax + 1, Q = (Wl + 4 + 3) / 4, WS = 4 * Q;
   const int slot = WS + A;
   const int kp = blockIdx.x, s = blockIdx.y, tid = threadIdx.x, nth = blockDim.x;
   auto Pdig = [&](int idx, int ndig) {  // linear box offset of an (ndig)-digit base-(n+1) index
@@ -959,8 +961,9 @@ __global__ void __launch_bounds__(kMvThreads) k_toeplitz_mv(int d, int n, int q,
   auto issue = [&](int hp, int buf) {
     double2* w = mvs + buf * slot;
     const int wbase = Lq * (pk - Pdig(hp, d - q)) + shift - Pmax;
-    const uint32_t sw = (uint32_t)__cvta_generic_to_shared(w + 1);
-    for (int j = tid; j < Wl; j += nth) cp_async16(sw + 16u * j, g + wbase + j, 16);
+    const uint32_t sw = (uint32_t)__cvta_generic_to_shared(w);
+    for (int j = tid; j < Wl; j += nth)
+      cp_async16(sw + 16u * (((j + 1) & 3) * Q + ((j + 1) >> 2)), g + wbase + j, 16);
     const uint32_t sx = (uint32_t)__cvta_generic_to_shared(w + WS);
     for (int b = tid; b < A; b += nth) cp_async16(sx + 16u * b, x + ((size_t)hp * A + b) * ldx, 16);
     cp_async_commit();
@@ -980,7 +983,8 @@ __global__ void __launch_bounds__(kMvThreads) k_toeplitz_mv(int d, int n, int q,
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double2* w = mvs + buf * slot + 1;  // w[j] = g[wbase + j], j in [-1, Wl + 2] readable
+    const double2* wb = mvs + buf * slot;  // w(j) = g[wbase + j], j in [-1, Wl + 2] readable
+    auto w = [&](int j) { return wb[((j + 1) & 3) * Q + ((j + 1) >> 2)]; };
     const double2* xs = mvs + buf * slot + WS;
 #pragma unroll
     for (int u = 0; u < kMvMaxSlots; ++u) {
@@ -1003,11 +1007,11 @@ __global__ void __launch_bounds__(kMvThreads) k_toeplitz_mv(int d, int n, int q,
           // outputs (rho, j0 + r), inputs (beta, bl): window index c + r - bl
           const int c = prho - L * Pdig(beta, q - 1) + j0 + Pmax;
           const double2* xr = xs + beta * n1;
-          double2 v0 = w[c], v1 = w[c + 1], v2 = w[c + 2], v3 = w[c + 3];
+          double2 v0 = w(c), v1 = w(c + 1), v2 = w(c + 2), v3 = w(c + 3);
           int bl = 0;
           for (; bl + 4 <= n1; bl += 4) {
             const double2 x0 = xr[bl], x1 = xr[bl + 1], x2 = xr[bl + 2], x3 = xr[bl + 3];
-            const double2 u0 = w[c - bl - 1], u1 = w[c - bl - 2], u2 = w[c - bl - 3], u3 = w[c - bl - 4];
+            const double2 u0 = w(c - bl - 1), u1 = w(c - bl - 2), u2 = w(c - bl - 3), u3 = w(c - bl - 4);
             step(v0, v1, v2, v3, x0);
             step(u0, v0, v1, v2, x1);
             step(u1, u0, v0, v1, x2);
@@ -1022,7 +1026,7 @@ __global__ void __launch_bounds__(kMvThreads) k_toeplitz_mv(int d, int n, int q,
             v3 = v2;
             v2 = v1;
             v1 = v0;
-            v0 = w[c - bl - 1];
+            v0 = w(c - bl - 1);
           }
         }
         acc[u][0] = c0;
@@ -1128,7 +1132,7 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
     const char* esl = getenv("PRONY_MV_SLICES");
     int S = std::max(1, std::min({kMvMaxSlices, Mp, (40 * sm_count + Mp - 1) / Mp}));
     if (esl) S = std::max(1, std::min({kMvMaxSlices, Mp, atoi(esl)}));
-    const size_t smem = (size_t)2 * ((2 * Pmax + 1 + 4) + A) * sizeof(double2);
+    const size_t smem = (size_t)2 * (4 * ((2 * Pmax + 1 + 4 + 3) / 4) + A) * sizeof(double2);
     if (smem > 227 * 1024) q = 0;
     if (q) {
       if (smem > 48 * 1024 &&
