@@ -407,7 +407,10 @@ int host_pencil(int d, int n, int m, int64_t N, const prony_c128* grid, const pr
   if (rc == PRONY_OK)
     rc = ls_launch(d, n, m, (int)N, (const double2*)(w + h.z), (const double2*)(w + h.grid), c0, c1, nullptr, G_dev,
                    b_dev, solve ? c_dev : nullptr, solve ? t_dev : nullptr, w + h.inner_ls, dst, sms, s3, nullptr);
-  if (rc == PRONY_OK && !(ok(cudaEventRecord(ev_done, s3)) && ok(cudaStreamWaitEvent(st, ev_done, 0))))
+  // `st` ends after everything the call enqueued on s2 and s3 (also when the projection had nothing to
+  // do and never waited on s2): the host buffers may be released once `st` is synchronized
+  if (rc == PRONY_OK && !(ok(cudaEventRecord(ev_done, s3)) && ok(cudaStreamWaitEvent(st, ev_done, 0)) &&
+                          ok(cudaEventRecord(ev[6], s2)) && ok(cudaStreamWaitEvent(st, ev[6], 0))))
     rc = PRONY_ERR_CUDA;
   if (rc != PRONY_OK) {
     cudaStreamSynchronize(s2);

@@ -675,3 +675,28 @@ def test_workspace_too_small_is_rejected(pb):
     with pytest.raises(pb.PronyError) as e:
         pb.toeplitz_apply(dev(prob.grid), dev(prob.U), c.d, c.n, 0, workspace=small)
     assert e.value.code == pb.PRONY_ERR_WORKSPACE
+
+
+def test_pencil_host_part_empty_and_partial(pb, orc):
+    """prony_pencil_host_part: an empty unit / column range gives zero partials; a partial range equals
+    the oracle's partial pencil and LS products over the same units / columns."""
+    prob = problem(3, 5, 6, 909, 1e-6, random_uv=True)
+    c = prob.cfg
+    d, n, m, N = c.d, c.n, c.m, c.N
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    S = torch.empty((d, m, m), dtype=torch.complex128, device="cuda")
+    G = torch.empty((m, m), dtype=torch.complex128, device="cuda")
+    b = torch.empty(m, dtype=torch.complex128, device="cuda")
+    args = [pin(prob.grid), pin(prob.U), pin(prob.V), pin(prob.sigma), pin(prob.z), d, n, m]
+    pb.pencil_host_part(*args, 40, 40, 17, 17, S, G, b)
+    torch.cuda.synchronize()
+    assert float(S.abs().max()) == 0.0 and float(G.abs().max()) == 0.0 and float(b.abs().max()) == 0.0
+    E = (n + 2) ** d
+    pb.pencil_host_part(*args, 37, E - 50, 11, N - 9, S, G, b)
+    torch.cuda.synchronize()
+    S_or = orc.project_units(prob.grid, prob.U, prob.V, prob.sigma, d, n, 37, E - 50, 2)
+    for l in range(d):
+        assert rel(S[l], S_or[l]) <= TOL
+    A = orc.vandermonde(prob.z, d, n, 11, N - 9)
+    G_or, b_or = orc.ls_products(A, prob.grid, d, n, 11, N - 9)
+    assert rel(G, G_or) <= TOL and rel(b, b_or) <= TOL
