@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kReduceThreads, 1) k_reduce(RedParams p) {
     if (stg + kRedStages - 1 < nstage) issue(stg + kRedStages - 1, (stg + kRedStages - 1) % kRedStages);
     else cp_async_commit();
     double* sb = rsm + buf * T::STAGE;
-    {  // sum planes: Re+Im of Y, Re-Im of U (the B operand is conj(U))
+    if constexpr (MODE == 3) {  // sum planes: Re+Im of Y, Re-Im of U (the B operand is conj(U))
       const double2* Yc = reinterpret_cast<const double2*>(sb + T::Y_C);
       const double2* Uc = reinterpret_cast<const double2*>(sb + T::U_C);
       for (int e = tid; e < kRedSlab * BJ; e += kReduceThreads) {
@@ -486,8 +486,8 @@ __global__ void __launch_bounds__(kReduceThreads, 1) k_reduce(RedParams p) {
         const double2 v = Uc[r * T::LDU + i];
         sb[T::U_S + r * T::LDUS + i] = v.x - v.y;
       }
+      __syncthreads();
     }
-    __syncthreads();
     if (warp_rows) {
       const double2* Ac = reinterpret_cast<const double2*>(sb + T::Y_C) + wm * 16;
       const double* As = sb + T::Y_S + wm * 16;
