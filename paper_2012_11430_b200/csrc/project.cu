@@ -440,14 +440,28 @@ __global__ void __launch_bounds__(kReduceThreads, 1) k_reduce(RedParams p) {
       const double2* src = p.Y + (ok ? ((size_t)c * p.R_tot + p.yoff[l] + row) * NP + j : 0);
       cp_async16(st + (uint32_t)(T::Y_C + 2 * (r * T::LDY + jj)) * 8u, src, ok ? 16 : 0);
     }
-    for (int e = tid; e < kRedSlab * T::NPU; e += kReduceThreads) {
-      const int r = e / T::NPU, i = e % T::NPU;
-      const int row = r0 + r;
+    // U rows: the row map is loaded for all of this thread's elements first (independent loads in
+    // flight together), then the copies are issued
+    constexpr int kUPer = (kRedSlab * T::NPU + kReduceThreads - 1) / kReduceThreads;
+    int urows[kUPer];
+#pragma unroll
+    for (int u = 0; u < kUPer; ++u) {
+      const int e = tid + u * kReduceThreads;
+      const int row = r0 + e / T::NPU;
       int urow = p.kb[l] + row;
-      if (p.umap && row < rend) urow = __ldg(p.umap + (size_t)l * p.E + urow);  // -1: no T_l row here
-      const bool ok = row < rend && i < m && urow >= 0;
-      const double2* src = p.U + (ok ? (size_t)urow * m + i : 0);
-      cp_async16(st + (uint32_t)(T::U_C + 2 * (r * T::LDU + i)) * 8u, src, ok ? 16 : 0);
+      if (p.umap && row < rend && e < kRedSlab * T::NPU) urow = __ldg(p.umap + (size_t)l * p.E + urow);  // -1: none
+      urows[u] = urow;
+    }
+#pragma unroll
+    for (int u = 0; u < kUPer; ++u) {
+      const int e = tid + u * kReduceThreads;
+      if (e < kRedSlab * T::NPU) {
+        const int r = e / T::NPU, i = e % T::NPU;
+        const int row = r0 + r;
+        const bool ok = row < rend && i < m && urows[u] >= 0;
+        const double2* src = p.U + (ok ? (size_t)urows[u] * m + i : 0);
+        cp_async16(st + (uint32_t)(T::U_C + 2 * (r * T::LDU + i)) * 8u, src, ok ? 16 : 0);
+      }
     }
     cp_async_commit();
   };
