@@ -396,7 +396,8 @@ def run_ours(args, cfg):
             "roofline": {"bound": "tensor", "kernel": "k_project (complex FP64 DMMA, implicit Toeplitz gather)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                          "traffic": traffic,
-                         "peak_source": "cuBLAS ZGEMM 4096^3 complex128 measured in this run (MEASURED_PEAKS.json has no FP64 entry)",
+                         "peak_source": "cuBLAS ZGEMM 4096^3 complex128 measured in this run (MEASURED_PEAKS.json has no FP64 entry; a bf16-peak x nominal-ratio figure would understate the FP64 pipe)",
+                         "frac_of": "measured",
                          "flops_per_launch": flops_proj, "avg_launch_ms": proj_avg_s * 1e3,
                          # 3M executes 3 of 4 real products, on NP = 8 ceil(m/8) padded columns:
                          "executed_tflops": achieved * cm * (8 * ((m + 7) // 8)) / m,
