@@ -277,6 +277,19 @@ def test_full_size_sampled_columns_oracle(pb, orc, name, cols):
         assert rel(S[ell - 1][:, cols], want) <= TOL
 
 
+@pytest.mark.parametrize("name", ["cfg4", "cfg5"])
+def test_full_size_all_entries_fft_convolution(pb, name):
+    """Every entry of S_l at full BASELINE size against F7: U* (T_l V) Sigma^-1 with T_l V by FFT
+    convolution of the (noisy, for cfg4) grid (tests/f7_fft.py, pinned to the oracle on CPU)."""
+    from f7_fft import fft_apply
+    prob = W.make_problem(name)
+    c = prob.cfg
+    S = run_project(pb, prob).cpu().numpy()
+    for ell in range(1, c.d + 1):
+        want = prob.U.conj().T @ fft_apply(prob.grid, c.d, c.n, ell, prob.V) / prob.sigma[None, :]
+        assert rel(S[ell - 1], want) <= TOL, ell
+
+
 # ------------------------------------------------------------------ Vandermonde / LS parity
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5"])
 def test_vandermonde_ls_configs(pb, orc, name):

@@ -10,6 +10,8 @@ import math
 import os
 
 import numpy as np
+
+from f7_fft import fft_apply  # noqa: E402  (tests/f7_fft.py, shared with the full-size GPU check)
 import pytest
 
 import workload as W
@@ -179,27 +181,6 @@ def test_S_d1_n1_golden(oracle_mod):
             U = V
         S = oracle_mod.project(grid, U, V, np.array([2.0]), 1, 1)
         assert abs(S[0, 0, 0] - ex["S1"]) < 1e-15
-
-
-def fft_apply(grid, d, n, ell, X):
-    """F7: (T_l x)[k] = (g * x)[k + e_l + n 1] — d-dim linear convolution by FFT (numpy),
-    independent of the oracle's gather. X: (N, r). Returns (N, r)."""
-    L = 2 * n + 2
-    g = np.asarray(grid).reshape((L,) * d)
-    size = 3 * n + 2
-    shape = (size,) * d
-    ax = list(range(d))
-    Gf = np.fft.fftn(g, shape, axes=ax)
-    out = np.empty_like(X)
-    sl = []
-    for i in range(d):
-        off = n + (1 if i == ell - 1 else 0)
-        sl.append(slice(off, off + n + 1))
-    for r in range(X.shape[1]):
-        x = X[:, r].reshape((n + 1,) * d)
-        conv = np.fft.ifftn(Gf * np.fft.fftn(x, shape, axes=ax), axes=ax)
-        out[:, r] = conv[tuple(sl)].reshape(-1)
-    return out
 
 
 @pytest.mark.parametrize("d,n,m,noise", [(2, 20, 6, 1e-6), (3, 6, 5, 1e-3), (2, 31, 8, 0.0)])
