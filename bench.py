@@ -149,13 +149,16 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(prob, budget_s=12.0):
+def cpu_baseline_sample(prob, budget_s=16.0):
     """cpu_baseline leg (rank 0, N=1): the oracle on a bounded sample of the bench workload."""
     import oracle
     oracle.build()
     c = prob.cfg
     d, n, m, N = c.d, c.n, c.m, c.N
-    R = 8
+    # calibrate the row count on a warm call (the first one pays the OpenMP pool start-up), aiming at
+    # ~0.8 * budget_s of projection work in the measured sample
+    oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, 8)
+    R = 64
     t0 = time.perf_counter()
     oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, R)
     per_row = (time.perf_counter() - t0) / R
