@@ -110,8 +110,10 @@ def run_reference(args, cfg):
     prob = W.make_problem(cfg)
     c = prob.cfg
     d, n, m, N = c.d, c.n, c.m, c.N
-    # calibrate the sample to ~3 s of project work per step
-    R = 8
+    # calibrate the sample to ~3 s of project work per step (on a warm call: the first one pays the
+    # OpenMP pool start-up)
+    oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, 8)
+    R = min(N, 64)
     t0 = time.perf_counter()
     oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, R)
     per_row = (time.perf_counter() - t0) / R
