@@ -36,7 +36,7 @@
 #include <omp.h>
 #endif
 
-typedef double complex cplx;
+#include "oracle_common.h"
 
 int oracle_abi_version(void) { return 1; }
 
@@ -54,26 +54,6 @@ void oracle_set_num_threads(int t) {
 #else
   (void)t;
 #endif
-}
-
-/* multi-index of element r of I_n (digits base n+1, last coordinate fastest) */
-static void index_of(int d, int n, int64_t r, int* k) {
-  for (int i = d - 1; i >= 0; --i) {
-    k[i] = (int)(r % (n + 1));
-    r /= (n + 1);
-  }
-}
-
-/* box index of the integer point v in {-n..n+1}^d; -1 if outside the box */
-static int64_t box_index(int d, int n, const int* v) {
-  const int64_t L = 2 * (int64_t)n + 2;
-  int64_t idx = 0;
-  for (int i = 0; i < d; ++i) {
-    int b = v[i] + n;
-    if (b < 0 || b >= L) return -1;
-    idx = idx * L + b;
-  }
-  return idx;
 }
 
 /* T_l[k,h] = f(k - h + e_l) for l in 1..d, T[k,h] = f(k - h) for l = 0 */

@@ -398,147 +398,6 @@ def test_end_to_end_recovery_with_oracle_tail(pb, orc):
     assert rel(out["c"].cpu().numpy()[perm], prob.c) <= 1e-8
 
 
-# ------------------------------------------------------------------ NEXT-1: device SVD + diagonalization
-def _proj(U):
-    return U @ U.conj().T
-
-
-@pytest.mark.parametrize("d,n,m,noise", [(2, 12, 5, 0.0), (3, 5, 6, 0.0), (2, 14, 7, 1e-6)])
-def test_build_pencil_svd_vs_oracle(pb, orc, d, n, m, noise):
-    """Block power SVD (Alg. 3) on the device vs the oracle's LAPACK SVD of the dense T: singular
-    values and the singular subspaces (gauge-invariant projectors), then S_l spectra = planted nodes."""
-    prob = problem(d, n, m, 900 + d + n + m, noise, random_uv=True)
-    tol = 1e-6 if noise else None
-    out = pb.build_pencil(dev(prob.grid), d, n, m, seed=3, tol=tol)
-    assert out["status"] in (pb.PRONY_OK, pb.PRONY_ERR_NOT_CONVERGED), out["status"]
-    assert out["rank"] == m
-    T = orc.T_dense(prob.grid, d, n, 0)
-    U_or, V_or, s_or, _ = orc.svd_reduced(T, rank=m)
-    s = out["sigma"].cpu().numpy()
-    assert np.max(np.abs(s - s_or) / s_or[0]) <= 1e-10
-    U = out["U"].cpu().numpy()
-    V = out["V"].cpu().numpy()
-    assert np.linalg.norm(_proj(U) - _proj(U_or)) <= 1e-8 * max(1.0, noise * 1e4)
-    assert np.linalg.norm(_proj(V) - _proj(V_or)) <= 1e-8 * max(1.0, noise * 1e4)
-    np.testing.assert_allclose(U.conj().T @ U, np.eye(m), atol=1e-12)
-    # S from the device equals the oracle's projection with the device's own U, V, sigma
-    S_or = orc.project(prob.grid, U, V, s, d, n)
-    S = out["S"].cpu().numpy()
-    for l in range(d):
-        assert rel(S[l], S_or[l]) <= TOL
-    if noise == 0.0:
-        for l in range(d):
-            ev = np.linalg.eigvals(S[l])
-            for zj in prob.z[:, l]:
-                assert np.min(np.abs(ev - zj)) < 1e-9
-
-
-@pytest.mark.parametrize("d,m", [(1, 4), (2, 5), (3, 12), (2, 40)])
-def test_diagonalize_vs_oracle(pb, orc, d, m):
-    """C_mu eig + W^-1 S_l W on the device vs the oracle (numpy eig + LU solves) on the same S, mu."""
-    rng = np.random.default_rng(d * 100 + m)
-    t_pl = rng.random((m, d))
-    z_pl = W.node_vectors(t_pl)
-    Wt = rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m))
-    S = np.stack([Wt @ np.diag(z_pl[:, l]) @ np.linalg.inv(Wt) for l in range(d)])
-    mu = orc.random_mu(d, 5)
-    z, t, Wd = pb.diagonalize(dev(S), dev(mu), d, m)
-    torch.cuda.synchronize()
-    z = z.cpu().numpy()
-    t = t.cpu().numpy()
-    perm = orc.match_nodes(t, t_pl)
-    assert np.max(np.abs(z[perm] - z_pl)) <= 1e-9
-    assert W.torus_dist_inf(t[perm], t_pl).max() <= 1e-9
-    Wd = Wd.cpu().numpy()
-    C = np.tensordot(mu, S, axes=1)
-    lam = np.diag(np.linalg.solve(Wd, C @ Wd))
-    assert np.linalg.norm(C @ Wd - Wd * lam[None, :]) <= 1e-9 * np.linalg.norm(C)
-    np.testing.assert_allclose(np.linalg.norm(Wd, axis=0), 1.0, atol=1e-12)
-
-
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5"])
-def test_algorithm1_on_device(pb, orc, name):
-    """Algorithm 1 end to end on the device (build_pencil -> diagonalize -> vandermonde_ls): planted
-    t within 1e-8 (noise-free) and c recovered; noisy cfg2: errors at the noise level."""
-    prob = W.make_problem(name, with_svd=False)
-    c = prob.cfg
-    tol = 1e-6 if c.noise else None
-    out = pb.build_pencil(dev(prob.grid), c.d, c.n, c.m, seed=1, tol=tol)
-    assert out["rank"] == c.m, (out["rank"], out["status"])
-    mu = dev(orc.random_mu(c.d, 2))
-    z, t, _ = pb.diagonalize(out["S"], mu, c.d, c.m)
-    ls = pb.vandermonde_ls(z, dev(prob.grid), c.d, c.n, c.m)
-    torch.cuda.synchronize()
-    t = t.cpu().numpy()
-    perm = orc.match_nodes(t, prob.t)
-    terr = W.torus_dist_inf(t[perm], prob.t).max()
-    cerr = rel(ls["c"].cpu().numpy()[perm], prob.c)
-    if c.noise == 0.0:
-        assert terr <= 1e-8 and cerr <= 1e-8, (terr, cerr)
-    else:
-        assert terr <= 1e-6 and cerr <= 1e-4, (terr, cerr)
-
-
-def test_accuracy_table_on_device(pb, orc):
-    """NEXT-2: the paper's accuracy experiment (d=3, n=20, m=5, paper family) on the
-    device: errors linear in eps and within x20 of the printed table (tests/golden/accuracy_table.json)."""
-    import json
-    import os
-    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "accuracy_table.json")))
-    d, n, m = 3, 20, 5
-    t_pl, c_pl = W.paper_family(d, m)
-    rows = {}
-    for eps, row in zip((1e-9, 1e-6), gold["rows"][1:3]):
-        grid = W.sample_grid(t_pl, c_pl, n, eps, 7)
-        out = pb.build_pencil(dev(grid), d, n, m, seed=4, tol=max(eps, 1e-7))
-        assert out["rank"] == m
-        z, t, _ = pb.diagonalize(out["S"], dev(orc.random_mu(d, 6)), d, m)
-        ls = pb.vandermonde_ls(z, dev(grid), d, n, m)
-        torch.cuda.synchronize()
-        t = t.cpu().numpy()
-        perm = orc.match_nodes(t, t_pl)
-        cc = ls["c"].cpu().numpy()[perm]
-        A = orc.vandermonde(z.cpu().numpy(), d, n)
-        f = orc.f_vector(grid, d, n)
-        resid = np.linalg.norm(A.T @ ls["c"].cpu().numpy() - f) / np.linalg.norm(f)
-        errs = (resid, W.torus_dist_inf(t[perm], t_pl).max(), rel(cc, c_pl))
-        for got, paper in zip(errs, row[2:]):
-            assert paper / 20 < got < paper * 20, (eps, errs, row)
-        rows[eps] = errs
-    for i in range(3):
-        assert 300 < rows[1e-6][i] / rows[1e-9][i] < 3000
-
-
-def test_accuracy_table_eps_1e3_rank_anomaly(pb, orc):
-    """NEXT-2, last row of the paper's table: eps = 1e-3 needs tol = 1e-4 (rank 5,
-    errors within x20 of the printed row); with tol = eps = 1e-3 the detected numerical rank drops to 4
-    ("the algorithm detected smaller numerical rank m = 4"), by the block power method and by Lanczos."""
-    import json
-    import os
-    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "accuracy_table.json")))
-    row = gold["rows"][3]
-    d, n, m = 3, 20, 5
-    t_pl, c_pl = W.paper_family(d, m)
-    grid = W.sample_grid(t_pl, c_pl, n, 1e-3, 7)
-    out = pb.build_pencil(dev(grid), d, n, m, seed=4, tol=1e-4)
-    assert out["rank"] == m
-    z, t, _ = pb.diagonalize(out["S"], dev(orc.random_mu(d, 6)), d, m)
-    ls = pb.vandermonde_ls(z, dev(grid), d, n, m)
-    torch.cuda.synchronize()
-    t = t.cpu().numpy()
-    perm = orc.match_nodes(t, t_pl)
-    A = orc.vandermonde(z.cpu().numpy(), d, n)
-    f = orc.f_vector(grid, d, n)
-    resid = np.linalg.norm(A.T @ ls["c"].cpu().numpy() - f) / np.linalg.norm(f)
-    errs = (resid, W.torus_dist_inf(t[perm], t_pl).max(), rel(ls["c"].cpu().numpy()[perm], c_pl))
-    for got, paper in zip(errs, row[2:]):
-        assert paper / 20 < got < paper * 20, (errs, row)
-    low = pb.build_pencil(dev(grid), d, n, m, seed=4, tol=1e-3, check=False)
-    assert low["rank"] == 4 and low["status"] == pb.PRONY_ERR_RANK
-    assert pb.lanczos_svd(dev(grid), d, n, max_rank=2 * m + 5, tol=1e-3, seed=3)["rank"] == 4
-    assert pb.lanczos_svd(dev(grid), d, n, max_rank=2 * m + 5, tol=1e-4, seed=3)["rank"] == 5
-
-
 @pytest.mark.parametrize("bad", ["tiny", "zero", "nan"])
 def test_project_sigma_guard(pb, orc, bad):
     """Scale guard (SURVEY §8(b) conventions; SPEC compute_S errors): sigma_min <= N eps sigma_max,

@@ -273,8 +273,8 @@ def test_b_and_c_noise_free_F3(oracle_mod):
     assert rel(b, G @ c.conj()) < 1e-13
     c_ne = oracle_mod.cholesky_solve(G, b)
     assert rel(c_ne, c) < 1e-12
-    c_qr = oracle_mod.lstsq_qr(A, oracle_mod.f_vector(grid, d, n))
-    assert rel(c_qr, c) < 1e-12
+    c_qr, resid = oracle_mod.lstsq_qr(A, grid, d, n)
+    assert rel(c_qr, c) < 1e-12 and resid < 1e-13
 
 
 def test_ls_products_partition(oracle_mod):
@@ -352,25 +352,21 @@ def test_algorithm1_paper_family_ranks(oracle_mod):
     assert ranks[15] < 15 and ranks[20] < 20
 
 
-def test_algorithm1_error_linear_in_eps(oracle_mod):
-    """PAPER.md:647 / 571: forward errors proportional to eps; noise-free t error at roundoff.
-    Paper table (tests/golden/accuracy_table.json, d=3 n=20 m=5) is matched within x20 in
-    magnitude here at desk scale d=2, n=20, m=5 (same family), rank by tol = eps."""
-    gold = json.load(open(os.path.join(GOLD, "accuracy_table.json")))
+def test_algorithm1_error_linear_in_eps_desk(oracle_mod):
+    """PAPER.md:647 / 571: forward errors proportional to eps (Jacobi route, desk scale d=2, n=20, m=5 of the
+    paper family, rank by tol = eps). The table itself is pinned at its own configuration
+    d=3, n=20, m=5 in test_oracle_alg1_pins.py."""
     d, n, m = 2, 20, 5
     t, c = W.paper_family(d, m)
     errs = {}
     for eps in (0.0, 1e-9, 1e-6):
-        grid = W.sample_grid(t, c, n, eps, 7)
+        grid = W.sample_grid(t, c, n, eps, 7, noise_model="disk")
         tol = eps if eps > 0 else None
         out = oracle_mod.algorithm1(grid, d, n, tol=tol, seed=5)
         assert out["rank"] == m
         perm = oracle_mod.match_nodes(out["t"], t)
         errs[eps] = (out["resid"], W.torus_dist_inf(out["t"][perm], t).max(), rel(out["c"][perm], c))
     assert errs[0.0][1] < 1e-13 and errs[0.0][2] < 1e-11
-    for eps, row in ((1e-9, gold["rows"][1]), (1e-6, gold["rows"][2])):
-        for got, paper in zip(errs[eps], row[2:]):
-            assert paper / 20 < got < paper * 20
-    for i in range(3):    # linear in eps: ratio of errors ~ 1e3
+    for i in range(3):    # linear in eps: one pattern scaled by eps (R5b) gives a ratio of 1e3
         r = errs[1e-6][i] / errs[1e-9][i]
-        assert 300 < r < 3000
+        assert 900 < r < 1100

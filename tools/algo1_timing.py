@@ -20,7 +20,7 @@ c = prob.cfg
 grid = torch.from_numpy(prob.grid).cuda()
 tol = 1e-6 if c.noise else None
 ws = pb.alloc_workspace(pb.WS_BUILD, c.d, c.n, c.m)
-mu = torch.from_numpy(oracle.random_mu(c.d, 2)).cuda()
+mu = torch.from_numpy(W.random_mu(c.d, 2)).cuda()
 res = {}
 for rep in range(2):
     torch.cuda.synchronize()

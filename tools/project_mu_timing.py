@@ -18,7 +18,7 @@ prob = W.make_problem("cfg4")
 c = prob.cfg
 tg = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
 grid, U, V, s = tg(prob.grid), tg(prob.U), tg(prob.V), tg(prob.sigma)
-mu = tg(oracle.random_mu(c.d, 3))
+mu = tg(W.random_mu(c.d, 3))
 ws = pb.alloc_workspace(pb.WS_PROJECT_MU, c.d, c.n, c.m)
 wsp = pb.alloc_workspace(pb.WS_PROJECT, c.d, c.n, c.m)
 

@@ -140,13 +140,47 @@ def noise_pattern(shape, seed: int) -> np.ndarray:
     return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / math.sqrt(2.0)
 
 
-def sample_grid(t: np.ndarray, c: np.ndarray, n: int, noise: float = 0.0, seed: int = 0) -> np.ndarray:
-    """f~(k) = f(k)(1 + delta_k) on the box {-n..n+1}^d (reading R1)."""
+def disk_pattern(shape, seed: int) -> np.ndarray:
+    """One normalized bounded pattern rho e^{i theta}, rho ~ U[0,1], theta ~ U[0, 2 pi): |delta| <= 1
+    (the paper's noise model |delta_k| <= eps; reading R5b: SPEC S:73 draws r uniform on
+    [0, eps], and the identical mantissas of the table rows 1e-9 / 1e-6, say one pattern is
+    reused and scaled by eps)."""
+    rng = np.random.default_rng([seed, 13])
+    rho = rng.random(shape)
+    theta = 2.0 * np.pi * rng.random(shape)
+    return rho * np.exp(1j * theta)
+
+
+def sample_grid(t: np.ndarray, c: np.ndarray, n: int, noise: float = 0.0, seed: int = 0,
+                noise_model: str = "gauss") -> np.ndarray:
+    """f~(k) = f(k)(1 + delta_k) on the box {-n..n+1}^d (reading R1).
+    noise_model "gauss": delta = sigma (xi + i eta)/sqrt 2 (BASELINE configs, reading R5);
+    "disk": delta = eps rho e^{i theta}, |delta| <= eps (the paper's accuracy experiment, reading R5b)."""
     d = t.shape[1]
     f = evaluate(t, c, box_coords(d, n))
     if noise > 0.0:
-        f = f * (1.0 + noise * noise_pattern(f.shape, seed))
+        if noise_model == "gauss":
+            f = f * (1.0 + noise * noise_pattern(f.shape, seed))
+        elif noise_model == "disk":
+            f = f * (1.0 + noise * disk_pattern(f.shape, seed))
+        else:
+            raise ValueError(noise_model)
     return np.ascontiguousarray(f)
+
+
+def random_mu(d: int, seed: int) -> np.ndarray:
+    """mu ~ complex Gaussian, normalized to ||mu||_2 = 1 (the random point of S_C^{d-1}, PAPER.md:56;
+    reading R7). A random draw of the method, passed to both the oracle and the device diagonalization."""
+    rng = np.random.default_rng([seed, 11])
+    mu = rng.standard_normal(d) + 1j * rng.standard_normal(d)
+    return mu / math.sqrt(float(np.sum(np.abs(mu) ** 2)))
+
+
+def gaussian_block(N: int, r: int, seed: int, which: int) -> np.ndarray:
+    """Seeded complex Gaussian N x r block: the random starting matrices U_0 (which=0), V_0 (which=1) of
+    Algorithm 3 before orthonormalization (PAPER.md:181 leaves them unspecified; reading R14)."""
+    rng = np.random.default_rng([seed, 17, which])
+    return np.ascontiguousarray(rng.standard_normal((N, r)) + 1j * rng.standard_normal((N, r)))
 
 
 def node_vectors(t: np.ndarray) -> np.ndarray:
