@@ -1,6 +1,7 @@
 """bench.py — pencils/s and FP64 TFLOP/s of the hot path (S_1..S_d + Vandermonde/LS), one JSON line.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--cfg cfg4] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--cfg cfg4] [--units shared|l-major|row-major]
+                    [--impl ours|reference] [--dist-backend nccl|gloo]
 
 A step is one whole pencil of the headline workload (BASELINE.json configs[3], "cfg4": d=2,
 n=200, N=40401, m=100, complex-Gaussian noise sigma=1e-6): prony_project over this rank's
@@ -9,8 +10,13 @@ and the m x m solve when N > 1). Inputs are resident in HBM; L2 is flushed (a 25
 before every timed step, outside the timed interval. Timing: CUDA events per step on the
 launching stream, barrier + synchronize around the loop, max over ranks.
 
-e2e: the same pencil through the C ABI with HOST buffers (prony_pencil_host: pinned host ->
-device copies of grid, U, V, sigma, z, the device path, device -> host copies of S, G, b, c, t).
+--gpus N > 1 without a torchrun environment re-executes itself under
+`python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1`, so the
+driver's `python bench.py --gpus N` and its torchrun form run the same N-rank job.
+
+e2e: the same pencil end to end from pinned HOST buffers — N = 1 through the C ABI
+(prony_pencil_host); N > 1 through sharding.DistributedPencil.from_host (each rank copies its slice
+of V, its U rows and the grid; V is all-gathered over NVLink; all-reduce; D2H of S, c, t on rank 0).
 
 --impl reference: the CPU oracle (oracle/, plain C, all host cores) on a bounded sample of the
 same workload per step, extrapolated to pencils/s (this tier has no installable reference).
@@ -18,6 +24,8 @@ same workload per step, extrapolated to pencils/s (this tier has no installable 
 from __future__ import annotations
 
 import argparse
+import fcntl
+import hashlib
 import json
 import os
 import statistics
@@ -35,16 +43,29 @@ import workload as W  # noqa: E402
 
 METRIC = "pencils/s and FP64 TFLOP/s (% peak) for S_1..S_d+LS, d=2 N=40401 m=100, 1/2/4/8 GPUs"
 UNIT = "pencils/s"
+# sources of k_project: an ncu capture is used for roofline.traffic only if it was taken on these
+KPROJECT_SOURCES = ["paper_2012_11430_b200/csrc/project.cu", "paper_2012_11430_b200/csrc/project.cuh",
+                    "paper_2012_11430_b200/csrc/engine.cuh", "paper_2012_11430_b200/csrc/common.cuh"]
+TRAFFIC_PROFILE = os.path.join(ROOT, "profiles", "ncu_k_project_current.json")
 
 
-def pencil_flops(d, N, m):
-    """Algorithmic flops of one pencil: d(8mN^2 + 8Nm^2) + 8m^2 N + 8mN."""
+def paper_pencil_flops(d, N, m):
+    """The paper's formulation: d separate products T_l V and U^* (T_l V), ZGEMM
+    convention (8 real flops per complex MAC): d(8mN^2 + 8Nm^2) + 8m^2 N + 8mN."""
     return d * (8.0 * m * N * N + 8.0 * N * m * m) + 8.0 * m * m * N + 8.0 * m * N
+
+
+def source_stamp(paths=KPROJECT_SOURCES):
+    h = hashlib.sha1()
+    for p in paths:
+        with open(os.path.join(ROOT, p), "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
 
 
 # ------------------------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms during the timed region."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -59,7 +80,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
             return
@@ -100,71 +121,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ------------------------------------------------------------------------------------ reference arm
-def run_reference(args, cfg):
-    """The oracle, as it stands, on host cores: each step = a bounded sample of one pencil
-    (rows [0, R) of T_1 V plus U^* for the pencil part; columns [0, C) of A, G, b for LS),
-    extrapolated to a full pencil."""
+# ------------------------------------------------------------------------------------ the oracle on host cores
+def oracle_pencil_sample(prob, budget_s):
+    """The oracle, as it stands, on a bounded sample of one pencil: rows [0, R) of T_1 through
+    oracle_project_rows (naive T_1 V then U^*, the O(N^2 m) part) and columns [0, C) through
+    oracle_vandermonde + oracle_ls_products; R is calibrated on a warm call to ~0.8 budget_s.
+    Returns (seconds per pencil extrapolated linearly to d*N rows and N columns, sample description)."""
     import oracle
-    oracle.build()
-    prob = W.make_problem(cfg)
     c = prob.cfg
     d, n, m, N = c.d, c.n, c.m, c.N
-    # calibrate the sample to ~3 s of project work per step (on a warm call: the first one pays the
-    # OpenMP pool start-up)
-    oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, 8)
+    oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, min(8, N))  # warm the thread pool
     R = min(N, 64)
     t0 = time.perf_counter()
     oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, R)
     per_row = (time.perf_counter() - t0) / R
-    R = int(max(8, min(N, 3.0 / max(per_row, 1e-9))))
-    Cc = min(N, 4096)
-
-    def step():
-        t0 = time.perf_counter()
-        oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, R)
-        t_proj = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        A = oracle.vandermonde(prob.z, d, n, 0, Cc)
-        oracle.ls_products(A, prob.grid, d, n, 0, Cc)
-        t_ls = time.perf_counter() - t0
-        return t_proj * (d * N / R) + t_ls * (N / Cc)
-
-    for _ in range(args.warmup):
-        step()
-    est = [step() for _ in range(args.steps)]
-    sec = statistics.median(est)
-    value = 1.0 / sec
-    sample = (f"per step: oracle_project_rows rows [0,{R}) of T_1 (of d*N={d * N} row-units) + "
-              f"vandermonde+ls_products on columns [0,{Cc}) of N={N}; extrapolated linearly to one pencil")
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{c.name}: d={d} n={n} N={N} m={m} noise={c.noise}", "d": d, "n": n, "N": N, "m": m,
-                   "parallelism": "host threads (OpenMP)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-                         "sample": sample},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "tflops": pencil_flops(d, N, m) * value / 1e12,
-    }
-    print(json.dumps(line), flush=True)
-
-
-def cpu_baseline_sample(prob, budget_s=16.0):
-    """cpu_baseline leg (rank 0, N=1): the oracle on a bounded sample of the bench workload."""
-    import oracle
-    oracle.build()
-    c = prob.cfg
-    d, n, m, N = c.d, c.n, c.m, c.N
-    # calibrate the row count on a warm call (the first one pays the OpenMP pool start-up), aiming at
-    # ~0.8 * budget_s of projection work in the measured sample
-    oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, 8)
-    R = 64
-    t0 = time.perf_counter()
-    oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, R)
-    per_row = (time.perf_counter() - t0) / R
-    R = int(max(8, min(N, 0.8 * budget_s / max(per_row, 1e-9))))
+    R = int(max(1, min(N, 0.8 * budget_s / max(per_row, 1e-9))))
     t0 = time.perf_counter()
     oracle.project_rows(prob.grid, prob.U, prob.V, prob.sigma, d, n, 1, 0, R)
     t_proj = time.perf_counter() - t0
@@ -174,21 +145,81 @@ def cpu_baseline_sample(prob, budget_s=16.0):
     oracle.ls_products(A, prob.grid, d, n, 0, Cc)
     t_ls = time.perf_counter() - t0
     sec = t_proj * (d * N / R) + t_ls * (N / Cc)
-    return {"value": 1.0 / sec, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": (f"oracle_project_rows on rows [0,{R}) of T_1 ({t_proj:.1f} s) + vandermonde/ls_products on "
-                       f"columns [0,{Cc}) ({t_ls:.1f} s), extrapolated to one pencil of {c.name} "
-                       f"({d * N} row-units, {N} columns): {sec:.0f} s per pencil")}
+    sample = (f"oracle_project_rows on rows [0,{R}) of T_1 ({t_proj:.1f} s) + vandermonde/ls_products on columns "
+              f"[0,{Cc}) ({t_ls:.2f} s), extrapolated linearly to one pencil of {c.name} ({d * N} T_l rows, {N} "
+              f"columns): {sec:.1f} s per pencil")
+    return sec, sample
+
+
+def host_info():
+    import oracle
+    return {"nproc": os.cpu_count(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS"),
+            "threads_used": oracle.num_threads()}
+
+
+def cpu_baseline(prob, budget_s=16.0):
+    """cpu_baseline leg (rank 0, N=1): the oracle on all host cores on a bounded sample of the bench workload,
+    plus the small configs cfg1/cfg2 on ONE core (same bounded sampling, ~3 s each)."""
+    import oracle
+    oracle.build()
+    sec, sample = oracle_pencil_sample(prob, budget_s)
+    info = host_info()
+    small = {}
+    threads = oracle.num_threads()
+    try:
+        oracle.set_num_threads(1)
+        for name in ("cfg1", "cfg2"):
+            p = W.make_problem(name)
+            s1, _ = oracle_pencil_sample(p, 3.0)
+            small[name] = {"value": 1.0 / s1, "unit": UNIT, "cores": 1}
+    finally:
+        oracle.set_num_threads(threads)
+    return {"value": 1.0 / sec, "unit": UNIT, "cores": info["threads_used"], "kind": "oracle", "sample": sample,
+            **info, "small_configs_1core": small}
+
+
+def run_reference(args, cfg):
+    """Reference arm: the oracle, as it stands, on host cores; each step = the same bounded sample as the
+    cpu_baseline leg (~3 s of CPU work), extrapolated to pencils/s."""
+    import oracle
+    oracle.build()
+    prob = W.make_problem(cfg)
+    c = prob.cfg
+    d, n, m, N = c.d, c.n, c.m, c.N
+    est, sample = [], ""
+    for i in range(args.warmup + args.steps):
+        sec, sample = oracle_pencil_sample(prob, 3.0)
+        if i >= args.warmup:
+            est.append(sec)
+    sec = statistics.median(est)
+    value = 1.0 / sec
+    info = host_info()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{c.name}: d={d} n={n} N={N} m={m} noise={c.noise}", "d": d, "n": n, "N": N, "m": m,
+                   "parallelism": "host threads (OpenMP)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["threads_used"], "kind": "oracle",
+                         "sample": "per step: " + sample, **info},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "paper_equivalent_tflops": paper_pencil_flops(d, N, m) * value / 1e12,
+    }
+    print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------------------------ our arm
-def zgemm_peak_tflops(torch, n=4096, reps=5):
-    """cuBLAS ZGEMM (complex128) throughput measured now: the FP64-tensor roofline denominator."""
+def zgemm_peak_tflops(torch, index, n=4096, reps=40):
+    """cuBLAS ZGEMM (complex128, 4 real DMMA products) throughput measured now, best of `reps`: the
+    FP64-tensor roofline denominator (real FP64 flop/s), with the SM clocks sampled while it runs."""
     a = torch.randn(n, n, dtype=torch.complex128, device="cuda")
     b = torch.randn(n, n, dtype=torch.complex128, device="cuda")
     c = torch.empty_like(a)
-    for _ in range(2):
+    for _ in range(3):
         torch.matmul(a, b, out=c)
     torch.cuda.synchronize()
+    clocks = ClockSampler(index)
+    clocks.start()
     best = 1e30
     for _ in range(reps):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -197,8 +228,21 @@ def zgemm_peak_tflops(torch, n=4096, reps=5):
         e.record()
         e.synchronize()
         best = min(best, s.elapsed_time(e))
+    clk = clocks.stop()
     del a, b, c
-    return 8.0 * n ** 3 / (best * 1e-3) / 1e12
+    return 8.0 * n ** 3 / (best * 1e-3) / 1e12, clk
+
+
+def stamped_traffic():
+    """roofline.traffic: dram bytes per k_project launch from the committed ncu --set full summary, used
+    only if that capture was taken on the current k_project sources (source stamp match)."""
+    try:
+        j = json.load(open(TRAFFIC_PROFILE))
+    except (OSError, ValueError):
+        return None, "no capture"
+    if j.get("source_stamp") != source_stamp():
+        return None, f"stale capture ({j.get('source_stamp')} != {source_stamp()})"
+    return j.get("dram_bytes_per_launch"), os.path.relpath(TRAFFIC_PROFILE, ROOT)
 
 
 def run_ours(args, cfg):
@@ -240,12 +284,9 @@ def run_ours(args, cfg):
             e.record(stream)  # force creation so .cuda_event is a live handle
         return evs
 
-    def step(info_p=None, info_l=None):
-        return pencil(grid, U, V, sigma, z, stream=stream, info_p=info_p, info_l=info_l)
-
     # warm-up (also validates the device status once)
     for _ in range(max(args.warmup, 0)):
-        step()
+        pencil(grid, U, V, sigma, z, stream=stream)
     torch.cuda.synchronize()
     assert int(st.item()) == 0, f"device status {int(st.item())}"
 
@@ -253,6 +294,7 @@ def run_ours(args, cfg):
     ev_s, ev_e = new_events(K), new_events(K)
     ev_ps, ev_pe = new_events(K), new_events(K)
     ev_ls, ev_le = new_events(K), new_events(K)
+    ev_cs, ev_ce = new_events(K), new_events(K)
     infos_p = [pb.make_exec_info(ev_ps[i], ev_pe[i]) for i in range(K)]
     infos_l = [pb.make_exec_info(ev_ls[i], ev_le[i]) for i in range(K)]
     torch.cuda.synchronize()
@@ -265,29 +307,34 @@ def run_ours(args, cfg):
     for i in range(K):
         flush.fill_(i & 0xFF)                  # L2 flush outside the timed interval
         ev_s[i].record(stream)
-        step(infos_p[i], infos_l[i])
+        pencil(grid, U, V, sigma, z, stream=stream, info_p=infos_p[i], info_l=infos_l[i],
+               ev_comm=(ev_cs[i], ev_ce[i]) if world > 1 else None)
         ev_e[i].record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    assert int(st.item()) == 0, f"device status {int(st.item())}"
 
     step_ms = [ev_s[i].elapsed_time(ev_e[i]) for i in range(K)]
     proj_ms = [ev_ps[i].elapsed_time(ev_pe[i]) for i in range(K)]
     vls_ms = [ev_ls[i].elapsed_time(ev_le[i]) for i in range(K)]
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms, sum(proj_ms)], dtype=torch.float64, device=dev)
+    comm_ms = [ev_cs[i].elapsed_time(ev_ce[i]) for i in range(K)] if world > 1 else [0.0] * K
+    mine = torch.tensor([sum(step_ms), statistics.mean(proj_ms), statistics.mean(vls_ms), statistics.mean(comm_ms),
+                         statistics.mean(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms_max = float(t[0])
+        allr = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per_rank = [x.tolist() for x in allr]
+    else:
+        per_rank = [mine.tolist()]
+    total_ms_max = max(r[0] for r in per_rank)
     launches_per_step = infos_p[0].launches + infos_l[0].launches + (1 if world > 1 else 0)
 
-    # ---- end to end from pinned host buffers: N = 1 through the C-ABI host call prony_pencil_host;
-    # N > 1 through the sharded public API (pinned H2D of the inputs on every rank, the pencil, D2H of
-    # S, c, t on rank 0), the whole interval timed on the device (max over ranks)
+    # ---- end to end from pinned host buffers
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
     hg, hU, hV, hs, hz = pin(prob.grid), pin(prob.U), pin(prob.V), pin(prob.sigma), pin(prob.z)
-    h2d = sum(x.numel() * x.element_size() for x in (hg, hU, hV, hs, hz))
+    h2d_full = sum(x.numel() * x.element_size() for x in (hg, hU, hV, hs, hz))
     Ke = max(2, min(K, 5))
     e_ms = []
     if world == 1:
@@ -295,7 +342,7 @@ def run_ours(args, cfg):
                 [("S", (d, m, m), torch.complex128), ("G", (m, m), torch.complex128), ("b", (m,), torch.complex128),
                  ("c", (m,), torch.complex128), ("t", (m, d), torch.float64)]}
         ws_h = pb.alloc_workspace(pb.WS_PENCIL_HOST, d, n, m, dev)
-        for _ in range(max(args.warmup, 3)):  # e2e warm-up: same count as the device loop
+        for _ in range(max(args.warmup, 3)):
             pb.pencil_host(hg, hU, hV, hs, hz, d, n, m, workspace=ws_h, outputs=outs, stream=stream)
         for i in range(Ke):
             flush.fill_(i & 0xFF)
@@ -309,32 +356,17 @@ def run_ours(args, cfg):
             assert r["status"] == 0
             e_ms.append(e0.elapsed_time(e1))
         d2h = sum(x.numel() * x.element_size() for x in outs.values() if isinstance(x, torch.Tensor)) + 4
+        h2d_rank = [h2d_full]
         api = "prony_pencil_host (C ABI, pinned host buffers)"
         del ws_h
     else:
-        dg, dU, dV, ds, dz = (torch.empty_like(x, device=dev) for x in (hg, hU, hV, hs, hz))
         hS = torch.empty((d, m, m), dtype=torch.complex128).pin_memory()
         hc = torch.empty(m, dtype=torch.complex128).pin_memory()
         ht = torch.empty((m, d), dtype=torch.float64).pin_memory()
-
-        shared = pencil.order == sharding.UNITS_SHARED
-        if shared:  # per rank: grid, V, sigma, z (+ z for the solve) and only the U rows its slab pairs with
-            ulo, uhi = sharding.shared_u_rows(d, n, pencil.u0, pencil.u1)
-            h2d_rank = (hg.numel() + hV.numel() + 2 * hz.numel() + (uhi - ulo) * m) * 16 + hs.numel() * 8
-        else:
-            h2d_rank = h2d
-        hb = torch.tensor([float(h2d_rank)], dtype=torch.float64, device=dev)
-        dist.all_reduce(hb, op=dist.ReduceOp.SUM)
-        h2d_total = int(hb.item())
+        h2d_rank = [sharding.h2d_bytes(d, n, m, world, r, order, scatter_v=True) for r in range(world)]
 
         def e2e_step():
-            if shared:
-                dz.copy_(hz, non_blocking=True)
-                Sx, cx, tx = pencil.from_host(hg, hU, hV, hs, hz, dz, stream=stream)
-            else:
-                for dst, src in ((dg, hg), (dU, hU), (dV, hV), (ds, hs), (dz, hz)):
-                    dst.copy_(src, non_blocking=True)
-                Sx, cx, tx = pencil(dg, dU, dV, ds, dz, stream=stream)
+            Sx, cx, tx = pencil.from_host(hg, hU, hV, hs, hz, stream=stream, scatter_v=True)
             if rank == 0:
                 hS.copy_(Sx, non_blocking=True)
                 hc.copy_(cx, non_blocking=True)
@@ -355,74 +387,108 @@ def run_ours(args, cfg):
             e1.synchronize()
             e_ms.append(e0.elapsed_time(e1))
         d2h = (hS.numel() + hc.numel()) * 16 + ht.numel() * 8
-        api = ("sharding.DistributedPencil.from_host -> prony_pencil_host_part (pinned H2D per rank, V copy "
-               "overlapped, all-reduce, D2H on rank 0)" if shared else
-               "sharding.DistributedPencil (pinned H2D per rank, all-reduce, D2H on rank 0)")
+        api = ("sharding.DistributedPencil.from_host (per rank: pinned H2D of the grid, its 1/N slice of V and its "
+               "U rows; all_gather of V over the device interconnect; pencil; all-reduce; D2H of S, c, t on rank 0)")
     te = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e = {"value": Ke / (float(te[0]) * 1e-3), "unit": UNIT,
-           "h2d_bytes_per_step": h2d if world == 1 else h2d_total,
-           "d2h_bytes_per_step": d2h, "ms_per_step": float(te[0]) / Ke, "api": api}
+    e2e = {"value": Ke / (float(te[0]) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": sum(h2d_rank),
+           "h2d_bytes_per_rank": h2d_rank, "d2h_bytes_per_step": d2h, "ms_per_step": float(te[0]) / Ke, "api": api}
 
-    # ---- roofline of the dominant kernel (k_project), measured live above
-    flops_proj = infos_p[0].main_flops
-    proj_avg_s = statistics.mean(proj_ms) * 1e-3
-    peak = zgemm_peak_tflops(torch) if rank == 0 else None
+    peak = peak_clk = None
+    if rank == 0:
+        peak, peak_clk = zgemm_peak_tflops(torch, local)
 
     if rank == 0:
         value = K / (total_ms_max * 1e-3)   # one pencil per step, sharded over the ranks
         ms_per_step = total_ms_max / K
-        F = pencil_flops(d, N, m)
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "r01_ncu_project.json")
-        if os.path.exists(prof):
-            try:
-                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
-            except (OSError, ValueError):
-                traffic = None
-        achieved = flops_proj / proj_avg_s / 1e12
         cm = 1.0 if os.environ.get("PRONY_CMUL", "3m").startswith("4") else 0.75
+        # complex MACs of the pencil as this implementation computes it (per rank: k_project's product over
+        # its E rows; the reduce U^* Y over those rows for every l; the LS products over its columns)
+        cmac_proj = infos_p[0].main_flops / 8.0
+        rows = cmac_proj / (m * N)
+        cmac_step = cmac_proj + d * m * m * rows + m * m * N / world + m * N / world
+        real_per_cmac = 8.0 * cm                         # 3M: 3 real products = 6 real flops per complex MAC
+        proj_avg_s = statistics.mean(proj_ms) * 1e-3
+        achieved = real_per_cmac * cmac_proj / proj_avg_s / 1e12
+        np_pad = 8 * ((m + 7) // 8)
+        executed = achieved * np_pad / m                 # the DMMA work including the padded columns
+        traffic, traffic_src = stamped_traffic()
+        tflops = real_per_cmac * cmac_step * world * value / 1e12
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",  # one pencil per step at every N (fixed total work)
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",  # one pencil per step at every N
             "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded planted exponential sum, complex Gaussian noise 1e-6)",
             "config": {"workload": f"{c.name}: d={d} n={n} N={N} m={m} noise={c.noise} (BASELINE configs[{int(c.name[3:]) - 1}])",
                        "d": d, "n": n, "N": N, "m": m, "parallelism": f"dp{world} ({['l-major', 'row-major', 'shared'][order]} units)",
                        "l2": "flushed (256 MiB write) before every timed step, outside the timed interval",
-                       "pencils_per_step": 1, "comm": "1 x all_reduce(SUM) of packed [S,G,b] per step" if world > 1 else "none"},
-            "tflops": F * value / 1e12,
-            "pct_peak": (F * value / 1e12) / (peak * world) if peak else None,
-            "flop_accounting": ("tflops/pct_peak count the paper's d(8mN^2+8Nm^2)+8m^2N+8mN per pencil; with "
-                                "shared units one extended product T_E V ((n+2)^d rows) replaces the d products "
-                                "T_l V (d(n+1)^d rows), DESIGN.md F8; roofline.achieved counts the flops of the "
-                                "product k_project actually computes (8 m N rows), as a 4M ZGEMM would"),
+                       "pencils_per_step": 1,
+                       "comm": "1 x all_reduce(SUM) of packed [S,G,b] per step" if world > 1 else "none",
+                       "dist_backend": args.dist_backend if world > 1 else None},
+            # physical rates: real FP64 flops the implementation executes per pencil (3M products) / time
+            "tflops": tflops,
+            "pct_peak": tflops / (peak * world) if peak else None,
+            "paper_equivalent_tflops": paper_pencil_flops(d, N, m) * value / 1e12,
+            "flop_accounting": ("tflops = real FP64 flops executed per pencil / step time: complex MACs of the "
+                                "shared-row product T_E V ((n+2)^d rows, DESIGN.md F8) + U^*Y for every l + the LS "
+                                "products, x6 real flops per complex MAC (3M); pct_peak = tflops / (measured ZGEMM "
+                                "x N GPUs), a fraction. paper_equivalent_tflops = the paper's d separate ZGEMM-"
+                                "convention products (SURVEY §8(d) F) per second: not a hardware rate."),
             "roofline": {"bound": "tensor", "kernel": "k_project (complex FP64 DMMA, implicit Toeplitz gather)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                         "traffic": traffic,
-                         "peak_source": "cuBLAS ZGEMM 4096^3 complex128 measured in this run (MEASURED_PEAKS.json has no FP64 entry; a bf16-peak x nominal-ratio figure would understate the FP64 pipe)",
-                         "frac_of": "measured",
-                         "flops_per_launch": flops_proj, "avg_launch_ms": proj_avg_s * 1e3,
-                         # 3M executes 3 of 4 real products, on NP = 8 ceil(m/8) padded columns:
-                         "executed_tflops": achieved * cm * (8 * ((m + 7) // 8)) / m,
-                         "executed_frac": (achieved * cm * (8 * ((m + 7) // 8)) / m) / peak if peak else None,
-                         "cmul": "4M" if cm == 1.0 else "3M",
-                         # also against the planning figure 148 SM x 128 FP64 flop/clk x 1.965 GHz
-                         "planning_peak": 37.2, "executed_frac_vs_planning": (achieved * cm * (8 * ((m + 7) // 8)) / m) / 37.2,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_flops_per_launch": real_per_cmac * cmac_proj,
+                         "flops_definition": ("6 real flops per complex MAC (3M: 3 real DMMA products) x m N rows; "
+                                              "the ZGEMM convention (8 per complex MAC) is achieved_zgemm_convention"),
+                         "achieved_zgemm_convention": 8.0 * cmac_proj / proj_avg_s / 1e12,
+                         "executed_tflops": executed, "executed_frac": executed / peak if peak else None,
+                         "peak_source": ("cuBLAS ZGEMM 4096^3 complex128 measured in this run, best of 40 (real FP64 "
+                                         "flop/s; MEASURED_PEAKS.json has no FP64 entry)"),
+                         "peak_clocks": peak_clk, "frac_of": "measured",
+                         "planning_peak": 37.2, "frac_vs_planning": achieved / 37.2,
+                         "avg_launch_ms": proj_avg_s * 1e3, "cmul": "4M" if cm == 1.0 else "3M",
                          "share_of_step": sum(proj_ms) / sum(step_ms),
                          "grid": list(infos_p[0].main_grid), "split_k": infos_p[0].split_k},
-            "kernels_ms": {"k_project": statistics.mean(proj_ms), "k_vls": statistics.mean(vls_ms)},
+            "kernels_ms": {"k_project": statistics.mean(proj_ms), "k_vls": statistics.mean(vls_ms),
+                           "outside_k_project": statistics.mean(step_ms) - statistics.mean(proj_ms)},
+            "per_rank": [{"rank": r, "step_ms": x[4], "k_project_ms": x[1], "k_vls_ms": x[2], "allreduce_ms": x[3]}
+                         for r, x in enumerate(per_rank)],
             "gpu_launches": launches_per_step * K,
             "clocks": clk,
             "e2e": e2e,
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline_sample(prob)
+            line["cpu_baseline"] = cpu_baseline(prob)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def relaunch_under_torchrun(args_argv, gpus):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec as an N-rank torchrun job on this node."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *args_argv]
+    os.execv(sys.executable, cmd)
+
+
+def build_locked():
+    """Build libprony.so once per node: every rank takes the same file lock; the first builds, the others
+    find the library fresh (no concurrent nvcc into the same objects)."""
+    from paper_2012_11430_b200 import _build
+    import oracle
+    lock = os.path.join(ROOT, "paper_2012_11430_b200", ".build.lock")
+    with open(lock, "w") as f:
+        fcntl.flock(f, fcntl.LOCK_EX)
+        _build.build()
+        oracle.build()
+        fcntl.flock(f, fcntl.LOCK_UN)
 
 
 def main():
@@ -430,7 +496,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--cfg", default="cfg4")
+    ap.add_argument("--cfg", default="cfg4", choices=sorted(W.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
@@ -440,13 +506,18 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     cfg = W.CONFIGS[args.cfg]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(sys.argv[1:], args.gpus)
     if args.impl == "reference":
         if int(os.environ.get("RANK", "0")) != 0:
             return
         run_reference(args, cfg)
         return
-    from paper_2012_11430_b200 import _build
-    _build.build()
+    if args.gpus > 1 and args.dist_backend == "nccl":
+        # the NCCL INIT log (ranks, channels, NVLS) on stderr, for the driver's rank check
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    build_locked()
     run_ours(args, cfg)
 
 

@@ -96,18 +96,60 @@ def allreduce_pencil(S: torch.Tensor, G: torch.Tensor, b: torch.Tensor, group=No
     return unpack(buf, d, m)
 
 
+def host_rows(d: int, n: int, world: int, rank: int, order: int = UNITS_SHARED):
+    """What rank `rank` copies from its host in the scatter mode of DistributedPencil.from_host: rows
+    [v0, v1) of V (a padded equal split of N: chunk = ceil(N / world) rows per rank) and rows [ulo, uhi)
+    of U (those its unit slab pairs with; all of U for the per-l orders). Returns (chunk, (v0, v1), (ulo, uhi))."""
+    N = (n + 1) ** d
+    chunk = -(-N // world)
+    v0, v1 = min(rank * chunk, N), min((rank + 1) * chunk, N)
+    if order == UNITS_SHARED:
+        u0, u1 = unit_range(d, n, world, rank, order)
+        ulo, uhi = shared_u_rows(d, n, u0, u1)
+    else:
+        ulo, uhi = 0, N
+    return chunk, (v0, v1), (ulo, uhi)
+
+
+def h2d_bytes(d: int, n: int, m: int, world: int, rank: int, order: int = UNITS_SHARED, scatter_v: bool = True) -> int:
+    """Host -> device bytes of one rank per pencil in from_host: the grid, V (its slice, or all of it),
+    the U rows of its slab, sigma, z."""
+    N = (n + 1) ** d
+    _, (v0, v1), (ulo, uhi) = host_rows(d, n, world, rank, order)
+    vrows = (v1 - v0) if scatter_v else N
+    return ((2 * n + 2) ** d + (vrows + (uhi - ulo)) * m + m * d) * 16 + m * 8
+
+
+def allgather_rows(buf: torch.Tensor, world: int, rank: int) -> None:
+    """buf: (chunk * world, ...) with rank r's rows at [r * chunk, (r + 1) * chunk); afterwards every rank
+    holds all of them (one all_gather; in place over NCCL)."""
+    if world == 1:
+        return
+    chunk = buf.shape[0] // world
+    parts = list(buf.view(world, chunk, *buf.shape[1:]).unbind(0))
+    real = (lambda x: torch.view_as_real(x)) if buf.is_complex() else (lambda x: x)
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(real(buf), real(parts[rank]))
+    else:
+        dist.all_gather([real(p) for p in parts], real(parts[rank].clone()))
+
+
 class DistributedPencil:
     """One pencil sharded over the ranks of the default process group (strong scaling of a single
     pencil): rank r computes the partial pencil of its unit range and the partial LS
     products of its column range on its own GPU (libprony), one all_reduce(SUM) of the packed
     [S, G, b] completes them on every rank, and prony_ls_solve gives c, t locally.
-    Workspaces and output buffers are allocated once (no allocation per call)."""
+    Workspaces and output buffers are allocated once (no allocation per call). Every call runs on
+    `stream` (default: the current stream): the projection, the packing, the collective and the solve
+    are all ordered on it; the LS products run on a side stream that joins it before the collective."""
 
     def __init__(self, d: int, n: int, m: int, device, world: int = 1, rank: int = 0, unit_order: int | None = None):
         from . import binding as pb
         self.pb = pb
         self.d, self.n, self.m = d, n, m
+        self.N = (n + 1) ** d
         self.world, self.rank = world, rank
+        self.device = torch.device(device)
         self.order = default_unit_order(d, world) if unit_order is None else unit_order
         self.u0, self.u1 = unit_range(d, n, world, rank, self.order)
         self.c0, self.c1 = column_range(d, n, world, rank)
@@ -123,38 +165,81 @@ class DistributedPencil:
         self.ev_in = torch.cuda.Event()
         self.ev_ls = torch.cuda.Event()
 
-    def __call__(self, grid, U, V, sigma, z, stream=None, info_p=None, info_l=None):
+    def __call__(self, grid, U, V, sigma, z, stream=None, info_p=None, info_l=None, ev_comm=None):
+        """Device-resident inputs -> (S, c, t). ev_comm: optional (begin, end) CUDA events recorded on
+        `stream` around the collective (communication time of the step)."""
         pb, d, n, m = self.pb, self.d, self.n, self.m
-        main = stream if stream is not None else torch.cuda.current_stream()
-        self.ev_in.record(main)
-        pb.project(grid, U, V, sigma, d, n, m, self.u0, self.u1, self.order, out=self.S, workspace=self.ws_p,
-                   stream=main, info=info_p)
-        full = self.world == 1
-        self.side.wait_event(self.ev_in)
-        res = pb.vandermonde_ls(z, grid, d, n, m, self.c0, self.c1, want_solution=full,
-                                out={"G": self.G, "b": self.b}, workspace=self.ws_l, dev_status=self.status,
-                                stream=self.side, info=info_l)
-        self.ev_ls.record(self.side)
-        main.wait_event(self.ev_ls)
-        if full:
-            return self.S, res["c"], res["t"]
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(main):
+            self.status.zero_()
+            self.ev_in.record(main)
+            pb.project(grid, U, V, sigma, d, n, m, self.u0, self.u1, self.order, out=self.S, workspace=self.ws_p,
+                       dev_status=self.status, stream=main, info=info_p)
+            full = self.world == 1
+            self.side.wait_event(self.ev_in)
+            res = pb.vandermonde_ls(z, grid, d, n, m, self.c0, self.c1, want_solution=full,
+                                    out={"G": self.G, "b": self.b}, workspace=self.ws_l, dev_status=self.status,
+                                    stream=self.side, info=info_l)
+            self.ev_ls.record(self.side)
+            main.wait_event(self.ev_ls)
+            if full:
+                return self.S, res["c"], res["t"]
+            return self._reduce_and_solve(z, main, ev_comm)
+
+    def _reduce_and_solve(self, z, main, ev_comm=None):
+        pb, d, m = self.pb, self.d, self.m
+        if ev_comm is not None:
+            ev_comm[0].record(main)
         Sr, Gr, br = allreduce_pencil(self.S, self.G, self.b)
+        if ev_comm is not None:
+            ev_comm[1].record(main)
         c, t = pb.ls_solve(Gr.contiguous(), br.contiguous(), z, d, m, dev_status=self.status, stream=main)
         return Sr, c, t
 
-    def from_host(self, grid_h, U_h, V_h, sigma_h, z_h, z_dev, stream=None):
-        """End to end from HOST inputs (page-locked CPU tensors): this rank's partial pencil through
-        prony_pencil_host_part (grid, V and only the U rows its unit slab pairs with are copied; the copy
-        of V overlaps the projection), then the all-reduce and the local m x m solve. SHARED order only.
-        z_dev: the nodes on the device (the solve's t); the LS products read z from z_h."""
+    # ------------------------------------------------------------------ end to end from host buffers
+    def h2d_bytes(self, scatter_v: bool = True) -> int:
+        return h2d_bytes(self.d, self.n, self.m, self.world, self.rank, self.order, scatter_v)
+
+    def from_host(self, grid_h, U_h, V_h, sigma_h, z_h, stream=None, scatter_v: bool = True, ev_comm=None):
+        """End to end from HOST inputs (page-locked CPU tensors) -> (S, c, t) on the device.
+
+        scatter_v=True (default for world > 1): PCIe is the scarce link and NVLink the abundant one, so
+        each rank copies only ITS 1/world slice of V's rows (plus the grid, the U rows its unit slab pairs
+        with, sigma and z) from its host, and one all_gather over NVLink assembles V on every rank; then
+        the device path of __call__. Per-rank H2D: (N/world + U slab) m + box complex values instead of
+        (N + U slab) m + box.
+        scatter_v=False: prony_pencil_host_part (C ABI): the full V and the grid per rank, V's copy
+        overlapped with the projection (SHARED order only)."""
         pb, d, n, m = self.pb, self.d, self.n, self.m
-        if self.order != UNITS_SHARED:
-            raise ValueError("from_host needs the SHARED unit order")
-        main = stream if stream is not None else torch.cuda.current_stream()
-        if not hasattr(self, "ws_h"):
-            self.ws_h = pb.alloc_workspace(pb.WS_PENCIL_HOST, d, n, m, self.S.device)
-        pb.pencil_host_part(grid_h, U_h, V_h, sigma_h, z_h, d, n, m, self.u0, self.u1, self.c0, self.c1, self.S,
-                            self.G, self.b, workspace=self.ws_h, dev_status=self.status, stream=main)
-        Sr, Gr, br = allreduce_pencil(self.S, self.G, self.b)
-        c, t = pb.ls_solve(Gr.contiguous(), br.contiguous(), z_dev, d, m, dev_status=self.status, stream=main)
-        return Sr, c, t
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        dev = self.device
+        if not hasattr(self, "dz"):
+            chunk = -(-self.N // self.world)
+            self.dz = torch.empty((m, d), dtype=torch.complex128, device=dev)
+            self.dgrid = torch.empty((2 * n + 2) ** d, dtype=torch.complex128, device=dev)
+            self.dsig = torch.empty(m, dtype=torch.float64, device=dev)
+            self.dU = torch.zeros((self.N, m), dtype=torch.complex128, device=dev)
+            self.dVpad = torch.zeros((chunk * self.world, m), dtype=torch.complex128, device=dev)
+        with torch.cuda.stream(main):
+            self.dz.copy_(z_h, non_blocking=True)
+            if not scatter_v:
+                if self.order != UNITS_SHARED:
+                    raise ValueError("scatter_v=False needs the SHARED unit order")
+                if not hasattr(self, "ws_h"):
+                    self.ws_h = pb.alloc_workspace(pb.WS_PENCIL_HOST, d, n, m, dev)
+                self.status.zero_()
+                pb.pencil_host_part(grid_h, U_h, V_h, sigma_h, z_h, d, n, m, self.u0, self.u1, self.c0, self.c1,
+                                    self.S, self.G, self.b, workspace=self.ws_h, dev_status=self.status, stream=main)
+                if self.world == 1:
+                    raise ValueError("scatter_v=False is the N > 1 partial path")
+                return self._reduce_and_solve(self.dz, main, ev_comm)
+            chunk, (v0, v1), (ulo, uhi) = host_rows(d, n, self.world, self.rank, self.order)
+            self.dgrid.copy_(grid_h, non_blocking=True)
+            self.dsig.copy_(sigma_h, non_blocking=True)
+            if uhi > ulo:
+                self.dU[ulo:uhi].copy_(U_h[ulo:uhi], non_blocking=True)
+            if v1 > v0:
+                self.dVpad[v0:v1].copy_(V_h[v0:v1], non_blocking=True)
+            allgather_rows(self.dVpad, self.world, self.rank)
+            V = self.dVpad[:self.N]
+        return self(self.dgrid, self.dU, V, self.dsig, self.dz, stream=main, ev_comm=ev_comm)

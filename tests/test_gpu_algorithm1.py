@@ -110,10 +110,16 @@ def test_build_pencil_svd_vs_oracle(pb, orc, d, n, m, noise):
     s = out["sigma"].cpu().numpy()
     U = out["U"].cpu().numpy()
     V = out["V"].cpu().numpy()
-    for s_or, U_or, V_or in ((s_j, U_j, V_j), (bp["sigma"], bp["U"], bp["V"])):
+    # sigma against both oracle routes; the subspaces against the exact (Jacobi) SVD to 1e-8. The oracle's
+    # Alg. 3 stops once ||R_k||_F <= tol ||T||_F, so on noisy data (tol = 1e-6) its own subspaces
+    # are only that close to the exact ones: it is held to 1e2 tol there.
+    for s_or in (s_j, bp["sigma"]):
         assert np.max(np.abs(s - s_or) / s_or[0]) <= 1e-10
-        assert np.linalg.norm(proj(U) - proj(U_or)) <= 1e-8 * max(1.0, noise * 1e4)
-        assert np.linalg.norm(proj(V) - proj(V_or)) <= 1e-8 * max(1.0, noise * 1e4)
+    assert np.linalg.norm(proj(U) - proj(U_j)) <= 1e-8
+    assert np.linalg.norm(proj(V) - proj(V_j)) <= 1e-8
+    bp_tol = 1e-8 if noise == 0.0 else 1e2 * tol
+    assert np.linalg.norm(proj(bp["U"]) - proj(U_j)) <= bp_tol
+    assert np.linalg.norm(proj(bp["V"]) - proj(V_j)) <= bp_tol
     np.testing.assert_allclose(U.conj().T @ U, np.eye(m), atol=1e-12)
     S_or = orc.project(prob.grid, U, V, s, d, n)
     S = out["S"].cpu().numpy()
@@ -215,8 +221,8 @@ def table(orc):
 @pytest.mark.parametrize("i", [0, 1, 2, 3])
 def test_accuracy_table_row_vs_oracle(pb, orc, table, i):
     """One row of Table tab_accuracy (eps = 0, 1e-9, 1e-6, 1e-3): device vs oracle on the same grid (rank,
-    t, c, residual), and the device's errors against the printed row (x5 noisy; noise-free at roundoff:
-    t, c x5, residual x20, as the oracle's own pin in test_oracle_alg1_pins.py)."""
+    t, c, residual), and the device's errors against the printed row: within x5 for the noisy rows; the
+    noise-free row is roundoff, so only bounded above (t, c x5, residual x20, as the oracle's own pin)."""
     d, n, m, t_pl, c_pl, mu, rows = table
     row, eps, tol, grid, oc = rows[i]
     dv = device_algorithm1(pb, orc, grid, d, n, m, tol, mu)
@@ -226,7 +232,9 @@ def test_accuracy_table_row_vs_oracle(pb, orc, table, i):
     errs = (dv["resid"], W.torus_dist_inf(dv["t"][perm], t_pl).max(), rel(dv["c"][perm], c_pl))
     bands = (20.0, 5.0, 5.0) if eps == 0.0 else (5.0, 5.0, 5.0)
     for got, paper, b in zip(errs, row[2:], bands):
-        assert paper / b < got < paper * b, (eps, errs, row)
+        assert got < paper * b, (eps, errs, row)
+        if eps > 0:
+            assert paper / b < got, (eps, errs, row)
 
 
 def test_accuracy_table_rank_anomaly(pb, orc, table):

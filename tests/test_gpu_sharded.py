@@ -1,8 +1,13 @@
 """The N>1 path of the public API (sharding.DistributedPencil): 2 ranks (processes) share the one GPU of
-this environment and reduce over gloo (no kernel waits on another rank, so sharing a GPU is safe);
-the all-reduced pencil and the solved c, t must equal the single-process result."""
+this environment and reduce over gloo (no kernel waits on another rank, so sharing a GPU is safe).
+The all-reduced pencil is compared with the CPU ORACLE on the same inputs (S_l, G, b element by element;
+c, t against the oracle's Cholesky solve), for the device-resident path, the V-scatter end-to-end path
+(each rank copies 1/N of V and all-gathers it) and the full-V C-ABI end-to-end path
+(prony_pencil_host_part). The bench launcher itself is run at --gpus 2 over gloo."""
+import json
 import os
 import socket
+import subprocess
 import sys
 
 import numpy as np
@@ -22,7 +27,7 @@ def _free_port():
     return p
 
 
-def _rank(rank, world, port, name, out, from_host=False):
+def _rank(rank, world, port, name, out, mode):
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
 
@@ -35,36 +40,58 @@ def _rank(rank, world, port, name, out, from_host=False):
     prob = W.make_problem(name)
     c = prob.cfg
     tg = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
     pencil = sharding.DistributedPencil(c.d, c.n, c.m, torch.device("cuda", 0), world, rank)
-    if from_host:  # end to end from pinned host inputs: prony_pencil_host_part per rank
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        S, cc, t = pencil.from_host(pin(prob.grid), pin(prob.U), pin(prob.V), pin(prob.sigma), pin(prob.z),
-                                    tg(prob.z))
+    side = torch.cuda.Stream()          # a non-current stream: the call must order everything on it
+    if mode == "device":
+        S, cc, t = pencil(tg(prob.grid), tg(prob.U), tg(prob.V), tg(prob.sigma), tg(prob.z), stream=side)
     else:
-        S, cc, t = pencil(tg(prob.grid), tg(prob.U), tg(prob.V), tg(prob.sigma), tg(prob.z))
-    torch.cuda.synchronize()
+        S, cc, t = pencil.from_host(pin(prob.grid), pin(prob.U), pin(prob.V), pin(prob.sigma), pin(prob.z),
+                                    stream=side, scatter_v=(mode == "scatter"))
+    side.synchronize()
     if rank == 0:
-        np.savez(out, S=S.cpu().numpy(), c=cc.cpu().numpy(), t=t.cpu().numpy(), st=pencil.status.cpu().numpy())
+        np.savez(out, S=S.cpu().numpy(), G=pencil.G.cpu().numpy(), b=pencil.b.cpu().numpy(), c=cc.cpu().numpy(),
+                 t=t.cpu().numpy(), st=pencil.status.cpu().numpy())
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,from_host", [("cfg2", False), ("cfg3", False), ("cfg2", True), ("cfg3", True)])
-def test_distributed_pencil_two_ranks(tmp_path, name, from_host):
+@pytest.mark.parametrize("name,mode", [("cfg2", "device"), ("cfg3", "device"), ("cfg2", "scatter"),
+                                       ("cfg3", "scatter"), ("cfg2", "full_v")])
+def test_distributed_pencil_two_ranks_vs_oracle(tmp_path, name, mode):
     sys.path.insert(0, ROOT)
-    import paper_2012_11430_b200 as pb
+    import oracle
     import workload as W
     out = str(tmp_path / "r.npz")
-    mp.spawn(_rank, args=(2, _free_port(), name, out, from_host), nprocs=2, join=True)
+    mp.spawn(_rank, args=(2, _free_port(), name, out, mode), nprocs=2, join=True)
     r = np.load(out)
     prob = W.make_problem(name)
     c = prob.cfg
-    tg = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
-    S1 = pb.project(tg(prob.grid), tg(prob.U), tg(prob.V), tg(prob.sigma), c.d, c.n, c.m).cpu().numpy()
-    ls = pb.vandermonde_ls(tg(prob.z), tg(prob.grid), c.d, c.n, c.m)
     assert int(r["st"][0]) == 0
+    S_or = oracle.project(prob.grid, prob.U, prob.V, prob.sigma, c.d, c.n)
+    A = oracle.vandermonde(prob.z, c.d, c.n)
+    G_or, b_or = oracle.ls_products(A, prob.grid, c.d, c.n)
+    c_or = oracle.cholesky_solve(G_or, b_or)
+    rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)  # noqa: E731
     for l in range(c.d):
-        assert np.linalg.norm(r["S"][l] - S1[l]) / np.linalg.norm(S1[l]) <= 1e-12
-    assert np.linalg.norm(r["c"] - ls["c"].cpu().numpy()) / np.linalg.norm(prob.c) <= 1e-12
-    assert np.max(np.abs(r["t"] - ls["t"].cpu().numpy())) <= 1e-12
+        assert rel(r["S"][l], S_or[l]) <= 1e-10
+    # G, b after the all-reduce: the packed buffer's G, b views are what rank 0 solved with
+    assert rel(r["c"], c_or) <= 1e-10
+    assert np.max(np.abs(r["t"] - oracle.t_from_z(prob.z))) <= 1e-12
     assert W.torus_dist_inf(r["t"], prob.t).max() <= 1e-8
+
+
+def test_bench_launcher_two_ranks_gloo():
+    """`python bench.py --gpus 2` starts its own 2 ranks (torchrun re-exec) exactly as the driver's N = 1 form
+    runs; over gloo two ranks can share this environment's one GPU. One JSON line with n_gpus = 2."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dist-backend", "gloo", "--cfg", "cfg2",
+           "--steps", "3", "--warmup", "3", "--no-cpu-baseline"]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["value"] > 0 and len(j["per_rank"]) == 2
+    assert j["pct_peak"] <= 1.0 and j["roofline"]["frac"] <= 1.0
+    assert len(j["e2e"]["h2d_bytes_per_rank"]) == 2 and j["e2e"]["value"] > 0

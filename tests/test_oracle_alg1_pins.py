@@ -328,8 +328,8 @@ def _errors(oracle_mod, out, t, c):
 
 def test_algorithm1_accuracy_table(oracle_mod, table_runs):
     """Noisy rows (eps = 1e-9, 1e-6, 1e-3): residual, t error and c error within x5 of the printed values.
-    Noise-free row: at roundoff (t and c within x5 of the printed values; the residual within x20 — it is
-    the n^d-fold amplification of the ~5e-15 node error through the powers z^k)."""
+    Noise-free row: roundoff, bounded above only (t and c below x5 of the printed values; the residual below
+    x20 — it is the amplification of the ~5e-15 node error through the powers z^k, |k| up to d n = 60)."""
     t, c, runs = table_runs
     for eps in (0.0, 1e-9, 1e-6, 1e-3):
         row, out = runs[eps]
@@ -337,7 +337,9 @@ def test_algorithm1_accuracy_table(oracle_mod, table_runs):
         got = _errors(oracle_mod, out, t, c)
         bands = (20.0, 5.0, 5.0) if eps == 0.0 else (5.0, 5.0, 5.0)
         for g, p, b in zip(got, row[2:], bands):
-            assert p / b < g < p * b, (eps, got, row)
+            assert g < p * b, (eps, got, row)
+            if eps > 0:                    # the noise-free row is roundoff: bounded above only
+                assert p / b < g, (eps, got, row)
         assert np.max(out["offdiag"]) < (1e-10 if eps == 0 else 100 * eps)
 
 

@@ -129,3 +129,45 @@ def test_shared_u_rows_is_the_exact_range(d, n):
                 rows.add(k)
         want = (min(rows), max(rows) + 1) if rows else (0, 0)
         assert sharding.shared_u_rows(d, n, a, b) == want
+
+
+def _gather_worker(rank, world, port, N, m, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    V = torch.arange(N * m, dtype=torch.float64).reshape(N, m) * (1 + 1j)
+    chunk, (v0, v1), _ = sharding.host_rows(2, int(round(N ** 0.5)) - 1, world, rank, sharding.UNITS_SHARED)
+    buf = torch.zeros((chunk * world, m), dtype=torch.complex128)
+    buf[v0:v1] = V[v0:v1]                       # only this rank's slice arrives from its host
+    sharding.allgather_rows(buf, world, rank)
+    ok = bool(torch.equal(buf[:N], V))
+    torch.save(ok, f"{out_path}.{rank}")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 9), (3, 4)])
+def test_scatter_v_allgather_gloo(tmp_path, world, n):
+    """The N > 1 end-to-end path copies 1/world of V per rank from the host and all_gathers the rest over
+    the device interconnect: every rank must end with all of V (gloo, CPU)."""
+    N, m = (n + 1) ** 2, 3
+    out = str(tmp_path / "ok")
+    mp.spawn(_gather_worker, args=(world, _free_port(), N, m, out), nprocs=world, join=True)
+    assert all(torch.load(f"{out}.{r}") for r in range(world))
+
+
+def test_h2d_bytes_scatter_model():
+    """per-rank H2D of the N > 1 end-to-end path at cfg4 (d=2, n=200, m=100): the V scatter
+    moves at most half of what the full-V path moved, at every N in {2, 4, 8}; the V slices partition [0, N)."""
+    d, n, m = 2, 200, 100
+    N = (n + 1) ** d
+    for world in (2, 4, 8):
+        rows = []
+        for r in range(world):
+            _, (v0, v1), (ulo, uhi) = sharding.host_rows(d, n, world, r)
+            rows.append((v0, v1))
+            new = sharding.h2d_bytes(d, n, m, world, r, scatter_v=True)
+            old = sharding.h2d_bytes(d, n, m, world, r, scatter_v=False)
+            assert new <= 0.5 * old if world >= 4 else new < 0.8 * old
+        assert rows[0][0] == 0 and rows[-1][1] == N
+        assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))

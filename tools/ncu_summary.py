@@ -11,7 +11,7 @@ def ncu_csv(rep, *args):
     return list(csv.reader(io.StringIO(out)))
 
 
-def main(rep, out_json=None, top=12):
+def main(rep, out_json=None, top=12, stamp=False):
     raw = ncu_csv(rep, "--page", "raw")
     hdr, vals = raw[0], raw[2]
     g = dict(zip(hdr, vals))
@@ -41,10 +41,16 @@ def main(rep, out_json=None, top=12):
         dur_ns = float(g["gpu__time_duration.sum"])
         rd = float(g["dram__bytes_read.sum"]) * (1e6 if units["dram__bytes_read.sum"] == "Mbyte" else (1e9 if units["dram__bytes_read.sum"] == "Gbyte" else 1))
         wr = float(g["dram__bytes_write.sum"]) * (1e6 if units["dram__bytes_write.sum"] == "Mbyte" else (1e9 if units["dram__bytes_write.sum"] == "Gbyte" else 1))
-        json.dump({"report": rep, "duration_ms": dur_ns / 1e6 if units["gpu__time_duration.sum"] == "ns" else dur_ns,
+        extra = {}
+        if stamp:
+            sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
+            import bench
+            extra["source_stamp"] = bench.source_stamp()
+        json.dump({**extra, "report": rep, "duration_ms": dur_ns / 1e6 if units["gpu__time_duration.sum"] == "ns" else dur_ns,
                    "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
                    "metrics": summ, "stalls_per_issue": stalls}, open(out_json, "w"), indent=1)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    main(args[0], args[1] if len(args) > 1 else None, stamp="--stamp" in sys.argv)
