@@ -69,7 +69,8 @@
 extern "C" {
 #endif
 
-#define PRONY_ABI_VERSION 3  /* 2: PRONY_UNITS_SHARED, prony_lanczos_svd, PRONY_WS_LANCZOS; 3: prony_pencil_host_part */
+#define PRONY_ABI_VERSION 4  /* 2: PRONY_UNITS_SHARED, prony_lanczos_svd, PRONY_WS_LANCZOS; 3: prony_pencil_host_part;
+                                 4: prony_host_context, prony_pencil_host_ctx, prony_pencil_host_part_ctx */
 #define PRONY_MAX_D 8
 #define PRONY_MAX_M 128
 
@@ -80,6 +81,8 @@ typedef struct prony_c128 {
 
 /* cudaStream_t without including the CUDA headers */
 typedef struct CUstream_st* prony_stream_t;
+/* opaque: the side streams and events of the host-input pencil, created once (prony_host_context_create) */
+typedef struct prony_host_context_s* prony_host_context;
 
 typedef enum prony_status {
   PRONY_OK = 0,
@@ -246,10 +249,10 @@ int prony_toeplitz_apply(int d, int n, const prony_c128* grid, int ell, int conj
 /*
  * prony_pencil_host — one full pencil (prony_project over all SHARED units + prony_vandermonde_ls over
  * [0, N), c and t included) from HOST inputs to HOST outputs, synchronizing `stream` at the end. Only
- * the grid and the V rows of split-K chunk 0 are copied before the first DMMA: two streams created
- * and destroyed by the call (ordered after prior work on `stream`) carry the rest of V with the
- * remaining chunks of the projection, then U (first needed by the final reduction), and z with the LS
- * step. Host buffers should be page-locked for full PCIe bandwidth (not required).
+ * the grid and the V rows of split-K chunk 0 are copied before the first DMMA: three side streams
+ * (created and destroyed by the call, or taken from a prony_host_context, ordered after prior work on
+ * `stream`) carry the rest of V with the remaining chunks of the projection, U after V on its own
+ * stream (first needed by the final reduction), and z with the LS step. Host buffers should be page-locked for full PCIe bandwidth (not required).
  *   host inputs : grid (L^d), U, V (N x m), sigma (m), z (m x d)
  *   host outputs: S (d x m x m), G (m x m), b (m), c (m), t (m x d); any output may be NULL
  *   workspace   : DEVICE scratch >= prony_workspace_size(PRONY_WS_PENCIL_HOST)
@@ -260,6 +263,32 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
                       const double* sigma, const prony_c128* z, prony_c128* S, prony_c128* G, prony_c128* b,
                       prony_c128* c, double* t, void* workspace, size_t workspace_bytes, int32_t* status_out,
                       prony_stream_t stream);
+
+/*
+ * prony_host_context_create / _destroy — an explicit context for the host-input pencil: the three side
+ * streams and eight events prony_pencil_host* would otherwise create and destroy on every call (tens of
+ * microseconds of host time, visible on small pencils). Owned by the caller; bound to the device current
+ * at creation (a call on another device returns PRONY_ERR_INVALID); one context serves one call at a time
+ * (calls sharing a context must be ordered on the same `stream`). _destroy synchronizes its streams.
+ * Returns PRONY_OK, PRONY_ERR_INVALID (null out / ctx) or PRONY_ERR_CUDA.
+ */
+int prony_host_context_create(prony_host_context* ctx_out);
+int prony_host_context_destroy(prony_host_context ctx);
+
+/*
+ * prony_pencil_host_ctx / prony_pencil_host_part_ctx — prony_pencil_host / prony_pencil_host_part with the
+ * side streams and events taken from `ctx` (NULL: created for the call, as the plain entry points do).
+ * Same arguments, results and errors otherwise.
+ */
+int prony_pencil_host_ctx(prony_host_context ctx, int d, int n, int m, const prony_c128* grid, const prony_c128* U,
+                          const prony_c128* V, const double* sigma, const prony_c128* z, prony_c128* S, prony_c128* G,
+                          prony_c128* b, prony_c128* c, double* t, void* workspace, size_t workspace_bytes,
+                          int32_t* status_out, prony_stream_t stream);
+int prony_pencil_host_part_ctx(prony_host_context ctx, int d, int n, int m, const prony_c128* grid,
+                               const prony_c128* U, const prony_c128* V, const double* sigma, const prony_c128* z,
+                               int64_t unit_begin, int64_t unit_end, int64_t col_begin, int64_t col_end, prony_c128* S,
+                               prony_c128* G, prony_c128* b, void* workspace, size_t workspace_bytes,
+                               int32_t* dev_status, prony_stream_t stream);
 
 /*
  * prony_pencil_host_part — one rank's share of a pencil from HOST inputs (multi-GPU end to end, P:259-267

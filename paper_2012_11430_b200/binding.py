@@ -31,7 +31,8 @@ MAX_D, MAX_M = 8, 128
 EXPORTS = ("prony_abi_version", "prony_status_string", "prony_device_info", "prony_workspace_size",
            "prony_project", "prony_project_ex", "prony_vandermonde_ls", "prony_vandermonde_ls_ex", "prony_ls_solve",
            "prony_toeplitz_apply", "prony_pencil_host", "prony_build_pencil", "prony_diagonalize",
-           "prony_project_mu", "prony_lanczos_svd", "prony_pencil_host_part")
+           "prony_project_mu", "prony_lanczos_svd", "prony_pencil_host_part", "prony_host_context_create",
+           "prony_host_context_destroy", "prony_pencil_host_ctx", "prony_pencil_host_part_ctx")
 
 
 class ExecInfo(ctypes.Structure):
@@ -86,9 +87,14 @@ def lib() -> ctypes.CDLL:
                                              vp, vp]
         L.prony_lanczos_svd.argtypes = [i32, i32, vp, i32, ctypes.c_double, ctypes.c_uint64, i32, vp, vp, vp, vp, vp,
                                         vp, sz, vp]
+        L.prony_host_context_create.argtypes = [ctypes.POINTER(vp)]
+        L.prony_host_context_destroy.argtypes = [vp]
+        L.prony_pencil_host_ctx.argtypes = [vp] + L.prony_pencil_host.argtypes
+        L.prony_pencil_host_part_ctx.argtypes = [vp] + L.prony_pencil_host_part.argtypes
         for f in ("prony_device_info", "prony_workspace_size", "prony_project", "prony_vandermonde_ls", "prony_ls_solve",
                   "prony_project_ex", "prony_vandermonde_ls_ex", "prony_toeplitz_apply", "prony_diagonalize",
-                  "prony_project_mu",
+                  "prony_project_mu", "prony_pencil_host_part", "prony_lanczos_svd", "prony_host_context_create",
+                  "prony_host_context_destroy", "prony_pencil_host_ctx", "prony_pencil_host_part_ctx",
                   "prony_pencil_host", "prony_build_pencil"):
             getattr(L, f).restype = i32
         _lib = L
@@ -214,14 +220,21 @@ def vandermonde_ls(z, grid, d: int, n: int, m: int, col_begin: int = 0, col_end:
     return res
 
 
-def ls_solve(G, b, z, d: int, m: int, want_t: bool = True, workspace=None, dev_status=None, stream=None):
-    """c = conj(G^-1 b) (Cholesky) and t = (-arg z/2pi) mod 1 for already-reduced G, b."""
+def ls_solve(G, b, z, d: int, m: int, want_t: bool = True, workspace=None, dev_status=None, stream=None, out=None):
+    """c = conj(G^-1 b) (Cholesky) and t = (-arg z/2pi) mod 1 for already-reduced G, b.
+    out: optional dict with preallocated "c" (m,) complex128 / "t" (m, d) float64 device tensors."""
     _dev_tensor(G, torch.complex128, "G")
     _dev_tensor(b, torch.complex128, "b")
     _dev_tensor(z, torch.complex128, "z")
     dev = G.device
-    c = torch.empty(m, dtype=torch.complex128, device=dev)
-    t = torch.empty((m, d), dtype=torch.float64, device=dev) if want_t else None
+    out = out or {}
+    c = out.get("c")
+    if c is None:
+        c = torch.empty(m, dtype=torch.complex128, device=dev)
+    _dev_tensor(c, torch.complex128, "c")
+    t = out.get("t") if want_t else None
+    if want_t and t is None:
+        t = torch.empty((m, d), dtype=torch.float64, device=dev)
     if workspace is None:
         workspace = torch.empty(m * m * 16 + m * 16 + 512, dtype=torch.uint8, device=dev)
     rc = lib().prony_ls_solve(d, m, _ptr(G), _ptr(b), _ptr(z), _ptr(c), _ptr(t), _ptr(workspace), workspace.numel(),
@@ -263,9 +276,32 @@ def toeplitz_apply(grid, X, d: int, n: int, ell: int = 0, conj: bool = False, ou
     return out
 
 
-def pencil_host(grid, U, V, sigma, z, d: int, n: int, m: int, workspace=None, outputs=None, stream=None):
+class HostContext:
+    """prony_host_context: the side streams / events of the host-input pencil, created once on the current
+    device and reused by pencil_host / pencil_host_part calls that pass it (destroyed with the object)."""
+
+    def __init__(self):
+        h = ctypes.c_void_p()
+        _check(lib().prony_host_context_create(ctypes.byref(h)), "prony_host_context_create")
+        self.handle = h
+
+    def close(self):
+        if self.handle is not None and self.handle.value:
+            _check(lib().prony_host_context_destroy(self.handle), "prony_host_context_destroy")
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def pencil_host(grid, U, V, sigma, z, d: int, n: int, m: int, workspace=None, outputs=None, stream=None,
+                context: HostContext | None = None):
     """Full pencil from HOST (numpy or pinned CPU torch) buffers: H2D copies, prony_project over
-    [0, dN), prony_vandermonde_ls over [0, N), D2H copies, stream sync. Returns dict of host arrays."""
+    [0, dN), prony_vandermonde_ls over [0, N), D2H copies, stream sync. Returns dict of host arrays.
+    context: a HostContext whose streams / events the call reuses (None: created per call)."""
     import numpy as np
 
     def host_ptr(a):
@@ -282,7 +318,8 @@ def pencil_host(grid, U, V, sigma, z, d: int, n: int, m: int, workspace=None, ou
     if workspace is None:
         workspace = alloc_workspace(WS_PENCIL_HOST, d, n, m)
     st = ctypes.c_int32(0)
-    rc = lib().prony_pencil_host(d, n, m, host_ptr(grid), host_ptr(U), host_ptr(V), host_ptr(sigma), host_ptr(z),
+    rc = lib().prony_pencil_host_ctx(None if context is None else context.handle, d, n, m, host_ptr(grid), host_ptr(U),
+                                     host_ptr(V), host_ptr(sigma), host_ptr(z),
                                  host_ptr(outputs["S"]), host_ptr(outputs["G"]), host_ptr(outputs["b"]),
                                  host_ptr(outputs["c"]), host_ptr(outputs["t"]), _ptr(workspace), workspace.numel(),
                                  ctypes.byref(st), _stream(stream))
@@ -292,7 +329,8 @@ def pencil_host(grid, U, V, sigma, z, d: int, n: int, m: int, workspace=None, ou
 
 
 def pencil_host_part(grid, U, V, sigma, z, d: int, n: int, m: int, unit_begin: int, unit_end: int, col_begin: int,
-                     col_end: int, S, G, b, workspace=None, dev_status=None, stream=None):
+                     col_end: int, S, G, b, workspace=None, dev_status=None, stream=None,
+                     context: HostContext | None = None):
     """One rank's partial pencil from HOST inputs (pinned CPU torch tensors for overlap): SHARED units
     [unit_begin, unit_end), LS columns [col_begin, col_end); partial S, G, b land in the given DEVICE
     tensors. Asynchronous on `stream`."""
@@ -305,7 +343,8 @@ def pencil_host_part(grid, U, V, sigma, z, d: int, n: int, m: int, unit_begin: i
         _dev_tensor(x, torch.complex128, name)
     if workspace is None:
         workspace = alloc_workspace(WS_PENCIL_HOST, d, n, m, S.device)
-    rc = lib().prony_pencil_host_part(d, n, m, host_ptr(grid), host_ptr(U), host_ptr(V), host_ptr(sigma), host_ptr(z),
+    rc = lib().prony_pencil_host_part_ctx(None if context is None else context.handle, d, n, m, host_ptr(grid),
+                                          host_ptr(U), host_ptr(V), host_ptr(sigma), host_ptr(z),
                                       int(unit_begin), int(unit_end), int(col_begin), int(col_end), _ptr(S), _ptr(G),
                                       _ptr(b), _ptr(workspace), workspace.numel(), _ptr(dev_status), _stream(stream))
     _check(rc, "prony_pencil_host_part")

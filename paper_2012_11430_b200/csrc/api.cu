@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <climits>
 #include <cstring>
+#include <new>
 
 #include "../../include/prony.h"
 #include "common.cuh"
@@ -143,6 +144,12 @@ int prony_device_info(int* sm_count, int* cc_major, int* cc_minor) {
 int prony_workspace_size(int kind, int d, int n, int m, size_t* bytes) {
   if (!bytes) return PRONY_ERR_INVALID;
   int64_t N = 0;
+  if (kind == PRONY_WS_DIAG) {  // the diagonalization does not depend on n: only d and m are checked
+    if (d < 1 || d > PRONY_MAX_D || m < 1) return PRONY_ERR_INVALID;
+    if (m > PRONY_MAX_M) return PRONY_ERR_RANGE;
+    *bytes = diag_workspace_bytes(d, m);
+    return PRONY_OK;
+  }
   if (kind == PRONY_WS_LANCZOS) {
     const int rc = validate_dnm(d, n, 1, &N);
     if (rc) return rc;
@@ -161,7 +168,6 @@ int prony_workspace_size(int kind, int d, int n, int m, size_t* bytes) {
     case PRONY_WS_BUILD:
       *bytes = std::max(svd_workspace_bytes(d, n, (int)N, m), ws_project(d, n, N, m, sms));
       return PRONY_OK;
-    case PRONY_WS_DIAG: *bytes = diag_workspace_bytes(d, m); return PRONY_OK;
     case PRONY_WS_PROJECT_MU: *bytes = ws_project_mu(d, n, N, m, sms); return PRONY_OK;
     case PRONY_WS_APPLY: *bytes = apply_workspace_bytes(d, n, (int)N); return PRONY_OK;
     default: return PRONY_ERR_INVALID;
@@ -342,15 +348,55 @@ void shared_u_rows(int d, int n, int64_t e0, int64_t e1, int64_t* lo, int64_t* h
   if (*hi < 0) *lo = *hi = 0;
 }
 
-// Host-input pencil on the device (prony_pencil_host / prony_pencil_host_part). Streams created for
-// this call only: `st` carries grid, the V rows of split-K chunk 0 and sigma -> k_prep -> chunk 0 of
-// the projection; `s2` carries the rest of V (after chunk 0's rows: the link is not shared) -> its Vsum
-// rows -> chunks 1..KC-1, then the U rows (needed only by k_reduce); `s3` carries z -> the LS step. So
-// only chunk 0's V rows are copied before the first DMMA. On return `st` is ordered after everything.
+}  // namespace
+
+// Streams and events of the host-input pencil (prony_pencil_host*): created once by
+// prony_host_context_create and reused by every call that passes the context, or created and destroyed by
+// a call that passes none.
+struct prony_host_context_s {
+  int device = -1;
+  cudaStream_t s2 = nullptr, s3 = nullptr, s4 = nullptr;
+  cudaEvent_t ev[8] = {};  // in, grid, v0, u, done, split a, split b, v rest
+};
+
+namespace {
+
+void host_ctx_release(prony_host_context_s* c) {
+  for (cudaEvent_t& e : c->ev)
+    if (e) {
+      cudaEventDestroy(e);
+      e = nullptr;
+    }
+  for (cudaStream_t* s : {&c->s2, &c->s3, &c->s4})
+    if (*s) {
+      cudaStreamDestroy(*s);
+      *s = nullptr;
+    }
+}
+
+int host_ctx_init(prony_host_context_s* c) {
+  if (cudaGetDevice(&c->device) != cudaSuccess) return PRONY_ERR_CUDA;
+  bool good = cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&c->s3, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&c->s4, cudaStreamNonBlocking) == cudaSuccess;
+  for (int i = 0; i < 8 && good; ++i) good = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!good) {
+    host_ctx_release(c);
+    return PRONY_ERR_CUDA;
+  }
+  return PRONY_OK;
+}
+
+// Host-input pencil on the device (prony_pencil_host / prony_pencil_host_part). `st` carries grid, the
+// V rows of split-K chunk 0 and sigma -> k_prep -> chunk 0 of the projection; `s2` carries the rest of V
+// (after chunk 0's rows: the link is not shared) -> its Vsum rows -> chunks 1..KC-1; `s4` carries the U rows
+// after the rest of V (needed only by k_reduce, so the chunks on s2 never wait for them); `s3` carries z ->
+// the LS step. So only chunk 0's V rows are copied before the first DMMA. On return `st` is ordered after
+// everything. The streams / events come from `ctx` (a caller's context) or are created for this call.
 int host_pencil(int d, int n, int m, int64_t N, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
                 const double* sigma, const prony_c128* z, int64_t e0, int64_t e1, int64_t c0, int64_t c1, bool solve,
                 double2* S_dev, double2* G_dev, double2* b_dev, double2* c_dev, double* t_dev, int32_t* dst,
-                char* w, const HostLayout& h, int sms, cudaStream_t st) {
+                char* w, const HostLayout& h, int sms, cudaStream_t st, prony_host_context_s* ctx) {
   int64_t box = 1;
   for (int i = 0; i < d; ++i) box *= (2 * (int64_t)n + 2);
   ProjGeom g{};
@@ -365,58 +411,58 @@ int host_pencil(int d, int n, int m, int64_t N, const prony_c128* grid, const pr
   const int64_t v0 = split ? std::min<int64_t>(pl.chunk_w, N) : N;
   int64_t ulo = 0, uhi = N;
   if (e0 != 0 || e1 != ext_rows(d, n)) shared_u_rows(d, n, e0, e1, &ulo, &uhi);
-  cudaStream_t s2 = nullptr, s3 = nullptr;
-  cudaEvent_t ev[7] = {};  // in, grid, v0, u, done, split a, split b
-  auto cleanup = [&]() {
-    for (cudaEvent_t e : ev)
-      if (e) cudaEventDestroy(e);
-    if (s2) cudaStreamDestroy(s2);
-    if (s3) cudaStreamDestroy(s3);
-  };
-  bool good = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) == cudaSuccess &&
-              cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking) == cudaSuccess;
-  for (int i = 0; i < 7 && good; ++i) good = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) == cudaSuccess;
-  if (!good) {
-    cleanup();
-    return PRONY_ERR_CUDA;
+  prony_host_context_s local;
+  const bool own = ctx == nullptr;
+  if (own) {
+    if (host_ctx_init(&local) != PRONY_OK) return PRONY_ERR_CUDA;
+    ctx = &local;
+  } else {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return PRONY_ERR_CUDA;
+    if (dev != ctx->device) return PRONY_ERR_INVALID;
   }
-  cudaEvent_t ev_in = ev[0], ev_grid = ev[1], ev_v0 = ev[2], ev_u = ev[3], ev_done = ev[4];
+  cudaStream_t s2 = ctx->s2, s3 = ctx->s3, s4 = ctx->s4;
+  cudaEvent_t* ev = ctx->ev;
+  cudaEvent_t ev_in = ev[0], ev_grid = ev[1], ev_v0 = ev[2], ev_u = ev[3], ev_done = ev[4], ev_vrest = ev[7];
   auto ok = [](cudaError_t e) { return e == cudaSuccess; };
   const size_t vrow = (size_t)m * sizeof(double2);
-  good = ok(cudaEventRecord(ev_in, st)) && ok(cudaStreamWaitEvent(s2, ev_in, 0)) &&
-         ok(cudaStreamWaitEvent(s3, ev_in, 0)) &&
-         ok(cudaMemcpyAsync(w + h.grid, grid, box * sizeof(double2), cudaMemcpyHostToDevice, st)) &&
-         ok(cudaEventRecord(ev_grid, st)) &&
-         ok(cudaMemcpyAsync(w + h.V, V, v0 * vrow, cudaMemcpyHostToDevice, st)) &&
-         ok(cudaMemcpyAsync(w + h.sigma, sigma, m * sizeof(double), cudaMemcpyHostToDevice, st)) &&
-         ok(cudaEventRecord(ev_v0, st)) && ok(cudaStreamWaitEvent(s2, ev_v0, 0)) &&
-         (v0 == N || ok(cudaMemcpyAsync(w + h.V + v0 * vrow, (const char*)V + v0 * vrow, (N - v0) * vrow,
-                                        cudaMemcpyHostToDevice, s2))) &&
-         (uhi <= ulo || ok(cudaMemcpyAsync(w + h.U + ulo * vrow, (const char*)U + ulo * vrow, (uhi - ulo) * vrow,
-                                           cudaMemcpyHostToDevice, s2))) &&
-         ok(cudaEventRecord(ev_u, s2)) && ok(cudaStreamWaitEvent(s3, ev_grid, 0)) &&
-         ok(cudaMemcpyAsync(w + h.z, z, (size_t)m * d * sizeof(double2), cudaMemcpyHostToDevice, s3));
-  if (!good) {
-    cleanup();
-    return PRONY_ERR_CUDA;
+  bool good = ok(cudaEventRecord(ev_in, st)) && ok(cudaStreamWaitEvent(s2, ev_in, 0)) &&
+              ok(cudaStreamWaitEvent(s3, ev_in, 0)) &&
+              ok(cudaMemcpyAsync(w + h.grid, grid, box * sizeof(double2), cudaMemcpyHostToDevice, st)) &&
+              ok(cudaEventRecord(ev_grid, st)) &&
+              ok(cudaMemcpyAsync(w + h.V, V, v0 * vrow, cudaMemcpyHostToDevice, st)) &&
+              ok(cudaMemcpyAsync(w + h.sigma, sigma, m * sizeof(double), cudaMemcpyHostToDevice, st)) &&
+              ok(cudaEventRecord(ev_v0, st)) && ok(cudaStreamWaitEvent(s2, ev_v0, 0)) &&
+              (v0 == N || ok(cudaMemcpyAsync(w + h.V + v0 * vrow, (const char*)V + v0 * vrow, (N - v0) * vrow,
+                                             cudaMemcpyHostToDevice, s2))) &&
+              ok(cudaEventRecord(ev_vrest, s2)) && ok(cudaStreamWaitEvent(s4, ev_vrest, 0)) &&
+              (uhi <= ulo || ok(cudaMemcpyAsync(w + h.U + ulo * vrow, (const char*)U + ulo * vrow,
+                                                (uhi - ulo) * vrow, cudaMemcpyHostToDevice, s4))) &&
+              ok(cudaEventRecord(ev_u, s4)) && ok(cudaStreamWaitEvent(s3, ev_grid, 0)) &&
+              ok(cudaMemcpyAsync(w + h.z, z, (size_t)m * d * sizeof(double2), cudaMemcpyHostToDevice, s3));
+  int rc = good ? PRONY_OK : PRONY_ERR_CUDA;
+  if (rc == PRONY_OK) {
+    ProjSplit sp{s2, ev[5], ev[6]};
+    rc = project_launch(g, pl, (const double2*)(w + h.grid), (const double2*)(w + h.U), (const double2*)(w + h.V),
+                        (const double*)(w + h.sigma), S_dev, w + h.inner, sms, st, nullptr, ev_u, 1, dst,
+                        split ? &sp : nullptr);
   }
-  ProjSplit sp{s2, ev[5], ev[6]};
-  int rc = project_launch(g, pl, (const double2*)(w + h.grid), (const double2*)(w + h.U), (const double2*)(w + h.V),
-                          (const double*)(w + h.sigma), S_dev, w + h.inner, sms, st, nullptr, ev_u, 1, dst,
-                          split ? &sp : nullptr);
   if (rc == PRONY_OK)
     rc = ls_launch(d, n, m, (int)N, (const double2*)(w + h.z), (const double2*)(w + h.grid), c0, c1, nullptr, G_dev,
                    b_dev, solve ? c_dev : nullptr, solve ? t_dev : nullptr, w + h.inner_ls, dst, sms, s3, nullptr);
-  // `st` ends after everything the call enqueued on s2 and s3 (also when the projection had nothing to
-  // do and never waited on s2): the host buffers may be released once `st` is synchronized
+  // `st` ends after everything the call enqueued on s2, s3 and s4 (also when the projection had nothing to
+  // do and never waited on them): the host buffers may be released once `st` is synchronized, and a
+  // context's streams are idle for the next call once `st` reaches this point
   if (rc == PRONY_OK && !(ok(cudaEventRecord(ev_done, s3)) && ok(cudaStreamWaitEvent(st, ev_done, 0)) &&
-                          ok(cudaEventRecord(ev[6], s2)) && ok(cudaStreamWaitEvent(st, ev[6], 0))))
+                          ok(cudaEventRecord(ev[6], s2)) && ok(cudaStreamWaitEvent(st, ev[6], 0)) &&
+                          ok(cudaEventRecord(ev_u, s4)) && ok(cudaStreamWaitEvent(st, ev_u, 0))))
     rc = PRONY_ERR_CUDA;
   if (rc != PRONY_OK) {
     cudaStreamSynchronize(s2);
     cudaStreamSynchronize(s3);
+    cudaStreamSynchronize(s4);
   }
-  cleanup();
+  if (own) host_ctx_release(&local);
   return rc;
 }
 
@@ -424,10 +470,41 @@ int host_pencil(int d, int n, int m, int64_t N, const prony_c128* grid, const pr
 
 extern "C" {
 
+int prony_host_context_create(prony_host_context* out) {
+  if (!out) return PRONY_ERR_INVALID;
+  *out = nullptr;
+  prony_host_context_s* c = new (std::nothrow) prony_host_context_s();
+  if (!c) return PRONY_ERR_CUDA;
+  const int rc = host_ctx_init(c);
+  if (rc != PRONY_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return PRONY_OK;
+}
+
+int prony_host_context_destroy(prony_host_context ctx) {
+  if (!ctx) return PRONY_ERR_INVALID;
+  for (cudaStream_t s : {ctx->s2, ctx->s3, ctx->s4})
+    if (s) cudaStreamSynchronize(s);
+  host_ctx_release(ctx);
+  delete ctx;
+  return PRONY_OK;
+}
+
 int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
                       const double* sigma, const prony_c128* z, prony_c128* S, prony_c128* G, prony_c128* b,
                       prony_c128* c, double* t, void* workspace, size_t workspace_bytes, int32_t* status_out,
                       prony_stream_t stream) {
+  return prony_pencil_host_ctx(nullptr, d, n, m, grid, U, V, sigma, z, S, G, b, c, t, workspace, workspace_bytes,
+                               status_out, stream);
+}
+
+int prony_pencil_host_ctx(prony_host_context ctx, int d, int n, int m, const prony_c128* grid, const prony_c128* U,
+                          const prony_c128* V, const double* sigma, const prony_c128* z, prony_c128* S, prony_c128* G,
+                          prony_c128* b, prony_c128* c, double* t, void* workspace, size_t workspace_bytes,
+                          int32_t* status_out, prony_stream_t stream) {
   int64_t N = 0;
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
@@ -443,7 +520,7 @@ int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c
   if (cudaMemsetAsync(dst, 0, sizeof(int32_t), st) != cudaSuccess) return PRONY_ERR_CUDA;
   rc = host_pencil(d, n, m, N, grid, U, V, sigma, z, 0, ext_rows(d, n), 0, N, true, (double2*)(w + h.S),
                    (double2*)(w + h.G), (double2*)(w + h.b), (double2*)(w + h.c), (double*)(w + h.t), dst, w, h, sms,
-                   st);
+                   st, ctx);
   if (rc != PRONY_OK) return rc;
   auto d2h = [&](void* dstp, size_t off, size_t bytes) {
     return dstp == nullptr || cudaMemcpyAsync(dstp, w + off, bytes, cudaMemcpyDeviceToHost, st) == cudaSuccess;
@@ -459,6 +536,15 @@ int prony_pencil_host_part(int d, int n, int m, const prony_c128* grid, const pr
                            const double* sigma, const prony_c128* z, int64_t unit_begin, int64_t unit_end,
                            int64_t col_begin, int64_t col_end, prony_c128* S, prony_c128* G, prony_c128* b,
                            void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream) {
+  return prony_pencil_host_part_ctx(nullptr, d, n, m, grid, U, V, sigma, z, unit_begin, unit_end, col_begin, col_end,
+                                    S, G, b, workspace, workspace_bytes, dev_status, stream);
+}
+
+int prony_pencil_host_part_ctx(prony_host_context ctx, int d, int n, int m, const prony_c128* grid,
+                               const prony_c128* U, const prony_c128* V, const double* sigma, const prony_c128* z,
+                               int64_t unit_begin, int64_t unit_end, int64_t col_begin, int64_t col_end, prony_c128* S,
+                               prony_c128* G, prony_c128* b, void* workspace, size_t workspace_bytes,
+                               int32_t* dev_status, prony_stream_t stream) {
   int64_t N = 0;
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
@@ -472,7 +558,7 @@ int prony_pencil_host_part(int d, int n, int m, const prony_c128* grid, const pr
   if (workspace_bytes < h.total) return PRONY_ERR_WORKSPACE;
   return host_pencil(d, n, m, N, grid, U, V, sigma, z, unit_begin, unit_end, col_begin, col_end, false, (double2*)S,
                      (double2*)G, (double2*)b, nullptr, nullptr, dev_status, (char*)workspace, h, sms,
-                     (cudaStream_t)stream);
+                     (cudaStream_t)stream, ctx);
 }
 
 int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t seed, double tol, int max_iter,

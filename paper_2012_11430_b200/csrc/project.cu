@@ -297,8 +297,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[a][j][e] = 0.0;
 
-  auto run = [&](auto na_c) {
+  // the warp owning the last n-tile packs it when it holds <= 4 valid columns (3M only): 2 real products
+  // instead of 3 on a half-empty tile (engine PK)
+  const bool pk = MODE == 3 && (m % 8) != 0 && (m % 8) <= 4 && nt_active > 0 && t0 + nt_active == ntot;
+  auto run = [&](auto na_c, auto pk_c) {
     constexpr int NA = decltype(na_c)::value;
+    constexpr bool PK = decltype(pk_c)::value;
     for (int kt = 0; kt < KT; ++kt) {
       const int s = kt % kStages;
       mbar_wait(full0 + 8u * s, (uint32_t)(kt / kStages) & 1u);
@@ -310,25 +314,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
         const double* Bs = st + T::B_S + t0 * 8;
 #pragma unroll kKkUnroll
         for (int kk = 0; kk < kBK / 4; ++kk)
-          warp_cmma_k4<NT, NA, MODE>(acc, Ac + kk * 4 * T::LDA, As + kk * 4 * T::LDAS, T::LDA, T::LDAS,
-                                     Bc + kk * 4 * T::LDB, Bs + kk * 4 * T::LDBS, T::LDB, T::LDBS, g, q);
+          warp_cmma_k4<NT, NA, MODE, false, PK>(acc, Ac + kk * 4 * T::LDA, As + kk * 4 * T::LDAS, T::LDA, T::LDAS,
+                                                Bc + kk * 4 * T::LDB, Bs + kk * 4 * T::LDBS, T::LDB, T::LDBS, g, q);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8u * s);
     }
   };
+  auto run_na = [&](auto na_c) {
+    if (pk) run(na_c, std::true_type{});
+    else run(na_c, std::false_type{});
+  };
   if (nt_active == NT) {
-    run(std::integral_constant<int, NT>{});
+    run_na(std::integral_constant<int, NT>{});
   } else if (nt_active == 0) {
-    run(std::integral_constant<int, 0>{});
+    run(std::integral_constant<int, 0>{}, std::false_type{});
   } else if constexpr (NT > 1) {
     if (nt_active == NT - 1) {
-      run(std::integral_constant<int, NT - 1>{});
+      run_na(std::integral_constant<int, NT - 1>{});
     } else if constexpr (NT > 2) {
       if (nt_active == NT - 2) {
-        run(std::integral_constant<int, NT - 2>{});
+        run_na(std::integral_constant<int, NT - 2>{});
       } else if constexpr (NT > 3) {
-        if (nt_active == NT - 3) run(std::integral_constant<int, NT - 3>{});
+        if (nt_active == NT - 3) run_na(std::integral_constant<int, NT - 3>{});
       }
     }
   }
@@ -340,7 +348,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
   for (int j = 0; j < NT; ++j) {
     if (j < nt_active) {
       double re[4], im[4];
-      acc_to_complex<NT, MODE>(acc, j, re, im);
+      if (pk && j == nt_active - 1) acc_packed_to_complex<NT>(acc, j, q, re, im);
+      else acc_to_complex<NT, MODE>(acc, j, re, im);
       const int col = (t0 + j) * 8 + 2 * q;
       if (r0 < rows) {
         double2* y = p.Y + (ybase + r0) * NP + col;

@@ -1,15 +1,17 @@
 // vandermonde_ls.cu — A = [z_j^k], G = A conj(A)^T, b = A conj(f) (PAPER.md:59,
 // normal equations of argmin ||A^T c - f||_2; R10), c = conj(G^-1 b), t.
 //
-//   k_powers     pw[l][j][a] = z_j(l)^a, a = 0..n, by repeated multiplication (R9)
+//   k_powers     pwT[l][a][j] = z_j(l)^a, a = 0..n, by repeated multiplication (R9)
 //   k_vls        per column block (16 warps): A tile (m x 16 columns) built in shared memory from
-//                the power tables (A[j][k] = prod_l pw[l][j][k_l]), optional coalesced A write,
-//                G_part += A_tile conj(A_tile)^T on the DMMA warp engine (3M), b_part += A conj(f)
-//   k_ls_reduce  fixed-order sum of the partials -> G, b
-//   k_solve      one CTA, factor resident in shared memory: right-looking Cholesky G = L L^H,
+//                the power tables (A[j][k] = prod_l pwT[l][k_l][j]), double-buffered against the MMAs,
+//                optional coalesced A write; the LOWER triangle of G_part += A_tile conj(A_tile)^T on the
+//                DMMA warp engine (3M; G is Hermitian), b_part += A conj(f)
+//   k_ls_reduce  fixed-order sum of the partials -> G (upper triangle mirrored), b
+//   k_solve      one CTA, factor resident in shared memory: blocked right-looking Cholesky G = L L^H,
 //                L y = b, L^H x = y, c = conj(x); t = (-arg z / 2 pi) mod 1 (R4)
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 
 #include "common.cuh"
 #include "engine.cuh"
@@ -17,52 +19,97 @@
 
 namespace prony {
 
+// pwT[l][a][j] = z_j(l)^a, a = 0..n, by repeated multiplication (R9); the j index is fastest so that the A-tile
+// build (consecutive threads = consecutive j) reads it coalesced
 __global__ void k_powers(int d, int n, int m, const double2* __restrict__ z, double2* __restrict__ pw) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d * m) return;
   const int l = e / m, j = e % m;
   const double2 zz = z[(size_t)j * d + l];
   double2 p = make_double2(1.0, 0.0);
-  double2* out = pw + (size_t)e * (n + 1);
+  double2* out = pw + (size_t)l * (n + 1) * m + j;
   for (int a = 0; a <= n; ++a) {
-    out[a] = p;
+    out[(size_t)a * m] = p;
     p = cmul(p, zz);
   }
 }
 
-// grid (CB, ceil(m/BI)); CTA (cb, ib) handles columns [cbeg, cend) of I_n in tiles of kTile and
-// rows i in [BI ib, BI ib + BI) of G. Shared memory (dynamic): At[kTile][cap] (A[j][k], double2),
-// Sp[kTile][cap] (Re+Im), Sm[kTile][cap] (Re-Im), Fs[kTile] (conj f). A operand rows i, B operand
-// conj(A) rows j (engine CONJB) -> G[i][j] = sum_k A[i][k] conj(A[j][k]).
-template <int NT, int WN>
+// grid (CB, ceil(units / 16)); CTA (cb, y) handles columns [cbeg, cend) of I_n in tiles of kTile. A "unit" is
+// one warp's share of the LOWER triangle of G (G is Hermitian: only i >= j is computed, k_ls_reduce mirrors
+// the rest): 16 rows i of m-tile r and up to NT n-tiles of 8 columns j <= 16 r + 15 (host table p.unit).
+// Per tile, double-buffered in shared memory: the column info (multi-index digits of k, conj f(k)), and the
+// A tile At[kk][j] = prod_l pwT[l][k_l][j] with its 3M planes Sp = Re+Im, Sm = Re-Im; warp (unit) MMAs of
+// tile t overlap the build of tile t+1 by the other warps, one barrier per tile.
+// G_part[i][j] += sum_k A[i][k] conj(A[j][k]) (B operand conj(A) rows, engine CONJB); b_part[i] += A[i][k]
+// conj(f(k)) by threads i < m of CTA y = 0, which also writes the optional A columns.
+template <int NT>
 __global__ void __launch_bounds__(kVlsThreads, 1) k_vls(VlsParams p) {
-  constexpr int WM = (kVlsThreads / 32) / WN, BI = 16 * WM;
   extern __shared__ __align__(16) double vsm[];
   const int cap = p.cap;  // row capacity of the smem planes (>= every row read)
   const int lda = cap + 2, lds = cap + 4;
-  double2* At = reinterpret_cast<double2*>(vsm);
-  double* Sp = vsm + 2 * kTile * lda;
-  double* Sm = Sp + kTile * lds;
-  double2* Fs = reinterpret_cast<double2*>(Sm + kTile * lds);
+  const int plane = 2 * kTile * lda + 2 * kTile * lds;  // doubles per buffer
+  int* cinfo = reinterpret_cast<int*>(vsm + 2 * plane);  // [2][kTile][PRONY_MAX_D + 1]: digits, -1 = padding
+  double2* Fs = reinterpret_cast<double2*>(vsm + 2 * plane + kTile * (PRONY_MAX_D + 1));  // [2][kTile] conj f
 
   const int cb = blockIdx.x;
-  const int i0 = blockIdx.y * BI;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % WM, wn = warp / WM;
   const int g = lane >> 2, q = lane & 3;
   const int m = p.m, d = p.d, n = p.n;
-  const int ntot = (m + 7) / 8;
-  const int t0 = (ntot * wn) / WN;
-  const int nt_active = (ntot * (wn + 1)) / WN - t0;
-  const bool warp_rows = (i0 + wm * 16) < m;
+  const int u = blockIdx.y * (kVlsThreads / 32) + warp;
+  const bool has_unit = u < p.nunits;
+  const int mt = has_unit ? p.unit[u][0] : 0, t0 = has_unit ? p.unit[u][1] : 0, nt_active = has_unit ? p.unit[u][2] : 0;
+  const bool lead = blockIdx.y == 0;
   const int64_t W = p.col_end - p.col_begin;
   const int64_t cbeg = p.col_begin + W * cb / p.CB;
   const int64_t cend = p.col_begin + W * (cb + 1) / p.CB;
+  const int ntiles = (int)((cend - cbeg + kTile - 1) / kTile);
   const int L = 2 * n + 2;
+  const size_t pwl = (size_t)(n + 1) * m;  // stride of l in pwT
 
-  // rows >= m of the planes stay zero
-  for (int e = tid; e < kTile * lda; e += kVlsThreads) At[e] = make_double2(0.0, 0.0);
-  for (int e = tid; e < kTile * lds; e += kVlsThreads) Sp[e] = Sm[e] = 0.0;
+  // rows >= m of the planes stay zero (both buffers)
+  for (int e = tid; e < 2 * plane; e += kVlsThreads) vsm[e] = 0.0;
+
+  auto colinfo = [&](int tile, int buf) {  // threads < kTile: digits of k and conj f(k)
+    if (tid < kTile) {
+      const int64_t k = cbeg + (int64_t)tile * kTile + tid;
+      int* ci = cinfo + (buf * kTile + tid) * (PRONY_MAX_D + 1);
+      double2 f = make_double2(0.0, 0.0);
+      if (k < cend) {
+        int64_t r = k, idx = 0, sL = 1;
+        for (int l = d - 1; l >= 0; --l) {  // digits of k, last coordinate fastest
+          const int dg = (int)(r % (n + 1));
+          r /= (n + 1);
+          ci[l] = dg;
+          idx += (int64_t)(dg + n) * sL;
+          sL *= L;
+        }
+        ci[PRONY_MAX_D] = 1;
+        f = cconj(ldg2(p.grid + idx));
+      } else {
+        ci[PRONY_MAX_D] = -1;
+      }
+      Fs[buf * kTile + tid] = f;
+    }
+  };
+  auto build = [&](int tile, int buf) {  // A tile: A[j][k] = prod_l pwT[l][k_l][j], product in order l = 1..d (R9)
+    double2* At = reinterpret_cast<double2*>(vsm + buf * plane);
+    double* Sp = vsm + buf * plane + 2 * kTile * lda;
+    double* Sm = Sp + kTile * lds;
+    const int64_t c0 = cbeg + (int64_t)tile * kTile;
+    for (int e = tid; e < m * kTile; e += kVlsThreads) {
+      const int kk = e / m, j = e % m;
+      const int* ci = cinfo + (buf * kTile + kk) * (PRONY_MAX_D + 1);
+      double2 a = make_double2(0.0, 0.0);
+      if (ci[PRONY_MAX_D] > 0) {
+        a = ldg2(p.pw + (size_t)ci[0] * m + j);
+        for (int l = 1; l < d; ++l) a = cmul(a, ldg2(p.pw + l * pwl + (size_t)ci[l] * m + j));
+        if (p.A && lead) p.A[(size_t)j * W + (c0 + kk - p.col_begin)] = a;
+      }
+      At[kk * lda + j] = a;
+      Sp[kk * lds + j] = a.x + a.y;
+      Sm[kk * lds + j] = a.x - a.y;
+    }
+  };
 
   double acc[3][NT][4];
 #pragma unroll
@@ -73,68 +120,47 @@ __global__ void __launch_bounds__(kVlsThreads, 1) k_vls(VlsParams p) {
       for (int e = 0; e < 4; ++e) acc[a][j][e] = 0.0;
   double2 bacc = make_double2(0.0, 0.0);
   __syncthreads();
+  if (ntiles > 0) colinfo(0, 0);
+  if (ntiles > 1) colinfo(1, 1);
+  __syncthreads();
+  if (ntiles > 0) build(0, 0);
+  __syncthreads();
 
-  for (int64_t c0 = cbeg; c0 < cend; c0 += kTile) {
-    // A tile: A[j][k] = prod_l pw[l][j][k_l], k = c0 + kk, product in order l = 1..d (R9)
-    for (int e = tid; e < m * kTile; e += kVlsThreads) {
-      const int j = e / kTile, kk = e % kTile;
-      const int64_t k = c0 + kk;
-      double2 a = make_double2(0.0, 0.0);
-      if (k < cend) {
-        int dig[PRONY_MAX_D];
-        int64_t r = k;
-        for (int l = d - 1; l >= 0; --l) {  // digits of k, last coordinate fastest
-          dig[l] = (int)(r % (n + 1));
-          r /= (n + 1);
-        }
-        a = p.pw[(size_t)j * (n + 1) + dig[0]];
-        for (int l = 1; l < d; ++l) a = cmul(a, p.pw[((size_t)l * m + j) * (n + 1) + dig[l]]);
-        if (p.A && blockIdx.y == 0) p.A[(size_t)j * W + (k - p.col_begin)] = a;
-      }
-      At[kk * lda + j] = a;
-      Sp[kk * lds + j] = a.x + a.y;
-      Sm[kk * lds + j] = a.x - a.y;
-    }
-    if (tid < kTile) {
-      const int64_t k = c0 + tid;
-      double2 f = make_double2(0.0, 0.0);
-      if (k < cend) {
-        int64_t r = k, idx = 0, s = 1;
-        for (int l = d - 1; l >= 0; --l) {
-          idx += (r % (n + 1) + n) * s;
-          r /= (n + 1);
-          s *= L;
-        }
-        f = cconj(ldg2(p.grid + idx));
-      }
-      Fs[tid] = f;
-    }
-    __syncthreads();
-    if (warp_rows) {
+  for (int tile = 0; tile < ntiles; ++tile) {
+    const int buf = tile & 1;
+    const double2* At = reinterpret_cast<const double2*>(vsm + buf * plane);
+    const double* Sp = vsm + buf * plane + 2 * kTile * lda;
+    const double* Sm = Sp + kTile * lds;
+    if (has_unit) {
+      const int i0 = mt * 16;
 #pragma unroll
       for (int kk = 0; kk < kTile / 4; ++kk)
-        warp_cmma_k4_n<NT, 3, true>(nt_active, acc, At + kk * 4 * lda + i0 + wm * 16,
-                                    Sp + kk * 4 * lds + i0 + wm * 16, lda, lds, At + kk * 4 * lda + t0 * 8,
-                                    Sm + kk * 4 * lds + t0 * 8, lda, lds, g, q);
+        warp_cmma_k4_n<NT, 3, true>(nt_active, acc, At + kk * 4 * lda + i0, Sp + kk * 4 * lds + i0, lda, lds,
+                                    At + kk * 4 * lda + t0 * 8, Sm + kk * 4 * lds + t0 * 8, lda, lds, g, q);
     }
-    if (tid < BI && i0 + tid < m) {
-      const int i = i0 + tid;
+    if (lead && tid < m) {
+      const double2* F = Fs + buf * kTile;
 #pragma unroll 4
       for (int kk = 0; kk < kTile; ++kk) {
-        const double2 a = At[kk * lda + i], f = Fs[kk];
+        const double2 a = At[kk * lda + tid], f = F[kk];
         bacc.x = fma(a.x, f.x, bacc.x);
         bacc.x = fma(-a.y, f.y, bacc.x);
         bacc.y = fma(a.x, f.y, bacc.y);
         bacc.y = fma(a.y, f.x, bacc.y);
       }
     }
+    // the other buffer: its tile (tile - 1) was consumed before the previous barrier
+    if (tile + 1 < ntiles) build(tile + 1, buf ^ 1);
+    __syncthreads();
+    // column info of tile + 2 into this buffer's slot (tile's build, its last reader, is done)
+    if (tile + 2 < ntiles) colinfo(tile + 2, buf);
     __syncthreads();
   }
   double2* G = p.Gpart + (size_t)cb * m * m;
-  const int ia = i0 + wm * 16 + g, ib = ia + 8;
+  const int ia = mt * 16 + g, ib = ia + 8;
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
-    if (j < nt_active) {
+    if (has_unit && j < nt_active) {
       double re[4], im[4];
       acc_to_complex<NT, 3>(acc, j, re, im);
       const int col = (t0 + j) * 8 + 2 * q;
@@ -148,98 +174,163 @@ __global__ void __launch_bounds__(kVlsThreads, 1) k_vls(VlsParams p) {
       }
     }
   }
-  if (tid < BI && i0 + tid < m) p.bpart[(size_t)cb * m + i0 + tid] = bacc;
+  if (lead && tid < m) p.bpart[(size_t)cb * m + tid] = bacc;
 }
 
+// G[i][j] = sum_c G_part[c][i][j] for j <= i (fixed order), G[j][i] = conj(G[i][j]); b likewise
 __global__ void k_ls_reduce(int m, int CB, const double2* __restrict__ Gpart, const double2* __restrict__ bpart,
                             double2* __restrict__ G, double2* __restrict__ b) {
   const int tot = m * m + m;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
     double2 s = make_double2(0.0, 0.0);
     if (e < m * m) {
-      for (int c = 0; c < CB; ++c) s = cadd(s, Gpart[(size_t)c * m * m + e]);
-      G[e] = s;
+      const int i = e / m, j = e % m;
+      const int src = j <= i ? e : j * m + i;
+      for (int c = 0; c < CB; ++c) s = cadd(s, __ldcg(Gpart + (size_t)c * m * m + src));
+      G[e] = j <= i ? s : cconj(s);
     } else {
       const int i = e - m * m;
-      for (int c = 0; c < CB; ++c) s = cadd(s, bpart[(size_t)c * m + i]);
+      for (int c = 0; c < CB; ++c) s = cadd(s, __ldcg(bpart + (size_t)c * m + i));
       b[i] = s;
     }
   }
 }
 
-// One CTA of kSolveThreads. Right-looking Cholesky G = L L^H with lazily scaled columns: column j is
-// never rescaled, L[i][j] = A[i][j] / sqrt(d_j) with d_j the pivot (inv[j] = 1/sqrt(d_j)). The lower
-// triangle lives in registers (each thread owns <= kSolveOwn entries); per column the owners publish
-// column j to a double-buffered shared vector, ONE barrier, and every owner of an entry right of it
-// applies the rank-1 update. The factor is then stored packed (A[i][k] at i(i+1)/2 + k) for the
-// substitutions.
-// Forward / backward substitution run in one warp with the right-hand side in registers.
+// One CTA of kSolveThreads (8 warps). Blocked right-looking Cholesky G = L L^H, the lower triangle packed in
+// shared memory (A[i][k] at i(i+1)/2 + k). Per panel of kPanel columns:
+//   1. warp 0 factors the panel (rows p0..m-1) in registers — lane owns rows p0 + lane + 32 q — with the
+//      pivots and the panel's own L entries broadcast by shuffles: no CTA barrier inside the panel;
+//   2. one barrier, then all warps apply the rank-kPanel update to the trailing triangle
+//      (A[i][k] -= sum_jj L[i][jj] conj(L[k][jj]); warp per row, lanes over columns);
+//   3. one barrier.
+// So the factorization has 2 ceil(m / kPanel) CTA barriers instead of m. Then L y = b, L^H x = y in one warp
+// with the right-hand side in registers (column-oriented, y_j broadcast by shuffle), c = conj(x) (R10),
+// t = (-arg z / 2 pi) mod 1 (R4). A pivot that is not > 0 (G not HPD) sets PRONY_ERR_SINGULAR, c = NaN.
 constexpr int kSolveMaxRowsPerLane = (PRONY_MAX_M + 31) / 32;
-constexpr int kSolveOwn = (PRONY_MAX_M * (PRONY_MAX_M + 1) / 2 + kSolveThreads - 1) / kSolveThreads;
+constexpr int kPanel = 8;
 __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const double2* __restrict__ G,
                                                          const double2* __restrict__ b,
                                                          const double2* __restrict__ z, double2* __restrict__ c,
                                                          double* __restrict__ t, int32_t* status) {
-  extern __shared__ __align__(16) double2 As[];  // m(m+1)/2 packed
-  __shared__ double inv[PRONY_MAX_M];
-  __shared__ double2 colbuf[2][PRONY_MAX_M];  // the pivot column, double-buffered
+  extern __shared__ __align__(16) double2 As[];  // m(m+1)/2 packed lower triangle
+  __shared__ double dinv[PRONY_MAX_M];            // 1 / L_jj (the substitutions never divide)
   __shared__ int bad;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kWarps = kSolveThreads / 32;
   auto at = [](int i, int k) { return i * (i + 1) / 2 + k; };
+#ifdef PRONY_SOLVE_TIMING
+  long long clk0 = clock64(), clk_panel = 0, clk_upd = 0, clk_tmp = 0;
+#endif
   if (tid == 0) bad = 0;
-  // each thread owns up to kSolveOwn entries of the lower triangle, kept in registers for the whole
-  // factorization: entry e = tid + kSolveThreads s of the packed order
-  const int T = m * (m + 1) / 2;
-  double2 val[kSolveOwn];
-  int oi[kSolveOwn], ok[kSolveOwn];
+  for (int i = warp; i < m; i += kWarps)
+    for (int k = lane; k <= i; k += 32) As[at(i, k)] = G[(size_t)i * m + k];
+  __syncthreads();
+#ifdef PRONY_SOLVE_TIMING
+  const long long clk_load = clock64() - clk0;
+#endif
+
+  for (int p0 = 0; p0 < m; p0 += kPanel) {
+    const int pb = min(kPanel, m - p0);
+#ifdef PRONY_SOLVE_TIMING
+    clk_tmp = clock64();
+#endif
+    if (warp == 0) {
+      const int qn = (m - p0 + 31) >> 5;  // row groups this panel spans (warp-uniform)
+      double2 pr[kSolveMaxRowsPerLane][kPanel];
 #pragma unroll
-  for (int s = 0; s < kSolveOwn; ++s) {
-    const int e = tid + kSolveThreads * s;
-    oi[s] = -1;
-    ok[s] = -1;
-    val[s] = make_double2(0.0, 0.0);
-    if (e < T) {
-      int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-      while (i * (i + 1) / 2 > e) --i;
-      while ((i + 1) * (i + 2) / 2 <= e) ++i;
-      oi[s] = i;
-      ok[s] = e - i * (i + 1) / 2;
-      val[s] = G[(size_t)i * m + ok[s]];
+      for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
+        const int i = p0 + lane + 32 * q;
+#pragma unroll
+        for (int jj = 0; jj < kPanel; ++jj)
+          pr[q][jj] = (q < qn && i < m && jj < pb && p0 + jj <= i) ? As[at(i, p0 + jj)] : make_double2(0.0, 0.0);
+      }
+      bool fail = false;
+#pragma unroll
+      for (int jj = 0; jj < kPanel; ++jj) {
+        if (jj < pb) {
+          const int j = p0 + jj;
+          const double djj = __shfl_sync(0xffffffffu, pr[0][jj].x, jj);  // row j = p0 + jj lives in lane jj
+          if (!(djj > 0.0)) fail = true;
+          const double inv = rsqrt(djj), ljj = djj * inv;  // 1 / sqrt(d_j), sqrt(d_j): no divide on the chain
+          if (lane == 0) dinv[j] = inv;
+#pragma unroll
+          for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
+            if (q < qn) {
+              const int i = p0 + lane + 32 * q;
+              if (i == j) pr[q][jj] = make_double2(ljj, 0.0);
+              else if (i > j) pr[q][jj] = make_double2(pr[q][jj].x * inv, pr[q][jj].y * inv);
+            }
+          }
+          // L[p0 + kk][j] of the panel's later columns live in lanes kk (q = 0): fetch them all first
+          double lkx[kPanel], lky[kPanel];
+#pragma unroll
+          for (int kk = 0; kk < kPanel; ++kk) {
+            lkx[kk] = __shfl_sync(0xffffffffu, pr[0][jj].x, kk);
+            lky[kk] = __shfl_sync(0xffffffffu, pr[0][jj].y, kk);
+          }
+#pragma unroll
+          for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
+            if (q < qn) {
+              const int i = p0 + lane + 32 * q;
+              const double2 li = pr[q][jj];
+#pragma unroll
+              for (int kk = 0; kk < kPanel; ++kk) {
+                if (kk > jj && kk < pb && i >= p0 + kk && i < m) {  // A[i][k] -= L[i][j] conj(L[k][j])
+                  pr[q][kk].x -= li.x * lkx[kk] + li.y * lky[kk];
+                  pr[q][kk].y -= li.y * lkx[kk] - li.x * lky[kk];
+                }
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
+        const int i = p0 + lane + 32 * q;
+#pragma unroll
+        for (int jj = 0; jj < kPanel; ++jj)
+          if (i < m && jj < pb && p0 + jj <= i) As[at(i, p0 + jj)] = pr[q][jj];
+      }
+      if (fail && lane == 0) bad = 1;
     }
-  }
-  for (int j = 0; j < m; ++j) {
-    double2* buf = colbuf[j & 1];
-#pragma unroll
-    for (int s = 0; s < kSolveOwn; ++s)
-      if (ok[s] == j) buf[oi[s]] = val[s];  // publish column j (final: updated through column j-1)
     __syncthreads();
-    const double dj = buf[j].x;  // uniform
-    if (!(dj > 0.0)) {
-      if (tid == 0) bad = 1;
-      break;
-    }
-    const double invd = 1.0 / dj;  // L[i][j] conj(L[k][j]) = A[i][j] conj(A[k][j]) / d_j
-    if (tid == 0) inv[j] = sqrt(invd);
+#ifdef PRONY_SOLVE_TIMING
+    clk_panel += clock64() - clk_tmp;
+    clk_tmp = clock64();
+#endif
+    if (bad) break;
+    // trailing update of rows/columns >= p0 + pb
+    const int t0 = p0 + pb;
+    for (int i = t0 + warp; i < m; i += kWarps) {
+      double2 li[kPanel];
 #pragma unroll
-    for (int s = 0; s < kSolveOwn; ++s) {
-      if (ok[s] > j) {
-        const double2 a = buf[oi[s]], bb = buf[ok[s]];
-        val[s].x -= (a.x * bb.x + a.y * bb.y) * invd;
-        val[s].y -= (a.y * bb.x - a.x * bb.y) * invd;
+      for (int jj = 0; jj < kPanel; ++jj) li[jj] = jj < pb ? As[at(i, p0 + jj)] : make_double2(0.0, 0.0);
+      for (int k = t0 + lane; k <= i; k += 32) {
+        double2 a = As[at(i, k)];
+#pragma unroll
+        for (int jj = 0; jj < kPanel; ++jj) {
+          if (jj < pb) {
+            const double2 lk = As[at(k, p0 + jj)];
+            a.x -= li[jj].x * lk.x + li[jj].y * lk.y;
+            a.y -= li[jj].y * lk.x - li[jj].x * lk.y;
+          }
+        }
+        As[at(i, k)] = a;
       }
     }
-    // no second barrier: column j+1 goes to the other buffer, and this buffer is rewritten only after
-    // the next iteration's barrier, which every thread reaches after its reads here
+    __syncthreads();
+#ifdef PRONY_SOLVE_TIMING
+    clk_upd += clock64() - clk_tmp;
+#endif
   }
-#pragma unroll
-  for (int s = 0; s < kSolveOwn; ++s)
-    if (oi[s] >= 0) As[at(oi[s], ok[s])] = val[s];  // lazily scaled factor for the substitutions
-  __syncthreads();
+#ifdef PRONY_SOLVE_TIMING
+  const long long clk_fact = clock64();
+#endif
+
   if (bad) {
     if (tid == 0) set_status(status, PRONY_ERR_SINGULAR);
     for (int i = tid; i < m; i += kSolveThreads) c[i] = make_double2(NAN, NAN);
-  } else if (tid < 32) {
-    const int lane = tid;
+  } else if (warp == 0) {
     double2 y[kSolveMaxRowsPerLane];
 #pragma unroll
     for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
@@ -255,15 +346,14 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const dou
         if (q == qj) yj = y[q];
       yj.x = __shfl_sync(0xffffffffu, yj.x, lj);
       yj.y = __shfl_sync(0xffffffffu, yj.y, lj);
-      const double ij = inv[j];
+      const double ij = dinv[j];
       yj = make_double2(yj.x * ij, yj.y * ij);
 #pragma unroll
       for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
         const int i = lane + 32 * q;
         if (i == j) y[q] = yj;
         if (i > j && i < m) {
-          const double2 a = As[at(i, j)];
-          const double2 l = make_double2(a.x * ij, a.y * ij);
+          const double2 l = As[at(i, j)];
           y[q].x -= l.x * yj.x - l.y * yj.y;
           y[q].y -= l.x * yj.y + l.y * yj.x;
         }
@@ -278,18 +368,16 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const dou
         if (q == qj) xj = y[q];
       xj.x = __shfl_sync(0xffffffffu, xj.x, lj);
       xj.y = __shfl_sync(0xffffffffu, xj.y, lj);
-      const double ij = inv[j];
+      const double ij = dinv[j];
       xj = make_double2(xj.x * ij, xj.y * ij);
 #pragma unroll
       for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
         const int i = lane + 32 * q;
         if (i == j) y[q] = xj;
         if (i < j) {
-          const double2 a = As[at(j, i)];
-          const double ii_ = inv[i];
-          const double2 l = make_double2(a.x * ii_, -a.y * ii_);  // conj(L_ji)
-          y[q].x -= l.x * xj.x - l.y * xj.y;
-          y[q].y -= l.x * xj.y + l.y * xj.x;
+          const double2 a = As[at(j, i)];  // conj(L_ji)
+          y[q].x -= a.x * xj.x + a.y * xj.y;
+          y[q].y -= a.x * xj.y - a.y * xj.x;
         }
       }
     }
@@ -298,6 +386,11 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const dou
       const int i = lane + 32 * q;
       if (i < m) c[i] = cconj(y[q]);
     }
+#ifdef PRONY_SOLVE_TIMING
+    if (lane == 0)
+      printf("k_solve m=%d clocks: load %lld panels %lld updates %lld substitution %lld total %lld\n", m, clk_load,
+             clk_panel, clk_upd, clock64() - clk_fact, clock64() - clk0);
+#endif
   }
   if (t) {
     const double inv2pi = 0.15915494309189533577;  // 1 / (2 pi)
@@ -313,29 +406,34 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const dou
 
 // ---------------------------------------------------------------------------- host side
 namespace {
-struct VlsShape {
-  int NT, WN, BI, cap;
-};
-VlsShape vls_shape(int m) {
-  VlsShape s;
-  const int ntot = (m + 7) / 8;
-  s.WN = ntot <= 8 ? 2 : 4;
-  s.NT = (ntot + s.WN - 1) / s.WN;
-  s.BI = 16 * ((kVlsThreads / 32) / s.WN);
-  const int rows_a = (m + s.BI - 1) / s.BI * s.BI;  // A-operand rows read (whole i-blocks)
-  const int rows_b = 8 * s.NT * s.WN;              // B-operand rows read
-  s.cap = std::max(rows_a, rows_b);
-  return s;
+constexpr int kVlsNT = 4;  // n-tiles per unit (3M accumulators: 48 doubles per thread)
+// lower-triangle units: m-tile r (rows 16r..16r+15) needs n-tiles 0..ceil(min(16r+16, m)/8)-1, split into
+// near-equal runs of <= kVlsNT
+int vls_units(int m, int (*unit)[3]) {
+  int cnt = 0;
+  for (int r = 0; 16 * r < m; ++r) {
+    const int nt = (std::min(16 * r + 16, m) + 7) / 8;
+    const int parts = (nt + kVlsNT - 1) / kVlsNT;
+    for (int pp = 0; pp < parts; ++pp) {
+      const int a = nt * pp / parts, b = nt * (pp + 1) / parts;
+      if (unit && cnt < kVlsMaxUnits) {
+        unit[cnt][0] = r;
+        unit[cnt][1] = a;
+        unit[cnt][2] = b - a;
+      }
+      ++cnt;
+    }
+  }
+  return cnt;
 }
 size_t vls_smem(int cap) {
   const int lda = cap + 2, lds = cap + 4;
-  return (size_t)(2 * kTile * lda + 2 * kTile * lds) * sizeof(double) + kTile * sizeof(double2);
+  return (size_t)2 * (2 * kTile * lda + 2 * kTile * lds) * sizeof(double) +
+         (size_t)kTile * (PRONY_MAX_D + 1) * sizeof(int) * 2 + 2 * kTile * sizeof(double2);
 }
-int vls_cb(int64_t W, int m, int sm_count) {
-  const VlsShape s = vls_shape(m);
-  const int ib = (m + s.BI - 1) / s.BI;
+int vls_cb(int64_t W, int ctas_per_block, int sm_count) {
   const int64_t tiles = (W + kTile - 1) / kTile;
-  int64_t cb = std::max<int64_t>(1, sm_count / ib);
+  int64_t cb = std::max<int64_t>(1, sm_count / std::max(1, ctas_per_block));
   cb = std::max<int64_t>(1, std::min<int64_t>(cb, tiles));
   return (int)cb;
 }
@@ -350,11 +448,10 @@ size_t ls_workspace_bytes(int d, int n, int m, int sm_count) {
   return bytes;
 }
 
-template <int NT, int WN>
-static int launch_vls_t(const VlsParams& p, dim3 grid, size_t smem, cudaStream_t st) {
-  if (cudaFuncSetAttribute(k_vls<NT, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+static int launch_vls(const VlsParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+  if (cudaFuncSetAttribute(k_vls<kVlsNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return PRONY_ERR_CUDA;
-  k_vls<NT, WN><<<grid, kVlsThreads, smem, st>>>(p);
+  k_vls<kVlsNT><<<grid, kVlsThreads, smem, st>>>(p);
   return PRONY_OK;
 }
 
@@ -394,35 +491,27 @@ int ls_launch(int d, int n, int m, int N, const double2* z, const double2* grid,
     return PRONY_OK;
   }
   k_powers<<<(d * m + 127) / 128, 128, 0, st>>>(d, n, m, z, pw);
-  const VlsShape sh = vls_shape(m);
   VlsParams p{};
   p.d = d;
   p.n = n;
   p.m = m;
   p.col_begin = col_begin;
   p.col_end = col_end;
-  p.CB = vls_cb(W, m, sm_count);
-  p.cap = sh.cap;
+  p.nunits = vls_units(m, p.unit);
+  if (p.nunits > kVlsMaxUnits) return PRONY_ERR_RANGE;
+  const int per_cta = kVlsThreads / 32;
+  const int ny = (p.nunits + per_cta - 1) / per_cta;
+  p.CB = vls_cb(W, ny, sm_count);
+  p.cap = (m + 15) / 16 * 16;  // every A row (m-tiles) and B row (n-tiles <= the row's m-tile) read
   p.pw = pw;
   p.grid = grid;
   p.A = A;
   p.Gpart = Gpart;
   p.bpart = bpart;
-  const int ib = (m + sh.BI - 1) / sh.BI;
-  const dim3 vgrid(p.CB, ib);
-  const size_t smem = vls_smem(sh.cap);
+  const dim3 vgrid(p.CB, ny);
+  const size_t smem = vls_smem(p.cap);
   if (info && info->ev_main_begin) cudaEventRecord((cudaEvent_t)info->ev_main_begin, st);
-  int rc = PRONY_OK;
-  switch (sh.WN * 16 + sh.NT) {
-#define PRONY_VCASE(nt, wn) \
-  case wn * 16 + nt:        \
-    rc = launch_vls_t<nt, wn>(p, vgrid, smem, st); \
-    break;
-    PRONY_VCASE(1, 2) PRONY_VCASE(2, 2) PRONY_VCASE(3, 2) PRONY_VCASE(4, 2) PRONY_VCASE(3, 4) PRONY_VCASE(4, 4)
-#undef PRONY_VCASE
-    default:
-      return PRONY_ERR_RANGE;
-  }
+  int rc = launch_vls(p, vgrid, smem, st);
   if (rc != PRONY_OK) return rc;
   if (info && info->ev_main_end) cudaEventRecord((cudaEvent_t)info->ev_main_end, st);
   int launches = 3;
@@ -436,10 +525,12 @@ int ls_launch(int d, int n, int m, int N, const double2* z, const double2* grid,
   if (info) {
     info->launches = launches;
     info->main_grid[0] = p.CB;
-    info->main_grid[1] = ib;
+    info->main_grid[1] = ny;
     info->main_grid[2] = 1;
     info->main_block = kVlsThreads;
     info->split_k = p.CB;
+    // the LS products as defined (G = A conj(A)^T in full, b = A conj(f)), ZGEMM convention; the kernel
+    // computes only the lower triangle of the Hermitian G
     info->main_flops = 8.0 * m * (double)m * (double)W + 8.0 * m * (double)W;
   }
   if (cudaGetLastError() != cudaSuccess) return PRONY_ERR_CUDA;

@@ -14,10 +14,13 @@ constexpr int kMaxM = PRONY_MAX_M;
 #endif
 constexpr int kTile = PRONY_VLS_TILE;  // columns of A per smem tile of k_vls
 constexpr int kVlsThreads = 512;   // 16 warps (DMMA warp engine)
-constexpr int kSolveThreads = 512;
+constexpr int kSolveThreads = 256;
+
+constexpr int kVlsMaxUnits = 32;  // lower-triangle warp units (m <= 128 needs 20 at 4 n-tiles each)
 
 struct VlsParams {
-  int d, n, m, CB, cap;
+  int d, n, m, CB, cap, nunits;
+  int unit[kVlsMaxUnits][3];  // (m-tile, first n-tile, n-tiles) per warp unit
   int64_t col_begin, col_end;
   const double2* pw;
   const double2* grid;

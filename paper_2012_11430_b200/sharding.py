@@ -155,46 +155,57 @@ class DistributedPencil:
         self.c0, self.c1 = column_range(d, n, world, rank)
         self.ws_p = pb.alloc_workspace(pb.WS_PROJECT, d, n, m, device)
         self.ws_l = pb.alloc_workspace(pb.WS_LS, d, n, m, device)
-        self.S = torch.empty((d, m, m), dtype=torch.complex128, device=device)
-        self.G = torch.empty((m, m), dtype=torch.complex128, device=device)
-        self.b = torch.empty(m, dtype=torch.complex128, device=device)
+        # S, G, b are views of ONE packed buffer: the kernels write their partials straight into it and the
+        # all-reduce runs in place (no pack / unpack copies)
+        self.buf = torch.empty(d * m * m + m * m + m, dtype=torch.complex128, device=device)
+        self.S, self.G, self.b = unpack(self.buf, d, m)
+        self.c = torch.empty(m, dtype=torch.complex128, device=device)
+        self.t = torch.empty((m, d), dtype=torch.float64, device=device)
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
-        # the LS step is independent of the projection: it runs on a side stream and fills the SMs
-        # the projection's last wave leaves idle
+        # the projection runs on a HIGH-priority stream, the LS step on a normal-priority side stream: the LS
+        # CTAs fill the SMs the projection's last wave leaves idle without delaying any projection CTA
+        self.hi = torch.cuda.Stream(device=device, priority=-1)
         self.side = torch.cuda.Stream(device=device)
         self.ev_in = torch.cuda.Event()
         self.ev_ls = torch.cuda.Event()
 
     def __call__(self, grid, U, V, sigma, z, stream=None, info_p=None, info_l=None, ev_comm=None):
-        """Device-resident inputs -> (S, c, t). ev_comm: optional (begin, end) CUDA events recorded on
-        `stream` around the collective (communication time of the step)."""
+        """Device-resident inputs -> (S, c, t) (views of this object's buffers, valid until the next call).
+        Ordered after prior work on `stream` (default: the current stream), which is ordered after all of it
+        on return. ev_comm: optional (begin, end) CUDA events recorded around the collective."""
         pb, d, n, m = self.pb, self.d, self.n, self.m
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
-        with torch.cuda.stream(main):
+        hi = self.hi
+        hi.wait_stream(main)
+        with torch.cuda.stream(hi):
             self.status.zero_()
-            self.ev_in.record(main)
+            self.ev_in.record(hi)
             pb.project(grid, U, V, sigma, d, n, m, self.u0, self.u1, self.order, out=self.S, workspace=self.ws_p,
-                       dev_status=self.status, stream=main, info=info_p)
+                       dev_status=self.status, stream=hi, info=info_p)
             full = self.world == 1
             self.side.wait_event(self.ev_in)
             res = pb.vandermonde_ls(z, grid, d, n, m, self.c0, self.c1, want_solution=full,
-                                    out={"G": self.G, "b": self.b}, workspace=self.ws_l, dev_status=self.status,
-                                    stream=self.side, info=info_l)
+                                    out={"G": self.G, "b": self.b, "c": self.c, "t": self.t}, workspace=self.ws_l,
+                                    dev_status=self.status, stream=self.side, info=info_l)
             self.ev_ls.record(self.side)
-            main.wait_event(self.ev_ls)
+            hi.wait_event(self.ev_ls)
             if full:
-                return self.S, res["c"], res["t"]
-            return self._reduce_and_solve(z, main, ev_comm)
+                out = (self.S, res["c"], res["t"])
+            else:
+                out = self._reduce_and_solve(z, hi, ev_comm)
+        main.wait_stream(hi)
+        return out
 
-    def _reduce_and_solve(self, z, main, ev_comm=None):
+    def _reduce_and_solve(self, z, st, ev_comm=None):
         pb, d, m = self.pb, self.d, self.m
         if ev_comm is not None:
-            ev_comm[0].record(main)
-        Sr, Gr, br = allreduce_pencil(self.S, self.G, self.b)
+            ev_comm[0].record(st)
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            dist.all_reduce(torch.view_as_real(self.buf), op=dist.ReduceOp.SUM)
         if ev_comm is not None:
-            ev_comm[1].record(main)
-        c, t = pb.ls_solve(Gr.contiguous(), br.contiguous(), z, d, m, dev_status=self.status, stream=main)
-        return Sr, c, t
+            ev_comm[1].record(st)
+        c, t = pb.ls_solve(self.G, self.b, z, d, m, dev_status=self.status, stream=st, out={"c": self.c, "t": self.t})
+        return self.S, c, t
 
     # ------------------------------------------------------------------ end to end from host buffers
     def h2d_bytes(self, scatter_v: bool = True) -> int:
@@ -227,11 +238,13 @@ class DistributedPencil:
                     raise ValueError("scatter_v=False needs the SHARED unit order")
                 if not hasattr(self, "ws_h"):
                     self.ws_h = pb.alloc_workspace(pb.WS_PENCIL_HOST, d, n, m, dev)
-                self.status.zero_()
-                pb.pencil_host_part(grid_h, U_h, V_h, sigma_h, z_h, d, n, m, self.u0, self.u1, self.c0, self.c1,
-                                    self.S, self.G, self.b, workspace=self.ws_h, dev_status=self.status, stream=main)
+                    self.hctx = pb.HostContext()
                 if self.world == 1:
                     raise ValueError("scatter_v=False is the N > 1 partial path")
+                self.status.zero_()
+                pb.pencil_host_part(grid_h, U_h, V_h, sigma_h, z_h, d, n, m, self.u0, self.u1, self.c0, self.c1,
+                                    self.S, self.G, self.b, workspace=self.ws_h, dev_status=self.status, stream=main,
+                                    context=self.hctx)
                 return self._reduce_and_solve(self.dz, main, ev_comm)
             chunk, (v0, v1), (ulo, uhi) = host_rows(d, n, self.world, self.rank, self.order)
             self.dgrid.copy_(grid_h, non_blocking=True)

@@ -42,7 +42,7 @@ def test_exported_symbols_are_c_abi(pb):
 
 def test_abi_version_and_status_strings(pb):
     hdr = open(os.path.join(ROOT, "include", "prony.h")).read()
-    assert pb.lib().prony_abi_version() == int(re.search(r"#define PRONY_ABI_VERSION (\d+)", hdr).group(1)) == 3
+    assert pb.lib().prony_abi_version() == int(re.search(r"#define PRONY_ABI_VERSION (\d+)", hdr).group(1)) == 4
     for code in range(0, 9):
         assert len(pb.status_string(code)) > 0
     assert pb.status_string(12345) == "unknown status"
@@ -77,6 +77,13 @@ def test_validation_before_any_cuda_call(pb):
     assert L.prony_lanczos_svd(2, 4, p, 5, 0.0, 0, 6, p, p, p, ctypes.byref(r), None, p, 0,
                                null) == pb.PRONY_ERR_INVALID
     assert L.prony_workspace_size(pb.WS_LANCZOS, 2, 20, 256, ctypes.byref(sz)) == pb.PRONY_ERR_RANGE
+    # the diagonalization's workspace does not depend on n: a huge n is fine, m is still checked
+    assert L.prony_workspace_size(pb.WS_DIAG, 8, 100000, 40, ctypes.byref(sz)) == pb.PRONY_OK and sz.value > 0
+    assert L.prony_workspace_size(pb.WS_DIAG, 8, 1, 129, ctypes.byref(sz)) == pb.PRONY_ERR_RANGE
+    # host context: null out-pointer / null context
+    assert L.prony_host_context_create(None) == pb.PRONY_ERR_INVALID
+    assert L.prony_host_context_destroy(None) == pb.PRONY_ERR_INVALID
+    assert L.prony_pencil_host_ctx(None, 0, 4, 2, *([None] * 11), 0, None, None) == pb.PRONY_ERR_INVALID
 
 
 def test_misaligned_pointer_rejected(pb):

@@ -369,6 +369,24 @@ def test_pencil_host_matches_device_path(pb, orc):
     assert W.torus_dist_inf(out["t"], prob.t).max() <= 1e-8
 
 
+def test_pencil_host_context_reuse(pb, orc):
+    """prony_host_context: one context serves many calls (different shapes included); results are bitwise those
+    of the per-call-stream path (the same kernels in the same order) and match the oracle."""
+    ctx = pb.HostContext()
+    for name in ("cfg2", "cfg1", "cfg2"):
+        prob = W.make_problem(name)
+        c = prob.cfg
+        a = pb.pencil_host(prob.grid, prob.U, prob.V, prob.sigma, prob.z, c.d, c.n, c.m, context=ctx)
+        b = pb.pencil_host(prob.grid, prob.U, prob.V, prob.sigma, prob.z, c.d, c.n, c.m)
+        assert a["status"] == 0 and b["status"] == 0
+        for k in ("S", "G", "b", "c", "t"):
+            assert np.array_equal(a[k], b[k]), k
+        S_or = orc.project(prob.grid, prob.U, prob.V, prob.sigma, c.d, c.n)
+        for l in range(c.d):
+            assert rel(a["S"][l], S_or[l]) <= TOL
+    ctx.close()
+
+
 @pytest.mark.parametrize("d,n,m,noise", [(1, 300, 9, 1e-6), (3, 9, 13, 0.0), (2, 40, 37, 1e-6), (2, 5, 3, 0.0)])
 def test_pencil_host_shapes(pb, orc, d, n, m, noise):
     """prony_pencil_host over shapes whose plans split K into several chunks (the copy/compute overlap

@@ -22,6 +22,7 @@ VARIANTS = {
     "vt32": ["PRONY_VLS_TILE=32"],
     "vt64": ["PRONY_VLS_TILE=64"],
     "bk8s5": ["PRONY_BK=8", "PRONY_STAGES=5"],
+    "solvet": ["PRONY_SOLVE_TIMING"],
 }
 
 if __name__ == "__main__":
