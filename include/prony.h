@@ -69,8 +69,9 @@
 extern "C" {
 #endif
 
-#define PRONY_ABI_VERSION 4  /* 2: PRONY_UNITS_SHARED, prony_lanczos_svd, PRONY_WS_LANCZOS; 3: prony_pencil_host_part;
-                                 4: prony_host_context, prony_pencil_host_ctx, prony_pencil_host_part_ctx */
+#define PRONY_ABI_VERSION 5  /* 2: PRONY_UNITS_SHARED, prony_lanczos_svd, PRONY_WS_LANCZOS; 3: prony_pencil_host_part;
+                                 4: prony_host_context, prony_pencil_host_ctx, prony_pencil_host_part_ctx;
+                                 5: prony_pencil, PRONY_WS_PENCIL */
 #define PRONY_MAX_D 8
 #define PRONY_MAX_M 128
 
@@ -105,7 +106,8 @@ typedef enum prony_workspace_kind {
   PRONY_WS_APPLY = 4,        /* prony_toeplitz_apply, any r */
   PRONY_WS_DIAG = 5,         /* prony_diagonalize */
   PRONY_WS_PROJECT_MU = 6,   /* prony_project_mu */
-  PRONY_WS_LANCZOS = 7       /* prony_lanczos_svd; the m argument is max_rank (<= 255) */
+  PRONY_WS_LANCZOS = 7,      /* prony_lanczos_svd; the m argument is max_rank (<= 255) */
+  PRONY_WS_PENCIL = 8        /* prony_pencil: the scratch of prony_project and prony_vandermonde_ls side by side */
 } prony_workspace_kind;
 
 /* unit orders of prony_project. L_MAJOR / ROW_MAJOR: units u in [0, d*N), one row k
@@ -289,6 +291,25 @@ int prony_pencil_host_part_ctx(prony_host_context ctx, int d, int n, int m, cons
                                int64_t unit_begin, int64_t unit_end, int64_t col_begin, int64_t col_end, prony_c128* S,
                                prony_c128* G, prony_c128* b, void* workspace, size_t workspace_bytes,
                                int32_t* dev_status, prony_stream_t stream);
+
+/*
+ * prony_pencil — one full pencil on DEVICE buffers in ONE call: prony_project over all SHARED units on
+ * `stream` and, concurrently on the context's side stream, prony_vandermonde_ls over [0, N) with c and t
+ * (PAPER.md:27-29, 39, 58-59); `stream` is ordered after both on return (asynchronous). The launch path for
+ * small, launch-bound pencils: one C call instead of the two entry points plus the stream fork/join.
+ *   ctx          side stream + events (prony_host_context_create); NULL: created and destroyed by the call
+ *   grid, U, V, sigma, z   device inputs as prony_project / prony_vandermonde_ls
+ *   S, G, b, c, t          device outputs (d x m x m, m x m, m, m, m x d)
+ *   workspace    device scratch >= prony_workspace_size(PRONY_WS_PENCIL)
+ *   dev_status   as prony_project (zeroed by the caller)
+ *   info_project, info_ls  nullable prony_exec_info of the two halves (events recorded on their streams)
+ * Returns PRONY_OK, a validation error (as prony_project), PRONY_ERR_WORKSPACE or PRONY_ERR_CUDA.
+ */
+int prony_pencil(prony_host_context ctx, int d, int n, int m, const prony_c128* grid, const prony_c128* U,
+                 const prony_c128* V, const double* sigma, const prony_c128* z, prony_c128* S, prony_c128* G,
+                 prony_c128* b, prony_c128* c, double* t, void* workspace, size_t workspace_bytes,
+                 int32_t* dev_status, prony_stream_t stream, prony_exec_info* info_project,
+                 prony_exec_info* info_ls);
 
 /*
  * prony_pencil_host_part — one rank's share of a pencil from HOST inputs (multi-GPU end to end, P:259-267

@@ -12,10 +12,10 @@ from .binding import (  # noqa: F401
     WS_PENCIL_HOST, WS_PROJECT, PronyError, alloc_workspace, build_pencil, device_info, lib, ls_solve,
     pencil_host, project, status_string, toeplitz_apply, vandermonde_ls, workspace_size,
     WS_APPLY, WS_DIAG, WS_PROJECT_MU, project_mu, diagonalize, PRONY_ERR_RANK, PRONY_ERR_NOT_CONVERGED, WS_BUILD,
-    WS_LANCZOS, lanczos_svd, pencil_host_part, UNITS_SHARED, HostContext,
+    WS_LANCZOS, lanczos_svd, pencil_host_part, UNITS_SHARED, HostContext, pencil, WS_PENCIL,
 )
 from . import sharding  # noqa: F401
 
-__all__ = ["project", "vandermonde_ls", "ls_solve", "pencil_host", "pencil_host_part", "HostContext", "build_pencil", "lanczos_svd", "diagonalize",
+__all__ = ["project", "vandermonde_ls", "ls_solve", "pencil", "pencil_host", "pencil_host_part", "HostContext", "build_pencil", "lanczos_svd", "diagonalize",
            "project_mu", "toeplitz_apply", "workspace_size",
            "alloc_workspace", "device_info", "status_string", "PronyError", "sharding"]

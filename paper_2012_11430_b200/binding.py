@@ -23,7 +23,7 @@ PRONY_ERR_CUDA = 6
 PRONY_ERR_UNIMPLEMENTED = 7
 PRONY_ERR_WORKSPACE = 8
 
-WS_PROJECT, WS_LS, WS_PENCIL_HOST, WS_BUILD, WS_APPLY, WS_DIAG, WS_PROJECT_MU, WS_LANCZOS = 0, 1, 2, 3, 4, 5, 6, 7
+WS_PROJECT, WS_LS, WS_PENCIL_HOST, WS_BUILD, WS_APPLY, WS_DIAG, WS_PROJECT_MU, WS_LANCZOS, WS_PENCIL = range(9)
 UNITS_L_MAJOR, UNITS_ROW_MAJOR, UNITS_SHARED = 0, 1, 2
 MAX_D, MAX_M = 8, 128
 
@@ -32,7 +32,7 @@ EXPORTS = ("prony_abi_version", "prony_status_string", "prony_device_info", "pro
            "prony_project", "prony_project_ex", "prony_vandermonde_ls", "prony_vandermonde_ls_ex", "prony_ls_solve",
            "prony_toeplitz_apply", "prony_pencil_host", "prony_build_pencil", "prony_diagonalize",
            "prony_project_mu", "prony_lanczos_svd", "prony_pencil_host_part", "prony_host_context_create",
-           "prony_host_context_destroy", "prony_pencil_host_ctx", "prony_pencil_host_part_ctx")
+           "prony_host_context_destroy", "prony_pencil_host_ctx", "prony_pencil_host_part_ctx", "prony_pencil")
 
 
 class ExecInfo(ctypes.Structure):
@@ -91,11 +91,12 @@ def lib() -> ctypes.CDLL:
         L.prony_host_context_destroy.argtypes = [vp]
         L.prony_pencil_host_ctx.argtypes = [vp] + L.prony_pencil_host.argtypes
         L.prony_pencil_host_part_ctx.argtypes = [vp] + L.prony_pencil_host_part.argtypes
+        L.prony_pencil.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp, vp, vp]
         for f in ("prony_device_info", "prony_workspace_size", "prony_project", "prony_vandermonde_ls", "prony_ls_solve",
                   "prony_project_ex", "prony_vandermonde_ls_ex", "prony_toeplitz_apply", "prony_diagonalize",
                   "prony_project_mu", "prony_pencil_host_part", "prony_lanczos_svd", "prony_host_context_create",
                   "prony_host_context_destroy", "prony_pencil_host_ctx", "prony_pencil_host_part_ctx",
-                  "prony_pencil_host", "prony_build_pencil"):
+                  "prony_pencil_host", "prony_build_pencil", "prony_pencil"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -273,6 +274,21 @@ def toeplitz_apply(grid, X, d: int, n: int, ell: int = 0, conj: bool = False, ou
     rc = lib().prony_toeplitz_apply(d, n, _ptr(grid), int(ell), int(bool(conj)), _ptr(X), X.stride(0), r, _ptr(out),
                                     out.stride(0), _ptr(workspace), workspace.numel(), _stream(stream))
     _check(rc, "prony_toeplitz_apply")
+    return out
+
+
+def pencil(grid, U, V, sigma, z, d: int, n: int, m: int, out: dict, workspace, context=None, dev_status=None,
+           stream=None, info_p=None, info_l=None):
+    """One full pencil on DEVICE buffers in one C call (prony_pencil): S_1..S_d on `stream`, the LS products,
+    c and t concurrently on the context's side stream. out: preallocated device tensors "S" (d,m,m), "G" (m,m),
+    "b" (m,), "c" (m,), "t" (m,d); workspace >= WS_PENCIL. Asynchronous; returns `out`. Arguments are passed
+    through unchecked beyond the C ABI's validation (this is the low-overhead path)."""
+    rc = lib().prony_pencil(None if context is None else context.handle, d, n, m, _ptr(grid), _ptr(U), _ptr(V),
+                            _ptr(sigma), _ptr(z), _ptr(out["S"]), _ptr(out["G"]), _ptr(out["b"]), _ptr(out["c"]),
+                            _ptr(out["t"]), _ptr(workspace), workspace.numel(), _ptr(dev_status), _stream(stream),
+                            None if info_p is None else ctypes.byref(info_p),
+                            None if info_l is None else ctypes.byref(info_l))
+    _check(rc, "prony_pencil")
     return out
 
 

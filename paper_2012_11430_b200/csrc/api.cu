@@ -169,6 +169,7 @@ int prony_workspace_size(int kind, int d, int n, int m, size_t* bytes) {
       *bytes = std::max(svd_workspace_bytes(d, n, (int)N, m), ws_project(d, n, N, m, sms));
       return PRONY_OK;
     case PRONY_WS_PROJECT_MU: *bytes = ws_project_mu(d, n, N, m, sms); return PRONY_OK;
+    case PRONY_WS_PENCIL: *bytes = align_up(ws_project(d, n, N, m, sms), 256) + ws_ls(d, n, m, sms); return PRONY_OK;
     case PRONY_WS_APPLY: *bytes = apply_workspace_bytes(d, n, (int)N); return PRONY_OK;
     default: return PRONY_ERR_INVALID;
   }
@@ -491,6 +492,60 @@ int prony_host_context_destroy(prony_host_context ctx) {
   host_ctx_release(ctx);
   delete ctx;
   return PRONY_OK;
+}
+
+int prony_pencil(prony_host_context ctx, int d, int n, int m, const prony_c128* grid, const prony_c128* U,
+                 const prony_c128* V, const double* sigma, const prony_c128* z, prony_c128* S, prony_c128* G,
+                 prony_c128* b, prony_c128* c, double* t, void* workspace, size_t workspace_bytes,
+                 int32_t* dev_status, prony_stream_t stream, prony_exec_info* info_project,
+                 prony_exec_info* info_ls) {
+  int64_t N = 0;
+  int rc = validate_dnm(d, n, m, &N);
+  if (rc) return rc;
+  if (!grid || !U || !V || !sigma || !z || !S || !G || !b || !workspace) return PRONY_ERR_INVALID;
+  if (!aligned16(grid) || !aligned16(U) || !aligned16(V) || !aligned16(z) || !aligned16(S) || !aligned16(G) ||
+      !aligned16(b) || (c && !aligned16(c)) || (t && ((uintptr_t)t & 7u)) || ((uintptr_t)sigma & 7u) ||
+      ((uintptr_t)workspace & 255u))
+    return PRONY_ERR_INVALID;
+  const int sms = sm_count_current();
+  if (sms <= 0) return PRONY_ERR_CUDA;
+  const size_t off_ls = align_up(ws_project(d, n, N, m, sms), 256);
+  if (workspace_bytes < off_ls + ws_ls(d, n, m, sms)) return PRONY_ERR_WORKSPACE;
+  prony_host_context_s local;
+  const bool own = ctx == nullptr;
+  if (own) {
+    if (host_ctx_init(&local) != PRONY_OK) return PRONY_ERR_CUDA;
+    ctx = &local;
+  } else {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return PRONY_ERR_CUDA;
+    if (dev != ctx->device) return PRONY_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream, side = ctx->s3;
+  cudaEvent_t ev_in = ctx->ev[0], ev_done = ctx->ev[4];
+  ProjGeom g{};
+  g.d = d;
+  g.n = n;
+  g.m = m;
+  g.N = (int)N;
+  unit_rows(d, n, N, 0, ext_rows(d, n), PRONY_UNITS_SHARED, &g);
+  ProjPlan pl{};
+  project_plan(g, sms, &pl);
+  char* w = (char*)workspace;
+  rc = (cudaEventRecord(ev_in, st) == cudaSuccess && cudaStreamWaitEvent(side, ev_in, 0) == cudaSuccess)
+           ? PRONY_OK : PRONY_ERR_CUDA;
+  if (rc == PRONY_OK)
+    rc = project_launch(g, pl, (const double2*)grid, (const double2*)U, (const double2*)V, sigma, (double2*)S, w,
+                        sms, st, info_project, nullptr, 1, dev_status);
+  if (rc == PRONY_OK)
+    rc = ls_launch(d, n, m, (int)N, (const double2*)z, (const double2*)grid, 0, N, nullptr, (double2*)G, (double2*)b,
+                   (double2*)c, t, w + off_ls, dev_status, sms, side, info_ls);
+  if (rc == PRONY_OK && !(cudaEventRecord(ev_done, side) == cudaSuccess &&
+                          cudaStreamWaitEvent(st, ev_done, 0) == cudaSuccess))
+    rc = PRONY_ERR_CUDA;
+  if (rc != PRONY_OK) cudaStreamSynchronize(side);
+  if (own) host_ctx_release(&local);
+  return rc;
 }
 
 int prony_pencil_host(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,

@@ -561,19 +561,32 @@ __global__ void k_finalize(int d, int m, int RP, const double2* __restrict__ Spa
       if (sigma[j] <= (double)N * 2.220446049250313e-16 * smax) bad = true;
     if (bad) set_status(status, PRONY_ERR_SINGULAR);
   }
+  // a group of kFinLanes lanes per output: lane l sums P = l, l + kFinLanes, ... in order, then a fixed
+  // shuffle tree (deterministic; independent load streams instead of one chain of RP dependent loads)
+  constexpr int kFinLanes = 8;
+  const int sub = threadIdx.x & (kFinLanes - 1);
   const int64_t total = (int64_t)d * m * m;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int l = (int)(e / ((int64_t)m * m));
-    const int ij = (int)(e % ((int64_t)m * m));
-    const int j = ij % m;
+  const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / kFinLanes;
+  for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kFinLanes; e < total + groups - 1 - (total + groups - 1) % groups; e += groups) {
+    const bool live = e < total;
+    const int l = live ? (int)(e / ((int64_t)m * m)) : 0;
+    const int ij = live ? (int)(e % ((int64_t)m * m)) : 0;
     double2 s = make_double2(0.0, 0.0);
-    for (int P = 0; P < RP; ++P) {
-      const double2 v = Spart[((size_t)l * RP + P) * m * m + ij];
-      s.x += v.x;
-      s.y += v.y;
+    if (live)
+      for (int P = sub; P < RP; P += kFinLanes) {
+        const double2 v = __ldcg(Spart + ((size_t)l * RP + P) * m * m + ij);
+        s.x += v.x;
+        s.y += v.y;
+      }
+#pragma unroll
+    for (int off = kFinLanes / 2; off > 0; off >>= 1) {
+      s.x += __shfl_down_sync(0xffffffffu, s.x, off, kFinLanes);
+      s.y += __shfl_down_sync(0xffffffffu, s.y, off, kFinLanes);
     }
-    const double inv = 1.0 / sigma[j];
-    S[e] = make_double2(s.x * inv, s.y * inv);
+    if (live && sub == 0) {
+      const double inv = 1.0 / sigma[ij % m];
+      S[e] = make_double2(s.x * inv, s.y * inv);
+    }
   }
 }
 
@@ -865,7 +878,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   }
   if (lrc != PRONY_OK) return lrc;
   const int64_t tot = (int64_t)g.d * g.m * g.m;
-  k_finalize<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256, 0, st>>>(g.d, g.m, pl.RP, Spart, sigma, S,
+  k_finalize<<<(int)std::min<int64_t>((8 * tot + 255) / 256, 4096), 256, 0, st>>>(g.d, g.m, pl.RP, Spart, sigma, S,
                                                                                   g.N, dev_status);
   if (info) {
     info->launches = (g.shared ? 5 : 4) + (split ? 2 : 0);  // k_prep (+ k_prep_ext), k_project, k_reduce,

@@ -177,36 +177,56 @@ __global__ void __launch_bounds__(kVlsThreads, 1) k_vls(VlsParams p) {
   if (lead && tid < m) p.bpart[(size_t)cb * m + tid] = bacc;
 }
 
-// G[i][j] = sum_c G_part[c][i][j] for j <= i (fixed order), G[j][i] = conj(G[i][j]); b likewise
+// G[i][j] = sum_c G_part[c][i][j] for j <= i, G[j][i] = conj(G[i][j]); b likewise. One WARP per output: lane l
+// sums the partials c = l, l + 32, ... in order, then a fixed shuffle tree (deterministic; 32 independent
+// load streams per output instead of one serial chain of CB dependent loads)
 __global__ void k_ls_reduce(int m, int CB, const double2* __restrict__ Gpart, const double2* __restrict__ bpart,
                             double2* __restrict__ G, double2* __restrict__ b) {
-  const int tot = m * m + m;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
-    double2 s = make_double2(0.0, 0.0);
-    if (e < m * m) {
-      const int i = e / m, j = e % m;
-      const int src = j <= i ? e : j * m + i;
-      for (int c = 0; c < CB; ++c) s = cadd(s, __ldcg(Gpart + (size_t)c * m * m + src));
-      G[e] = j <= i ? s : cconj(s);
+  const int lane = threadIdx.x & 31;
+  const int tri = m * (m + 1) / 2;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int o = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < tri + m; o += nwarps) {
+    const double2* src;
+    size_t stride;
+    int i = 0, j = 0;
+    if (o < tri) {
+      i = (int)((sqrt(8.0 * o + 1.0) - 1.0) * 0.5);
+      while (i * (i + 1) / 2 > o) --i;
+      while ((i + 1) * (i + 2) / 2 <= o) ++i;
+      j = o - i * (i + 1) / 2;
+      src = Gpart + (size_t)i * m + j;
+      stride = (size_t)m * m;
     } else {
-      const int i = e - m * m;
-      for (int c = 0; c < CB; ++c) s = cadd(s, __ldcg(bpart + (size_t)c * m + i));
-      b[i] = s;
+      src = bpart + (o - tri);
+      stride = (size_t)m;
+    }
+    double2 s = make_double2(0.0, 0.0);
+    for (int c = lane; c < CB; c += 32) s = cadd(s, __ldcg(src + (size_t)c * stride));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      s.x += __shfl_down_sync(0xffffffffu, s.x, off);
+      s.y += __shfl_down_sync(0xffffffffu, s.y, off);
+    }
+    if (lane == 0) {
+      if (o < tri) {
+        G[(size_t)i * m + j] = s;
+        if (j != i) G[(size_t)j * m + i] = cconj(s);
+      } else {
+        b[o - tri] = s;
+      }
     }
   }
 }
 
-// One CTA of kSolveThreads (8 warps). Blocked right-looking Cholesky G = L L^H, the lower triangle packed in
-// shared memory (A[i][k] at i(i+1)/2 + k). Per panel of kPanel columns:
-//   1. warp 0 factors the panel (rows p0..m-1) in registers — lane owns rows p0 + lane + 32 q — with the
-//      pivots and the panel's own L entries broadcast by shuffles: no CTA barrier inside the panel;
-//   2. one barrier, then all warps apply the rank-kPanel update to the trailing triangle
-//      (A[i][k] -= sum_jj L[i][jj] conj(L[k][jj]); warp per row, lanes over columns);
-//   3. one barrier.
-// So the factorization has 2 ceil(m / kPanel) CTA barriers instead of m. Then L y = b, L^H x = y in one warp
-// with the right-hand side in registers (column-oriented, y_j broadcast by shuffle), c = conj(x) (R10),
+// One CTA of kSolveThreads (16 warps). Blocked right-looking Cholesky G = L L^H, the lower triangle packed in
+// shared memory (A[i][k] at i(i+1)/2 + k), in panels of kPanel columns [p0, p0 + pb):
+//   1. warp 0 factors the diagonal block A11 = L11 L11^H (lane r owns row p0 + r; pivots and columns are
+//      broadcast by shuffles; 1/L_jj by rsqrt, kept in dinv);
+//   2. every thread solves its rows of L21 = A21 L11^{-H} (rows are independent: L11 is read as broadcasts);
+//   3. all warps apply the rank-pb update A22 -= L21 L21^H (warp per row, lanes over columns).
+// Three CTA barriers per panel. The substitutions L y = b and L^H x = y are blocked the same way: warp 0
+// solves the pb x pb diagonal block with shuffles, then every thread updates its rows. c = conj(x) (R10),
 // t = (-arg z / 2 pi) mod 1 (R4). A pivot that is not > 0 (G not HPD) sets PRONY_ERR_SINGULAR, c = NaN.
-constexpr int kSolveMaxRowsPerLane = (PRONY_MAX_M + 31) / 32;
 constexpr int kPanel = 8;
 __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const double2* __restrict__ G,
                                                          const double2* __restrict__ b,
@@ -214,6 +234,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const dou
                                                          double* __restrict__ t, int32_t* status) {
   extern __shared__ __align__(16) double2 As[];  // m(m+1)/2 packed lower triangle
   __shared__ double dinv[PRONY_MAX_M];            // 1 / L_jj (the substitutions never divide)
+  __shared__ double2 ys[PRONY_MAX_M];             // right-hand side -> y -> x
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int kWarps = kSolveThreads / 32;
@@ -224,6 +245,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const dou
   if (tid == 0) bad = 0;
   for (int i = warp; i < m; i += kWarps)
     for (int k = lane; k <= i; k += 32) As[at(i, k)] = G[(size_t)i * m + k];
+  for (int i = tid; i < m; i += kSolveThreads) ys[i] = b[i];
   __syncthreads();
 #ifdef PRONY_SOLVE_TIMING
   const long long clk_load = clock64() - clk0;
@@ -234,73 +256,75 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const dou
 #ifdef PRONY_SOLVE_TIMING
     clk_tmp = clock64();
 #endif
+    // 1. diagonal block
     if (warp == 0) {
-      const int qn = (m - p0 + 31) >> 5;  // row groups this panel spans (warp-uniform)
-      double2 pr[kSolveMaxRowsPerLane][kPanel];
+      const int i = p0 + lane;
+      double2 r[kPanel];
 #pragma unroll
-      for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
-        const int i = p0 + lane + 32 * q;
-#pragma unroll
-        for (int jj = 0; jj < kPanel; ++jj)
-          pr[q][jj] = (q < qn && i < m && jj < pb && p0 + jj <= i) ? As[at(i, p0 + jj)] : make_double2(0.0, 0.0);
-      }
+      for (int jj = 0; jj < kPanel; ++jj)
+        r[jj] = (lane < pb && jj <= lane) ? As[at(i, p0 + jj)] : make_double2(0.0, 0.0);
       bool fail = false;
 #pragma unroll
       for (int jj = 0; jj < kPanel; ++jj) {
         if (jj < pb) {
-          const int j = p0 + jj;
-          const double djj = __shfl_sync(0xffffffffu, pr[0][jj].x, jj);  // row j = p0 + jj lives in lane jj
+          const double djj = __shfl_sync(0xffffffffu, r[jj].x, jj);
           if (!(djj > 0.0)) fail = true;
-          const double inv = rsqrt(djj), ljj = djj * inv;  // 1 / sqrt(d_j), sqrt(d_j): no divide on the chain
-          if (lane == 0) dinv[j] = inv;
-#pragma unroll
-          for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
-            if (q < qn) {
-              const int i = p0 + lane + 32 * q;
-              if (i == j) pr[q][jj] = make_double2(ljj, 0.0);
-              else if (i > j) pr[q][jj] = make_double2(pr[q][jj].x * inv, pr[q][jj].y * inv);
-            }
-          }
-          // L[p0 + kk][j] of the panel's later columns live in lanes kk (q = 0): fetch them all first
-          double lkx[kPanel], lky[kPanel];
+          const double inv = rsqrt(djj), ljj = djj * inv;
+          if (lane == 0) dinv[p0 + jj] = inv;
+          if (lane == jj) r[jj] = make_double2(ljj, 0.0);
+          else if (lane > jj) r[jj] = make_double2(r[jj].x * inv, r[jj].y * inv);
 #pragma unroll
           for (int kk = 0; kk < kPanel; ++kk) {
-            lkx[kk] = __shfl_sync(0xffffffffu, pr[0][jj].x, kk);
-            lky[kk] = __shfl_sync(0xffffffffu, pr[0][jj].y, kk);
-          }
-#pragma unroll
-          for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
-            if (q < qn) {
-              const int i = p0 + lane + 32 * q;
-              const double2 li = pr[q][jj];
-#pragma unroll
-              for (int kk = 0; kk < kPanel; ++kk) {
-                if (kk > jj && kk < pb && i >= p0 + kk && i < m) {  // A[i][k] -= L[i][j] conj(L[k][j])
-                  pr[q][kk].x -= li.x * lkx[kk] + li.y * lky[kk];
-                  pr[q][kk].y -= li.y * lkx[kk] - li.x * lky[kk];
-                }
+            if (kk > jj && kk < pb) {
+              const double lkx = __shfl_sync(0xffffffffu, r[jj].x, kk);  // L[p0 + kk][p0 + jj]
+              const double lky = __shfl_sync(0xffffffffu, r[jj].y, kk);
+              if (lane >= kk && lane < pb) {
+                r[kk].x -= r[jj].x * lkx + r[jj].y * lky;
+                r[kk].y -= r[jj].y * lkx - r[jj].x * lky;
               }
             }
           }
         }
       }
 #pragma unroll
-      for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
-        const int i = p0 + lane + 32 * q;
-#pragma unroll
-        for (int jj = 0; jj < kPanel; ++jj)
-          if (i < m && jj < pb && p0 + jj <= i) As[at(i, p0 + jj)] = pr[q][jj];
-      }
+      for (int jj = 0; jj < kPanel; ++jj)
+        if (lane < pb && jj <= lane) As[at(i, p0 + jj)] = r[jj];
       if (fail && lane == 0) bad = 1;
+    }
+    __syncthreads();
+    if (bad) break;
+    // 2. L21 = A21 L11^{-H}, one row per thread
+    const int t0 = p0 + pb;
+    for (int i = t0 + tid; i < m; i += kSolveThreads) {
+      double2 x[kPanel];
+#pragma unroll
+      for (int jj = 0; jj < kPanel; ++jj) x[jj] = jj < pb ? As[at(i, p0 + jj)] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int jj = 0; jj < kPanel; ++jj) {
+        if (jj < pb) {
+          double2 a = x[jj];
+#pragma unroll
+          for (int tt = 0; tt < kPanel; ++tt) {
+            if (tt < jj) {  // a -= L[i][p0+tt] conj(L[p0+jj][p0+tt])
+              const double2 l = As[at(p0 + jj, p0 + tt)];
+              a.x -= x[tt].x * l.x + x[tt].y * l.y;
+              a.y -= x[tt].y * l.x - x[tt].x * l.y;
+            }
+          }
+          const double inv = dinv[p0 + jj];
+          x[jj] = make_double2(a.x * inv, a.y * inv);
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < kPanel; ++jj)
+        if (jj < pb) As[at(i, p0 + jj)] = x[jj];
     }
     __syncthreads();
 #ifdef PRONY_SOLVE_TIMING
     clk_panel += clock64() - clk_tmp;
     clk_tmp = clock64();
 #endif
-    if (bad) break;
-    // trailing update of rows/columns >= p0 + pb
-    const int t0 = p0 + pb;
+    // 3. trailing update of rows/columns >= t0
     for (int i = t0 + warp; i < m; i += kWarps) {
       double2 li[kPanel];
 #pragma unroll
@@ -330,64 +354,84 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(int d, int m, const dou
   if (bad) {
     if (tid == 0) set_status(status, PRONY_ERR_SINGULAR);
     for (int i = tid; i < m; i += kSolveThreads) c[i] = make_double2(NAN, NAN);
-  } else if (warp == 0) {
-    double2 y[kSolveMaxRowsPerLane];
+  } else {
+    // forward L y = b, blocked: warp 0 solves the diagonal block, then every thread updates its rows below
+    for (int p0 = 0; p0 < m; p0 += kPanel) {
+      const int pb = min(kPanel, m - p0);
+      if (warp == 0) {
+        double2 y = lane < pb ? ys[p0 + lane] : make_double2(0.0, 0.0);
 #pragma unroll
-    for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
-      const int i = lane + 32 * q;
-      y[q] = i < m ? b[i] : make_double2(0.0, 0.0);
-    }
-    // forward: L y = b, column oriented: y_j /= L_jj; y_i -= L_ij y_j (i > j)
-    for (int j = 0; j < m; ++j) {
-      const int qj = j >> 5, lj = j & 31;
-      double2 yj = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int q = 0; q < kSolveMaxRowsPerLane; ++q)
-        if (q == qj) yj = y[q];
-      yj.x = __shfl_sync(0xffffffffu, yj.x, lj);
-      yj.y = __shfl_sync(0xffffffffu, yj.y, lj);
-      const double ij = dinv[j];
-      yj = make_double2(yj.x * ij, yj.y * ij);
-#pragma unroll
-      for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
-        const int i = lane + 32 * q;
-        if (i == j) y[q] = yj;
-        if (i > j && i < m) {
-          const double2 l = As[at(i, j)];
-          y[q].x -= l.x * yj.x - l.y * yj.y;
-          y[q].y -= l.x * yj.y + l.y * yj.x;
+        for (int jj = 0; jj < kPanel; ++jj) {
+          if (jj < pb) {
+            double yjx = __shfl_sync(0xffffffffu, y.x, jj), yjy = __shfl_sync(0xffffffffu, y.y, jj);
+            const double inv = dinv[p0 + jj];
+            yjx *= inv;
+            yjy *= inv;
+            if (lane == jj) y = make_double2(yjx, yjy);
+            if (lane > jj && lane < pb) {
+              const double2 l = As[at(p0 + lane, p0 + jj)];
+              y.x -= l.x * yjx - l.y * yjy;
+              y.y -= l.x * yjy + l.y * yjx;
+            }
+          }
         }
+        if (lane < pb) ys[p0 + lane] = y;
       }
-    }
-    // backward: L^H x = y: x_j = y_j / L_jj; y_i -= conj(L_ji) x_j (i < j)
-    for (int j = m - 1; j >= 0; --j) {
-      const int qj = j >> 5, lj = j & 31;
-      double2 xj = make_double2(0.0, 0.0);
+      __syncthreads();
+      for (int i = p0 + pb + tid; i < m; i += kSolveThreads) {
+        double2 a = ys[i];
 #pragma unroll
-      for (int q = 0; q < kSolveMaxRowsPerLane; ++q)
-        if (q == qj) xj = y[q];
-      xj.x = __shfl_sync(0xffffffffu, xj.x, lj);
-      xj.y = __shfl_sync(0xffffffffu, xj.y, lj);
-      const double ij = dinv[j];
-      xj = make_double2(xj.x * ij, xj.y * ij);
-#pragma unroll
-      for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
-        const int i = lane + 32 * q;
-        if (i == j) y[q] = xj;
-        if (i < j) {
-          const double2 a = As[at(j, i)];  // conj(L_ji)
-          y[q].x -= a.x * xj.x + a.y * xj.y;
-          y[q].y -= a.x * xj.y - a.y * xj.x;
+        for (int jj = 0; jj < kPanel; ++jj) {
+          if (jj < pb) {
+            const double2 l = As[at(i, p0 + jj)], yj = ys[p0 + jj];
+            a.x -= l.x * yj.x - l.y * yj.y;
+            a.y -= l.x * yj.y + l.y * yj.x;
+          }
         }
+        ys[i] = a;
       }
+      __syncthreads();
     }
+    // backward L^H x = y, blocked from the last block: x_j = (y_j - sum_{i > j} conj(L_ij) x_i) / L_jj
+    for (int p0 = ((m - 1) / kPanel) * kPanel; p0 >= 0; p0 -= kPanel) {
+      const int pb = min(kPanel, m - p0);
+      if (warp == 0) {
+        double2 x = lane < pb ? ys[p0 + lane] : make_double2(0.0, 0.0);
 #pragma unroll
-    for (int q = 0; q < kSolveMaxRowsPerLane; ++q) {
-      const int i = lane + 32 * q;
-      if (i < m) c[i] = cconj(y[q]);
+        for (int jj = kPanel - 1; jj >= 0; --jj) {
+          if (jj < pb) {
+            double xjx = __shfl_sync(0xffffffffu, x.x, jj), xjy = __shfl_sync(0xffffffffu, x.y, jj);
+            const double inv = dinv[p0 + jj];
+            xjx *= inv;
+            xjy *= inv;
+            if (lane == jj) x = make_double2(xjx, xjy);
+            if (lane < jj) {  // x_lane -= conj(L[p0+jj][p0+lane]) x_jj
+              const double2 l = As[at(p0 + jj, p0 + lane)];
+              x.x -= l.x * xjx + l.y * xjy;
+              x.y -= l.x * xjy - l.y * xjx;
+            }
+          }
+        }
+        if (lane < pb) ys[p0 + lane] = x;
+      }
+      __syncthreads();
+      for (int i = tid; i < p0; i += kSolveThreads) {
+        double2 a = ys[i];
+#pragma unroll
+        for (int jj = 0; jj < kPanel; ++jj) {
+          if (jj < pb) {
+            const double2 l = As[at(p0 + jj, i)], xj = ys[p0 + jj];  // conj(L[p0+jj][i]) x_jj
+            a.x -= l.x * xj.x + l.y * xj.y;
+            a.y -= l.x * xj.y - l.y * xj.x;
+          }
+        }
+        ys[i] = a;
+      }
+      __syncthreads();
     }
+    for (int i = tid; i < m; i += kSolveThreads) c[i] = cconj(ys[i]);
 #ifdef PRONY_SOLVE_TIMING
-    if (lane == 0)
+    if (tid == 0)
       printf("k_solve m=%d clocks: load %lld panels %lld updates %lld substitution %lld total %lld\n", m, clk_load,
              clk_panel, clk_upd, clock64() - clk_fact, clock64() - clk0);
 #endif
@@ -515,7 +559,8 @@ int ls_launch(int d, int n, int m, int N, const double2* z, const double2* grid,
   if (rc != PRONY_OK) return rc;
   if (info && info->ev_main_end) cudaEventRecord((cudaEvent_t)info->ev_main_end, st);
   int launches = 3;
-  k_ls_reduce<<<(m * m + m + 255) / 256, 256, 0, st>>>(m, p.CB, Gpart, bpart, G, b);
+  k_ls_reduce<<<std::max(1, std::min(2 * sm_count, (m * (m + 1) / 2 + m + 7) / 8)), 256, 0, st>>>(m, p.CB, Gpart,
+                                                                                                   bpart, G, b);
   if (col_begin == 0 && col_end == N && (c || t)) {
     // only t requested: solve into the (now consumed) G partial buffer
     rc = ls_solve_launch(d, m, G, b, z, c ? c : Gpart, t, nullptr, status, st);

@@ -14,7 +14,7 @@ constexpr int kMaxM = PRONY_MAX_M;
 #endif
 constexpr int kTile = PRONY_VLS_TILE;  // columns of A per smem tile of k_vls
 constexpr int kVlsThreads = 512;   // 16 warps (DMMA warp engine)
-constexpr int kSolveThreads = 256;
+constexpr int kSolveThreads = 512;
 
 constexpr int kVlsMaxUnits = 32;  // lower-triangle warp units (m <= 128 needs 20 at 4 n-tiles each)
 

@@ -120,18 +120,22 @@ def h2d_bytes(d: int, n: int, m: int, world: int, rank: int, order: int = UNITS_
     return ((2 * n + 2) ** d + (vrows + (uhi - ulo)) * m + m * d) * 16 + m * 8
 
 
-def allgather_rows(buf: torch.Tensor, world: int, rank: int) -> None:
-    """buf: (chunk * world, ...) with rank r's rows at [r * chunk, (r + 1) * chunk); afterwards every rank
-    holds all of them (one all_gather; in place over NCCL)."""
-    if world == 1:
-        return
+def allgather_rows(buf: torch.Tensor, world: int, rank: int, mine: torch.Tensor | None = None) -> None:
+    """buf: (chunk * world, ...); this rank's rows are in `mine` (chunk, ...) — or already at
+    [rank * chunk, (rank + 1) * chunk) of buf when mine is None. Afterwards every rank holds all of them
+    in buf (one all_gather, out of place from `mine`)."""
     chunk = buf.shape[0] // world
-    parts = list(buf.view(world, chunk, *buf.shape[1:]).unbind(0))
+    if mine is None:
+        mine = buf[rank * chunk:(rank + 1) * chunk].clone()
+    if world == 1:
+        buf.copy_(mine)
+        return
     real = (lambda x: torch.view_as_real(x)) if buf.is_complex() else (lambda x: x)
     if dist.get_backend() == "nccl":
-        dist.all_gather_into_tensor(real(buf), real(parts[rank]))
+        dist.all_gather_into_tensor(real(buf), real(mine))
     else:
-        dist.all_gather([real(p) for p in parts], real(parts[rank].clone()))
+        parts = list(buf.view(world, chunk, *buf.shape[1:]).unbind(0))
+        dist.all_gather([real(p) for p in parts], real(mine))
 
 
 class DistributedPencil:
@@ -165,6 +169,8 @@ class DistributedPencil:
         # the projection runs on a HIGH-priority stream, the LS step on a normal-priority side stream: the LS
         # CTAs fill the SMs the projection's last wave leaves idle without delaying any projection CTA
         self.hi = torch.cuda.Stream(device=device, priority=-1)
+        self.ctx = None  # prony_host_context of the single-rank one-call path (created on first use)
+        self.outs = {"S": self.S, "G": self.G, "b": self.b, "c": self.c, "t": self.t}
         self.side = torch.cuda.Stream(device=device)
         self.ev_in = torch.cuda.Event()
         self.ev_ls = torch.cuda.Event()
@@ -172,36 +178,61 @@ class DistributedPencil:
     def __call__(self, grid, U, V, sigma, z, stream=None, info_p=None, info_l=None, ev_comm=None):
         """Device-resident inputs -> (S, c, t) (views of this object's buffers, valid until the next call).
         Ordered after prior work on `stream` (default: the current stream), which is ordered after all of it
-        on return. ev_comm: optional (begin, end) CUDA events recorded around the collective."""
+        on return. ev_comm: optional (begin, end) CUDA events recorded around the collective of S.
+
+        N > 1: the LS branch (side stream) all-reduces its G, b as soon as they are done and solves for c, t
+        there, while the projection (high-priority stream) is still running; only the all-reduce of S is left
+        on the projection's critical path."""
         pb, d, n, m = self.pb, self.d, self.n, self.m
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
-        hi = self.hi
+        full = self.world == 1
+        if full and self.order == UNITS_SHARED:
+            # one C call (prony_pencil): the projection on `main`, the LS step on the context's side stream
+            if self.ctx is None:
+                self.ctx = pb.HostContext()
+                self.ws_pencil = pb.alloc_workspace(pb.WS_PENCIL, d, n, m, self.device)
+            with torch.cuda.stream(main):
+                self.status.zero_()
+            pb.pencil(grid, U, V, sigma, z, d, n, m, self.outs, self.ws_pencil, context=self.ctx,
+                      dev_status=self.status, stream=main, info_p=info_p, info_l=info_l)
+            return self.S, self.c, self.t
+        hi, side = self.hi, self.side
         hi.wait_stream(main)
         with torch.cuda.stream(hi):
             self.status.zero_()
             self.ev_in.record(hi)
             pb.project(grid, U, V, sigma, d, n, m, self.u0, self.u1, self.order, out=self.S, workspace=self.ws_p,
                        dev_status=self.status, stream=hi, info=info_p)
-            full = self.world == 1
-            self.side.wait_event(self.ev_in)
+        side.wait_event(self.ev_in)
+        with torch.cuda.stream(side):
             res = pb.vandermonde_ls(z, grid, d, n, m, self.c0, self.c1, want_solution=full,
                                     out={"G": self.G, "b": self.b, "c": self.c, "t": self.t}, workspace=self.ws_l,
-                                    dev_status=self.status, stream=self.side, info=info_l)
-            self.ev_ls.record(self.side)
+                                    dev_status=self.status, stream=side, info=info_l)
+            if not full:
+                self._allreduce(self.buf[d * m * m:])            # G, b
+                pb.ls_solve(self.G, self.b, z, d, m, dev_status=self.status, stream=side,
+                            out={"c": self.c, "t": self.t})
+            self.ev_ls.record(side)
+        with torch.cuda.stream(hi):
+            if not full:
+                if ev_comm is not None:
+                    ev_comm[0].record(hi)
+                self._allreduce(self.buf[:d * m * m])            # S
+                if ev_comm is not None:
+                    ev_comm[1].record(hi)
             hi.wait_event(self.ev_ls)
-            if full:
-                out = (self.S, res["c"], res["t"])
-            else:
-                out = self._reduce_and_solve(z, hi, ev_comm)
         main.wait_stream(hi)
-        return out
+        return self.S, (res["c"] if full else self.c), (res["t"] if full else self.t)
+
+    def _allreduce(self, x):
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            dist.all_reduce(torch.view_as_real(x), op=dist.ReduceOp.SUM)
 
     def _reduce_and_solve(self, z, st, ev_comm=None):
         pb, d, m = self.pb, self.d, self.m
         if ev_comm is not None:
             ev_comm[0].record(st)
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-            dist.all_reduce(torch.view_as_real(self.buf), op=dist.ReduceOp.SUM)
+        self._allreduce(self.buf)
         if ev_comm is not None:
             ev_comm[1].record(st)
         c, t = pb.ls_solve(self.G, self.b, z, d, m, dev_status=self.status, stream=st, out={"c": self.c, "t": self.t})
@@ -231,6 +262,7 @@ class DistributedPencil:
             self.dsig = torch.empty(m, dtype=torch.float64, device=dev)
             self.dU = torch.zeros((self.N, m), dtype=torch.complex128, device=dev)
             self.dVpad = torch.zeros((chunk * self.world, m), dtype=torch.complex128, device=dev)
+            self.dVmine = torch.zeros((chunk, m), dtype=torch.complex128, device=dev)
         with torch.cuda.stream(main):
             self.dz.copy_(z_h, non_blocking=True)
             if not scatter_v:
@@ -252,7 +284,7 @@ class DistributedPencil:
             if uhi > ulo:
                 self.dU[ulo:uhi].copy_(U_h[ulo:uhi], non_blocking=True)
             if v1 > v0:
-                self.dVpad[v0:v1].copy_(V_h[v0:v1], non_blocking=True)
-            allgather_rows(self.dVpad, self.world, self.rank)
+                self.dVmine[:v1 - v0].copy_(V_h[v0:v1], non_blocking=True)
+            allgather_rows(self.dVpad, self.world, self.rank, self.dVmine)
             V = self.dVpad[:self.N]
         return self(self.dgrid, self.dU, V, self.dsig, self.dz, stream=main, ev_comm=ev_comm)

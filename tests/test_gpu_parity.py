@@ -590,3 +590,40 @@ def test_pencil_host_part_empty_and_partial(pb, orc):
     A = orc.vandermonde(prob.z, d, n, 11, N - 9)
     G_or, b_or = orc.ls_products(A, prob.grid, d, n, 11, N - 9)
     assert rel(G, G_or) <= TOL and rel(b, b_or) <= TOL
+
+
+def test_pencil_one_call_and_graph_replay(pb, orc):
+    """prony_pencil (one C call: projection on the stream, LS + solve on the context's side stream) through
+    sharding.DistributedPencil at N = 1, eager and captured once in a CUDA graph then replayed on new inputs
+    copied into the same buffers: S, G, b, c, t against the oracle each time."""
+    probs = [problem(2, 18, 11, 1700 + i, 1e-6, random_uv=True) for i in range(2)]
+    c0 = probs[0].cfg
+    d, n, m = c0.d, c0.n, c0.m
+    bufs = {k: dev(getattr(probs[0], k)) for k in ("grid", "U", "V", "sigma", "z")}
+    pencil = pb.sharding.DistributedPencil(d, n, m, torch.device("cuda", 0))
+    st = torch.cuda.Stream()
+
+    def check(prob, S, c, t):
+        S_or = orc.project(prob.grid, prob.U, prob.V, prob.sigma, d, n)
+        for l in range(d):
+            assert rel(S[l], S_or[l]) <= TOL
+        A_or = orc.vandermonde(prob.z, d, n)
+        G_or, b_or = orc.ls_products(A_or, prob.grid, d, n)
+        assert rel(pencil.G, G_or) <= TOL and rel(pencil.b, b_or) <= TOL
+        assert rel(c, orc.cholesky_solve(G_or, b_or)) <= 1e-9
+        assert np.max(np.abs(t.cpu().numpy() - orc.t_from_z(prob.z))) <= 1e-12
+        assert int(pencil.status.item()) == 0
+
+    with torch.cuda.stream(st):
+        S, c, t = pencil(bufs["grid"], bufs["U"], bufs["V"], bufs["sigma"], bufs["z"], stream=st)
+    torch.cuda.synchronize()
+    check(probs[0], S, c, t)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=st):
+        S, c, t = pencil(bufs["grid"], bufs["U"], bufs["V"], bufs["sigma"], bufs["z"], stream=st)
+    for prob in probs[::-1]:
+        for k in bufs:
+            bufs[k].copy_(torch.from_numpy(np.ascontiguousarray(getattr(prob, k))))
+        graph.replay()
+        torch.cuda.synchronize()
+        check(prob, S, c, t)

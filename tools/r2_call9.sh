@@ -1,0 +1,17 @@
+#!/bin/bash
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { echo BUILD FAILED; tail -30 gpurun_out/build.log; exit 1; }
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r2_call9_tests.log 2>&1; echo "pytest gpu rc=$?"; tail -3 gpurun_out/r2_call9_tests.log
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r2_bench9.log 2>&1; echo "bench rc=$?"
+python - << 'PY'
+import json; j = json.loads([l for l in open("gpurun_out/r2_bench9.log") if l.startswith("{")][-1])
+print("value", j["value"], "ms", j["ms_per_step"], "kernels", j["kernels_ms"], "frac", j["roofline"]["frac"], "e2e", j["e2e"]["value"], "launches", j["gpu_launches"])
+PY
+for c in cfg1 cfg2 cfg3 cfg5; do timeout 300 python bench.py --cfg $c --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/r2_bench9_$c.log 2>&1
+python - $c << 'PY'
+import json, sys; j = json.loads([l for l in open(f"gpurun_out/r2_bench9_{sys.argv[1]}.log") if l.startswith("{")][-1])
+print(sys.argv[1], "value", round(j["value"],2), "ms", round(j["ms_per_step"],4), "k_project", round(j["kernels_ms"]["k_project"],4), "frac", round(j["roofline"]["frac"],3), "e2e", round(j["e2e"]["value"],2))
+PY
+done
+timeout 600 python tools/graph_bench.py cfg1 cfg2 cfg3 > gpurun_out/r2_graph_bench.jsonl 2>&1; cat gpurun_out/r2_graph_bench.jsonl
