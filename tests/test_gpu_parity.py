@@ -93,6 +93,20 @@ def test_project_edge_shapes(pb, orc, d, n, m, noise, order):
         assert rel(S[l], S_or[l]) <= TOL
 
 
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 7, 8, 9, 12, 13, 20, 36, 44, 76, 80, 81, 84, 97, 100, 101, 104, 105, 124, 128])
+def test_project_packed_last_tile_every_m_class(pb, orc, m):
+    """k_project packs the last n-tile (2 real products, 4M form) exactly when m % 8 is 1..4: every residue
+    class of m, both consumer layouts (m <= 80: 2 column warps; m > 80: 3), both complex modes of the
+    other tiles' engine, against the oracle. N = 169 > m, ragged row blocks."""
+    d, n = 2, 12
+    prob = problem(d, n, m, 2000 + m, 1e-6, random_uv=True)
+    S = run_project(pb, prob)
+    torch.cuda.synchronize()
+    S_or = orc.project(prob.grid, prob.U, prob.V, prob.sigma, d, n)
+    for l in range(d):
+        assert rel(S[l], S_or[l]) <= TOL
+
+
 def test_project_shared_random_partitions(pb, orc):
     """Random partitions of the SHARED unit space [0, (n+2)^d) over 2-9 'ranks' sum to the full pencil
     (the multi-GPU decomposition), each partial equal to the oracle's rows of T_l it stands for."""
