@@ -24,7 +24,7 @@ __device__ __forceinline__ void mma16x8x4(double (&c)[4], double a0, double a1, 
 // MODE 3 (3M): acc0 += Ar Br, acc1 += Ai Bi, acc2 += (Ar+Ai)(Br+Bi)
 // MODE 4 (4M): acc0 += Ar Br - Ai Bi, acc1 += Ar Bi + Ai Br
 // NA <= NT n-tiles are active (compile-time, so no predicated MMAs).
-// PK (packed last n-tile, MODE 3, CONJB = false only): n-tile NA-1 holds w = m % 8 <= 4 valid columns; it is
+// PK (packed last n-tile, MODE 3): n-tile NA-1 holds w = m % 8 <= 4 valid columns; it is
 // computed as Ar [Br | Bi] (acc0) and Ai [Br | Bi] (acc1) on ONE 8-wide B fragment — lane column g reads
 // column (g & 3) of the tile, the real part for g < 4 and the imaginary part for g >= 4 — so 2 real DMMA
 // products instead of the 3 of a half-empty 3M tile; acc_packed_to_complex recombines (4M form).
@@ -46,26 +46,36 @@ __device__ __forceinline__ void warp_cmma_k4(double (&acc)[3][NT][4], const doub
   constexpr double sb = CONJB ? -1.0 : 1.0;
 #pragma unroll
   for (int j = 0; j < NA; ++j) {
-    if constexpr (PK && MODE == 3 && !CONJB) {
+#ifdef PRONY_PK_IFELSE
+    if (PK && MODE == 3 && j == NA - 1) {
+#else
+    if constexpr (PK && MODE == 3) {
       if (j == NA - 1) {
+#endif
         const double2 bb = brow[8 * j - (g & 4)];  // column 8j + (g & 3) of the tile
         const double bp = (g & 4) ? bb.y : bb.x;
         mma16x8x4(acc[0][j], a0.x, a1.x, bp);
         mma16x8x4(acc[1][j], a0.y, a1.y, bp);
+#ifdef PRONY_PK_IFELSE
+    } else {
+#else
         continue;
       }
     }
-    const double2 b = brow[8 * j];
-    if constexpr (MODE == 3) {
-      const double bs = bsrow[8 * j];
-      mma16x8x4(acc[0][j], a0.x, a1.x, b.x);
-      mma16x8x4(acc[1][j], sb * a0.y, sb * a1.y, b.y);  // Ai (sb Bi): sign folded into the A operand
-      mma16x8x4(acc[2][j], s0, s1, bs);
-    } else {
-      mma16x8x4(acc[0][j], a0.x, a1.x, b.x);
-      mma16x8x4(acc[1][j], sb * a0.x, sb * a1.x, b.y);
-      mma16x8x4(acc[0][j], -sb * a0.y, -sb * a1.y, b.y);
-      mma16x8x4(acc[1][j], a0.y, a1.y, b.x);
+    {
+#endif
+      const double2 b = brow[8 * j];
+      if constexpr (MODE == 3) {
+        const double bs = bsrow[8 * j];
+        mma16x8x4(acc[0][j], a0.x, a1.x, b.x);
+        mma16x8x4(acc[1][j], sb * a0.y, sb * a1.y, b.y);  // Ai (sb Bi): sign folded into the A operand
+        mma16x8x4(acc[2][j], s0, s1, bs);
+      } else {
+        mma16x8x4(acc[0][j], a0.x, a1.x, b.x);
+        mma16x8x4(acc[1][j], sb * a0.x, sb * a1.x, b.y);
+        mma16x8x4(acc[0][j], -sb * a0.y, -sb * a1.y, b.y);
+        mma16x8x4(acc[1][j], a0.y, a1.y, b.x);
+      }
     }
   }
 }
@@ -92,17 +102,23 @@ __device__ __forceinline__ void warp_cmma_k4_n(int nt_active, double (&acc)[3][N
 }
 
 // packed last n-tile (PK): lane q < 2 holds columns 2q, 2q+1 of Ar Br (acc0) and Ai Br (acc1); its partner
-// q + 2 (lane ^ 2) holds the same columns of Ar Bi and Ai Bi. Re = Ar Br - Ai Bi, Im = Ar Bi + Ai Br, valid on
-// lanes q < 2 (the tile's columns 0..3); lanes q >= 2 get 0 (padding columns). All 32 lanes must call it.
-template <int NT>
+// q + 2 (lane ^ 2) holds the same columns of Ar Bi and Ai Bi. A B: Re = Ar Br - Ai Bi, Im = Ar Bi + Ai Br;
+// A conj(B) (CONJB): Re = Ar Br + Ai Bi, Im = Ai Br - Ar Bi. Valid on lanes q < 2 (the tile's columns 0..3);
+// lanes q >= 2 get 0 (padding columns). All 32 lanes must call it.
+template <int NT, bool CONJB = false>
 __device__ __forceinline__ void acc_packed_to_complex(const double (&acc)[3][NT][4], int j, int q, double (&re)[4],
                                                       double (&im)[4]) {
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const double p0 = __shfl_xor_sync(0xffffffffu, acc[0][j][e], 2);
     const double p1 = __shfl_xor_sync(0xffffffffu, acc[1][j][e], 2);
-    re[e] = q < 2 ? acc[0][j][e] - p1 : 0.0;
-    im[e] = q < 2 ? p0 + acc[1][j][e] : 0.0;
+    if constexpr (CONJB) {
+      re[e] = q < 2 ? acc[0][j][e] + p1 : 0.0;
+      im[e] = q < 2 ? acc[1][j][e] - p0 : 0.0;
+    } else {
+      re[e] = q < 2 ? acc[0][j][e] - p1 : 0.0;
+      im[e] = q < 2 ? p0 + acc[1][j][e] : 0.0;
+    }
   }
 }
 

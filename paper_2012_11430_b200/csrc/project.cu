@@ -320,6 +320,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8u * s);
     }
+    // epilogue: Y[chunk][yoff_l + r][col], NP-wide rows (padding columns are zero). For NT <= 3 it runs here,
+    // where NA and PK are compile-time (with the runtime form below, ptxas turns acc[.][nt_active-1] into a
+    // dynamically indexed local-memory copy of acc for those shapes); for NT >= 4 after the dispatch
+    // (measured: 28.45 vs 28.72 ms at cfg4 for the in-lambda form).
+    if constexpr (NT <= 3) {
+      const int r0 = rb0 + wm * 16 + g, r1 = r0 + 8;
+      const size_t ybase = (size_t)chunk * p.R_tot + p.yoff[l];
+#pragma unroll
+      for (int j = 0; j < NA; ++j) {
+        double re[4], im[4];
+        if constexpr (PK) {
+          if (j == NA - 1) acc_packed_to_complex<NT>(acc, j, q, re, im);
+          else acc_to_complex<NT, MODE>(acc, j, re, im);
+        } else {
+          acc_to_complex<NT, MODE>(acc, j, re, im);
+        }
+        const int col = (t0 + j) * 8 + 2 * q;
+        if (r0 < rows) {
+          double2* y = p.Y + (ybase + r0) * NP + col;
+          y[0] = make_double2(re[0], im[0]);
+          y[1] = make_double2(re[1], im[1]);
+        }
+        if (r1 < rows) {
+          double2* y = p.Y + (ybase + r1) * NP + col;
+          y[0] = make_double2(re[2], im[2]);
+          y[1] = make_double2(re[3], im[3]);
+        }
+      }
+    }
   };
   auto run_na = [&](auto na_c) {
     if (pk) run(na_c, std::true_type{});
@@ -341,25 +370,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
     }
   }
 
-  // epilogue: Y[chunk][yoff_l + r][col], NP-wide rows (padding columns are zero)
-  const int r0 = rb0 + wm * 16 + g, r1 = r0 + 8;
-  const size_t ybase = (size_t)chunk * p.R_tot + p.yoff[l];
+  if constexpr (NT > 3) {
+    const int r0 = rb0 + wm * 16 + g, r1 = r0 + 8;
+    const size_t ybase = (size_t)chunk * p.R_tot + p.yoff[l];
 #pragma unroll
-  for (int j = 0; j < NT; ++j) {
-    if (j < nt_active) {
-      double re[4], im[4];
-      if (pk && j == nt_active - 1) acc_packed_to_complex<NT>(acc, j, q, re, im);
-      else acc_to_complex<NT, MODE>(acc, j, re, im);
-      const int col = (t0 + j) * 8 + 2 * q;
-      if (r0 < rows) {
-        double2* y = p.Y + (ybase + r0) * NP + col;
-        y[0] = make_double2(re[0], im[0]);
-        y[1] = make_double2(re[1], im[1]);
-      }
-      if (r1 < rows) {
-        double2* y = p.Y + (ybase + r1) * NP + col;
-        y[0] = make_double2(re[2], im[2]);
-        y[1] = make_double2(re[3], im[3]);
+    for (int j = 0; j < NT; ++j) {
+      if (j < nt_active) {
+        double re[4], im[4];
+        if (pk && j == nt_active - 1) acc_packed_to_complex<NT>(acc, j, q, re, im);
+        else acc_to_complex<NT, MODE>(acc, j, re, im);
+        const int col = (t0 + j) * 8 + 2 * q;
+        if (r0 < rows) {
+          double2* y = p.Y + (ybase + r0) * NP + col;
+          y[0] = make_double2(re[0], im[0]);
+          y[1] = make_double2(re[1], im[1]);
+        }
+        if (r1 < rows) {
+          double2* y = p.Y + (ybase + r1) * NP + col;
+          y[0] = make_double2(re[2], im[2]);
+          y[1] = make_double2(re[3], im[3]);
+        }
       }
     }
   }
@@ -543,6 +573,231 @@ __global__ void __launch_bounds__(kReduceThreads, 1) k_reduce(RedParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------- warp-specialized reduce
+// k_reduce_ws (3M, the default): the same S_part[l][P] = U[rows_P]^* Y[rows_P] (computed transposed,
+// S^T = Y^T conj(U)) with 8 consumer warps of 232 registers (WM = 4 along j -> 64-row j-blocks, WN = 2 along
+// i with up to 8 n-tiles per warp; the last n-tile packed when m % 8 <= 4) and the producer warpgroup feeding a kRedWsStages-deep ring of 16-row slabs: producer warp 0 moves each slab with
+// one bulk copy per Y row (columns [j0, j0 + BJ)) and per U row (through the row map; lanes 16..31 load the
+// map entries in parallel), completing on the slab's "landed" mbarrier (expect_tx); then the 4 producer
+// warps form the 3M sum planes (Re+Im of Y, Re-Im of U for the conj-B operand), zero the rows that have no
+// data, and arrive on "full"; consumers release slabs on "empty". No CTA-wide barrier in the loop, no DADD
+// on the consumer warps. Grid (RP, d, nj): every j-block takes the same row partitions (the U rows, which
+// dominate the traffic, cost the same for each); rp_j[z] < RP would make the extra CTAs write zero partials.
+constexpr int kRedWsStages = 3;
+constexpr int kRwsCons = 8;                        // consumer warps: WM = 4 along j x WN = 2 along i
+constexpr int kRwsThreads = 32 * (kRwsCons + 4);   // + the producer warpgroup
+constexpr int kRwsConsRegs = 232, kRwsProdRegs = 40;  // 256 x 232 + 128 x 40 = 64512 <= 65536
+template <int NT, int WN>
+struct RedWsTile {
+  static constexpr int WM = kRwsCons / WN;
+  static constexpr int BJ = 16 * WM;       // rows j of S^T per CTA
+  static constexpr int NPU = 8 * NT * WN;  // capacity of the i dimension
+  static constexpr int LDA = BJ + 2, LDAS = BJ + 4, LDB = NPU + 2, LDBS = NPU + 4;
+  static constexpr int A_C = 0, A_S = A_C + 2 * kRedSlab * LDA, B_C = A_S + kRedSlab * LDAS,
+                       B_S = B_C + 2 * kRedSlab * LDB, STAGE = B_S + kRedSlab * LDBS;
+  static constexpr int BAR = kRedWsStages * STAGE;                  // 3 mbarriers per stage
+  static constexpr int VAL = BAR + 3 * kRedWsStages;                // per stage: 16 U-row flags (ints)
+  static constexpr size_t SMEM = (size_t)VAL * sizeof(double) + (size_t)kRedWsStages * kRedSlab * sizeof(int);
+  static_assert(STAGE % 2 == 0 && A_S % 2 == 0 && B_C % 2 == 0 && B_S % 2 == 0, "16-byte alignment");
+  static_assert((2 * LDA) % 2 == 0 && (2 * LDB) % 2 == 0, "bulk-copy rows stay 16-byte aligned");
+};
+
+template <int NT, int WN>
+__global__ void __launch_bounds__(kRwsThreads, 1) k_reduce_ws(RedParams p) {
+  using T = RedWsTile<NT, WN>;
+  constexpr int WM = T::WM, BJ = T::BJ;
+  constexpr int kProd = kRwsThreads - kRwsCons * 32;  // producer threads
+  extern __shared__ __align__(16) double smem[];
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t full0 = sbase + (uint32_t)T::BAR * 8u, empty0 = full0 + (uint32_t)kRedWsStages * 8u,
+                 landed0 = empty0 + (uint32_t)kRedWsStages * 8u;
+  int* uval = reinterpret_cast<int*>(smem + T::VAL);  // [stage][16]: U row of the slab row, or -1
+  const int tid = threadIdx.x;
+  const int l = blockIdx.y, P = blockIdx.x, jb = blockIdx.z;
+  const int j0 = jb * BJ;
+  const int m = p.m, NP = p.NP;
+  const int RPj = p.rp_j[jb];
+  double2* out = p.Spart + ((size_t)l * p.RP + P) * m * m;
+  if (P >= RPj) {  // this j-block needs fewer partitions: its columns of this partial are zero
+    for (int e = tid; e < m * BJ; e += kRwsThreads) {
+      const int i = e / BJ, j = j0 + e % BJ;
+      if (j < m) out[(size_t)i * m + j] = make_double2(0.0, 0.0);
+    }
+    return;
+  }
+  const int rows = p.rows[l];
+  const int rbeg = (int)((int64_t)rows * P / RPj), rend = (int)((int64_t)rows * (P + 1) / RPj);
+  const int nslab = (rend - rbeg + kRedSlab - 1) / kRedSlab;
+  const int ny = min(BJ, NP - j0);  // Y columns this j-block reads
+
+  for (int e = tid; e < kRedWsStages * T::STAGE; e += kRwsThreads) smem[e] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < kRedWsStages; ++s) {
+      mbar_init(full0 + 8u * s, kProd);
+      mbar_init(empty0 + 8u * s, kRwsCons);
+      mbar_init(landed0 + 8u * s, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (tid >= kRwsCons * 32) {
+    // ================================================================== producer warpgroup
+    setmaxnreg_dec<kRwsProdRegs>();
+    const int pt = tid - kRwsCons * 32;
+    const int plane = pt & 31;
+    for (int st = 0; st <= nslab; ++st) {
+      if (st < nslab && pt < 32) {  // producer warp 0 issues slab st
+        const int s = st % kRedWsStages;
+        if (st >= kRedWsStages) mbar_wait(empty0 + 8u * s, (uint32_t)((st / kRedWsStages) - 1) & 1u);
+        const int r = plane & (kRedSlab - 1);
+        const int row = rbeg + st * kRedSlab + r;
+        uint32_t bytes = 0;
+        const double2* src = nullptr;
+        uint32_t dst = sbase + (uint32_t)(s * T::STAGE) * 8u;
+        if (plane < kRedSlab) {  // Y row
+          if (row < rend) {
+            bytes = (uint32_t)ny * 16u;
+            src = p.Y + ((size_t)p.yoff[l] + row) * NP + j0;
+          }
+          dst += (uint32_t)(T::A_C + 2 * r * T::LDA) * 8u;
+        } else {  // U row through the map
+          int urow = -1;
+          if (row < rend) {
+            urow = p.kb[l] + row;
+            if (p.umap) urow = __ldg(p.umap + (size_t)l * p.E + urow);  // -1: no row of T_l
+          }
+          uval[s * kRedSlab + r] = urow;
+          if (urow >= 0) {
+            bytes = (uint32_t)m * 16u;
+            src = p.U + (size_t)urow * m;
+          }
+          dst += (uint32_t)(T::B_C + 2 * r * T::LDB) * 8u;
+        }
+        uint32_t tot = bytes;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+        if (plane == 0) mbar_arrive_expect_tx(landed0 + 8u * s, tot);  // also publishes uval (release)
+        __syncwarp();
+        if (bytes) bulk_g2s(dst, src, bytes, landed0 + 8u * s);
+      }
+      if (st >= 1) {  // all producer warps: sum planes of slab st-1
+        const int s = (st - 1) % kRedWsStages;
+        mbar_wait(landed0 + 8u * s, (uint32_t)((st - 1) / kRedWsStages) & 1u);
+        const int r0 = rbeg + (st - 1) * kRedSlab;
+        double* sp = smem + s * T::STAGE;
+        double2* Yc = reinterpret_cast<double2*>(sp + T::A_C);
+        double2* Uc = reinterpret_cast<double2*>(sp + T::B_C);
+        for (int e = pt; e < kRedSlab * BJ; e += kProd) {
+          const int r = e / BJ, jj = e % BJ;
+          double v = 0.0;
+          if (r0 + r < rend) {
+            const double2 y = Yc[r * T::LDA + jj];
+            v = y.x + y.y;
+          } else {
+            Yc[r * T::LDA + jj] = make_double2(0.0, 0.0);  // no row: stale data of an earlier slab
+          }
+          sp[T::A_S + r * T::LDAS + jj] = v;
+        }
+        for (int e = pt; e < kRedSlab * T::NPU; e += kProd) {
+          const int r = e / T::NPU, i = e % T::NPU;
+          double v = 0.0;
+          if (uval[s * kRedSlab + r] >= 0) {
+            const double2 u = Uc[r * T::LDB + i];
+            v = u.x - u.y;  // the B operand is conj(U)
+          } else {
+            Uc[r * T::LDB + i] = make_double2(0.0, 0.0);
+          }
+          sp[T::B_S + r * T::LDBS + i] = v;
+        }
+        mbar_arrive(full0 + 8u * s);
+      }
+    }
+    return;
+  }
+
+  // ==================================================================== consumer warpgroups
+  setmaxnreg_inc<kRwsConsRegs>();
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WM, wn = warp / WM;
+  const int g = lane >> 2, q = lane & 3;
+  const int ntot = (m + 7) / 8;  // n-tiles over i
+  const int t0 = (ntot * wn) / WN;
+  const int nt_active = (ntot * (wn + 1)) / WN - t0;
+  const bool warp_rows = (j0 + wm * 16) < NP;
+  const bool pk = (m % 8) != 0 && (m % 8) <= 4 && nt_active > 0 && t0 + nt_active == ntot;
+
+  double acc[3][NT][4];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[a][j][e] = 0.0;
+
+  auto run = [&](auto na_c, auto pk_c) {
+    constexpr int NA = decltype(na_c)::value;
+    constexpr bool PK = decltype(pk_c)::value;
+    for (int st = 0; st < nslab; ++st) {
+      const int s = st % kRedWsStages;
+      mbar_wait(full0 + 8u * s, (uint32_t)(st / kRedWsStages) & 1u);
+      if constexpr (NA > 0) {
+        const double* sp = smem + s * T::STAGE;
+        const double2* Ac = reinterpret_cast<const double2*>(sp + T::A_C) + wm * 16;
+        const double* As = sp + T::A_S + wm * 16;
+        const double2* Bc = reinterpret_cast<const double2*>(sp + T::B_C) + t0 * 8;
+        const double* Bs = sp + T::B_S + t0 * 8;
+#pragma unroll
+        for (int kk = 0; kk < kRedSlab / 4; ++kk)
+          warp_cmma_k4<NT, NA, 3, true, PK>(acc, Ac + kk * 4 * T::LDA, As + kk * 4 * T::LDAS, T::LDA, T::LDAS,
+                                            Bc + kk * 4 * T::LDB, Bs + kk * 4 * T::LDBS, T::LDB, T::LDBS, g, q);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8u * s);
+    }
+    // acc rows = j, columns = i  ->  S_part[i][j] (NA, PK compile-time: static accumulator indices)
+    const int ja = j0 + wm * 16 + g, jb2 = ja + 8;
+#pragma unroll
+    for (int t = 0; t < NA; ++t) {
+      double re[4], im[4];
+      if constexpr (PK) {
+        if (t == NA - 1) acc_packed_to_complex<NT, true>(acc, t, q, re, im);
+        else acc_to_complex<NT, 3>(acc, t, re, im);
+      } else {
+        acc_to_complex<NT, 3>(acc, t, re, im);
+      }
+      const int i = (t0 + t) * 8 + 2 * q;
+      if (ja < m) {
+        if (i < m) out[(size_t)i * m + ja] = make_double2(re[0], im[0]);
+        if (i + 1 < m) out[(size_t)(i + 1) * m + ja] = make_double2(re[1], im[1]);
+      }
+      if (jb2 < m) {
+        if (i < m) out[(size_t)i * m + jb2] = make_double2(re[2], im[2]);
+        if (i + 1 < m) out[(size_t)(i + 1) * m + jb2] = make_double2(re[3], im[3]);
+      }
+    }
+  };
+  auto run_na = [&](auto na_c) {
+    if (pk) run(na_c, std::true_type{});
+    else run(na_c, std::false_type{});
+  };
+  if (!warp_rows || nt_active == 0) {
+    run(std::integral_constant<int, 0>{}, std::false_type{});
+  } else if (nt_active == NT) {
+    run_na(std::integral_constant<int, NT>{});
+  } else if constexpr (NT > 1) {
+    if (nt_active == NT - 1) {
+      run_na(std::integral_constant<int, NT - 1>{});
+    } else if constexpr (NT > 2) {
+      if (nt_active == NT - 2) {
+        run_na(std::integral_constant<int, NT - 2>{});
+      } else if constexpr (NT > 3) {
+        if (nt_active == NT - 3) run_na(std::integral_constant<int, NT - 3>{});
+      }
+    }
+  }
+}
+
 // S[l][i][j] = (sum_{p < RP} S_part[l][p][i][j]) / sigma_j   (fixed order).
 // Scale guard (SPEC compute_S "sigma_m below underflow guard"): a sigma that is not
 // finite and positive, or below N eps_M sigma_max (the rank rule of P:581), reports PRONY_ERR_SINGULAR
@@ -664,10 +919,22 @@ int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl) {
   pl->chunk_w = chunk_w;
   pl->KC = (g.N + chunk_w - 1) / chunk_w;  // every chunk non-empty
   // reduce partition: about 1 CTA per SM in total
+  const int slabs = std::max(1, (max_rows + 15) / 16);
+  if (cmul_mode() == 3) {
+    // k_reduce_ws: 64-row j-blocks, the same row partitions for each (about one CTA per SM in total)
+    const int nj = (sh.NP + 63) / 64;
+    const int rp = std::max(1, std::min(slabs, sm_count / std::max(1, g.d * nj)));
+    int rpmax = rp;
+    for (int z = 0; z < 4; ++z) pl->rp_j[z] = z < nj ? rp : 0;
+    pl->nj = nj;
+    pl->RP = rpmax;
+    return 0;
+  }
   const int ib = (sh.NP + sh.BI - 1) / sh.BI;  // j-blocks of k_reduce
   int RP = sm_count / std::max(1, g.d * ib);
-  RP = std::max(1, std::min(RP, std::max(1, (max_rows + 15) / 16)));
+  RP = std::max(1, std::min(RP, slabs));
   pl->RP = RP;
+  pl->nj = 0;
   return 0;
 }
 
@@ -696,8 +963,7 @@ WsLayout ws_layout(int d, int n, int N, int m, int sm_count) {
   w.vsum = take((size_t)N * sh.NP * sizeof(double));
   // Y partials: KC * R_tot <= kYCap * max(dN, |E|)
   w.Y = take((size_t)kYCap * std::max<int64_t>((int64_t)d * N, E) * sh.NP * sizeof(double2));
-  const int ib = (sh.NP + sh.BI - 1) / sh.BI;
-  const int RP = std::max(1, sm_count / std::max(1, d * ib));
+  const int RP = std::max(1, sm_count / std::max(1, d));  // >= the partitions of either reduce kernel
   w.Spart = take((size_t)d * RP * m * m * sizeof(double2));
   w.counters = take((size_t)d * ((std::max<int64_t>(N, E) + 15) / 16 + 1) * sizeof(int));  // split-K arrivals
   w.total = off;
@@ -729,6 +995,16 @@ static int launch_reduce_t(const RedParams& r, dim3 rgrid, cudaStream_t st, int 
     return PRONY_ERR_CUDA;
   rgrid.z = (r.NP + RedTile<NT, WN>::BJ - 1) / RedTile<NT, WN>::BJ;
   kr<<<rgrid, kReduceThreads, smem, st>>>(r);
+  return PRONY_OK;
+}
+
+template <int NT, int WN>
+static int launch_reduce_ws_t(const RedParams& r, dim3 rgrid, cudaStream_t st) {
+  const size_t smem = RedWsTile<NT, WN>::SMEM;
+  if (cudaFuncSetAttribute(k_reduce_ws<NT, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return PRONY_ERR_CUDA;
+  k_reduce_ws<NT, WN><<<rgrid, kRwsThreads, smem, st>>>(r);
   return PRONY_OK;
 }
 
@@ -824,6 +1100,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
     r.rows[l] = g.shared ? pl.R_tot : g.rows[l];
     r.yoff[l] = pl.yoff[l];
   }
+  for (int z = 0; z < 4; ++z) r.rp_j[z] = pl.rp_j[z];
   dim3 grd((pl.max_rows + pl.shape.BM - 1) / pl.shape.BM, pl.KC, pslots);
   dim3 rgrd(pl.RP, g.d, (pl.shape.NP + pl.shape.BI - 1) / pl.shape.BI);
   const int NT = pl.shape.NT, WN = pl.shape.WN;
@@ -866,6 +1143,20 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   if (lrc != PRONY_OK) return lrc;
   // U is first read by k_reduce: a caller may still be copying it on another stream
   if (wait_before_reduce && cudaStreamWaitEvent(st, wait_before_reduce, 0) != cudaSuccess) return PRONY_ERR_CUDA;
+  if (pl.nj > 0) {
+    const dim3 wgrd(pl.RP, g.d, pl.nj);
+    switch ((pl.shape.NP / 8 + 1) / 2) {  // n-tiles per consumer warp (WN = 2)
+#define PRONY_WCASE(nt) \
+  case nt:              \
+    lrc = launch_reduce_ws_t<nt, 2>(r, wgrd, st); \
+    break;
+      PRONY_WCASE(1) PRONY_WCASE(2) PRONY_WCASE(3) PRONY_WCASE(4) PRONY_WCASE(5) PRONY_WCASE(6) PRONY_WCASE(7)
+      PRONY_WCASE(8)
+#undef PRONY_WCASE
+      default:
+        return PRONY_ERR_RANGE;
+    }
+  } else {
   switch (pl.shape.rWN * 16 + pl.shape.rNT) {
 #define PRONY_RCASE(nt, wn) \
   case wn * 16 + nt:        \
@@ -875,6 +1166,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
 #undef PRONY_RCASE
     default:
       return PRONY_ERR_RANGE;
+  }
   }
   if (lrc != PRONY_OK) return lrc;
   const int64_t tot = (int64_t)g.d * g.m * g.m;

@@ -45,7 +45,9 @@ struct ProjPlan {
   int yoff[PRONY_MAX_D];
   int R_tot, max_rows;
   int chunk_w, KC;  // split-K: KC chunks of chunk_w columns of T_l
-  int RP;           // reduce partitions per l
+  int RP;           // reduce partitions per l (the largest over the j-blocks)
+  int nj;           // j-blocks of the warp-specialized reduce (k_reduce_ws)
+  int rp_j[4];      // its row partitions per j-block (weighted by the j-block's active m-tiles)
 };
 
 struct ProjParams {
@@ -71,6 +73,7 @@ struct RedParams {
   double2* Spart;
   int m, NP, KC, R_tot, RP, E;
   int kb[PRONY_MAX_D], rows[PRONY_MAX_D], yoff[PRONY_MAX_D];
+  int rp_j[4];  // k_reduce_ws: row partitions of j-block z (CTAs with blockIdx.x >= rp_j[z] write zeros)
 };
 
 // Copy/compute overlap for callers whose V arrives in two parts (prony_pencil_host): when KC > 1 the
