@@ -46,24 +46,16 @@ __device__ __forceinline__ void warp_cmma_k4(double (&acc)[3][NT][4], const doub
   constexpr double sb = CONJB ? -1.0 : 1.0;
 #pragma unroll
   for (int j = 0; j < NA; ++j) {
-#ifdef PRONY_PK_IFELSE
-    if (PK && MODE == 3 && j == NA - 1) {
-#else
     if constexpr (PK && MODE == 3) {
       if (j == NA - 1) {
-#endif
         const double2 bb = brow[8 * j - (g & 4)];  // column 8j + (g & 3) of the tile
         const double bp = (g & 4) ? bb.y : bb.x;
         mma16x8x4(acc[0][j], a0.x, a1.x, bp);
         mma16x8x4(acc[1][j], a0.y, a1.y, bp);
-#ifdef PRONY_PK_IFELSE
-    } else {
-#else
         continue;
       }
     }
     {
-#endif
       const double2 b = brow[8 * j];
       if constexpr (MODE == 3) {
         const double bs = bsrow[8 * j];

@@ -23,7 +23,6 @@ VARIANTS = {
     "vt64": ["PRONY_VLS_TILE=64"],
     "bk8s5": ["PRONY_BK=8", "PRONY_STAGES=5"],
     "solvet": ["PRONY_SOLVE_TIMING"],
-    "pkifelse": ["PRONY_PK_IFELSE"],
 }
 
 if __name__ == "__main__":
