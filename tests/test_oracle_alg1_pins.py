@@ -372,3 +372,24 @@ def test_algorithm1_jacobi_and_power_agree(oracle_mod):
     pa, pb = oracle_mod.match_nodes(a["t"], t), oracle_mod.match_nodes(b["t"], t)
     assert W.torus_dist_inf(a["t"][pa], b["t"][pb]).max() < 1e-12
     assert rel(a["c"][pa], b["c"][pb]) < 1e-10
+
+
+def test_perturbation_bounds_hoffman_wielandt_and_tail(oracle_mod):
+    """for T~ = T + dT built from samples f(1+delta), |delta| <= eps,
+    sqrt(sum_i |sigma~_i - sigma_i|^2) <= ||dT||_F <= eps ||T||_F (Hoffman-Wielandt) and the tail
+    sqrt(sum_{i>m} sigma~_i^2) <= eps ||T||_F — checked on the oracle's own Jacobi SVDs of both matrices."""
+    d, n, m = 2, 9, 4
+    t, c = W.paper_family(d, m)
+    eps = 1e-3
+    g0 = W.sample_grid(t, c, n)
+    g1 = W.sample_grid(t, c, n, eps, 3, noise_model="disk")
+    T0, T1 = oracle_mod.T_dense(g0, d, n, 0), oracle_mod.T_dense(g1, d, n, 0)
+    _, s0, _, _ = oracle_mod.jacobi_svd(T0)
+    _, s1, _, _ = oracle_mod.jacobi_svd(T1)
+    nT = oracle_mod.T_fro(g0, d, n)
+    hw = math.sqrt(float(np.sum((s1 - s0) ** 2)))
+    assert hw <= np.linalg.norm(T1 - T0) * (1 + 1e-12) <= eps * nT * (1 + 1e-12)
+    assert hw > 0.01 * eps * nT * 1e-3               # the noise is really there
+    tail = math.sqrt(float(np.sum(s1[m:] ** 2)))
+    assert tail <= eps * nT
+    assert s0[m] <= 1e-12 * s0[0]                    # noise-free T has rank m exactly
