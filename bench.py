@@ -417,8 +417,15 @@ def run_ours(args, cfg):
         real_per_cmac = 8.0 * cm                         # 3M: 3 real products = 6 real flops per complex MAC
         proj_avg_s = statistics.mean(proj_ms) * 1e-3
         achieved = real_per_cmac * cmac_proj / proj_avg_s / 1e12
-        np_pad = 8 * ((m + 7) // 8)
-        executed = achieved * np_pad / m                 # the DMMA work including the padded columns
+        # DMMA work actually issued per k-step and 16-row tile, in real products: 3 per full 8-column n-tile
+        # (3M), 2 for a last n-tile with <= 4 valid columns (packed, DESIGN.md v9), 3 otherwise; the useful
+        # work is 3 m / 8 (4M: 4 per tile, 4 m / 8)
+        ntile, w = (m + 7) // 8, m % 8
+        if cm == 1.0:
+            issued, useful = 4.0 * ntile, 4.0 * m / 8.0
+        else:
+            issued, useful = 3.0 * (ntile - 1) + (2.0 if 0 < w <= 4 else 3.0), 3.0 * m / 8.0
+        executed = achieved * issued / useful
         traffic, traffic_src = stamped_traffic()
         tflops = real_per_cmac * cmac_step * world * value / 1e12
         line = {
