@@ -304,6 +304,35 @@ def test_full_size_all_entries_fft_convolution(pb, name):
         assert rel(S[ell - 1], want) <= TOL, ell
 
 
+@pytest.mark.parametrize("m", [128, 97])
+def test_full_size_max_m_all_entries(pb, orc, m):
+    """The headline grid (d=2, n=200, N=40401, noisy) at m = PRONY_MAX_M = 128 (16 n-tiles: the 4-column-warp
+    k_project layout and the 8-n-tile k_reduce_ws warps) and m = 97 (a packed 1-column last n-tile): every
+    entry of S_l against F7, two sampled columns against the oracle, and the LS products against the oracle
+    on a column sub-range."""
+    from f7_fft import fft_apply
+    cfg = W.custom_config(2, 200, m, 1e-6, 4242 + m)
+    prob = W.make_problem(cfg, with_svd=False)
+    rng = np.random.default_rng(m)
+    N = cfg.N
+    prob.U = W.random_orthonormal(N, m, rng)
+    prob.V = W.random_orthonormal(N, m, rng)
+    prob.sigma = np.sort(rng.random(m) + 0.5)[::-1].copy()
+    S = run_project(pb, prob).cpu().numpy()
+    for ell in (1, 2):
+        want = prob.U.conj().T @ fft_apply(prob.grid, 2, 200, ell, prob.V) / prob.sigma[None, :]
+        assert rel(S[ell - 1], want) <= TOL, ell
+    cols = [0, m - 1]
+    want = orc.project_columns(prob.grid, prob.U, prob.V, prob.sigma, 2, 200, 2, cols)
+    assert rel(S[1][:, cols], want) <= TOL
+    a, e = 1000, 9000
+    out = pb.vandermonde_ls(dev(prob.z), dev(prob.grid), 2, 200, m, a, e, want_A=True)
+    torch.cuda.synchronize()
+    A_or = orc.vandermonde(prob.z, 2, 200, a, e)
+    G_or, b_or = orc.ls_products(A_or, prob.grid, 2, 200, a, e)
+    assert rel(out["A"], A_or) <= TOL and rel(out["G"], G_or) <= TOL and rel(out["b"], b_or) <= TOL
+
+
 # ------------------------------------------------------------------ Vandermonde / LS parity
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5"])
 def test_vandermonde_ls_configs(pb, orc, name):
