@@ -299,8 +299,6 @@ def run_ours(args, cfg):
     ev_ps, ev_pe = new_events(K), new_events(K)
     ev_ls, ev_le = new_events(K), new_events(K)
     ev_cs, ev_ce = new_events(K), new_events(K)
-    infos_p = [pb.make_exec_info(ev_ps[i], ev_pe[i]) for i in range(K)]
-    infos_l = [pb.make_exec_info(ev_ls[i], ev_le[i]) for i in range(K)]
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -311,7 +309,7 @@ def run_ours(args, cfg):
     for i in range(K):
         flush.fill_(i & 0xFF)                  # L2 flush outside the timed interval
         ev_s[i].record(stream)
-        pencil(grid, U, V, sigma, z, stream=stream, info_p=infos_p[i], info_l=infos_l[i],
+        pencil(grid, U, V, sigma, z, stream=stream, ev_project=(ev_ps[i], ev_pe[i]), ev_ls=(ev_ls[i], ev_le[i]),
                ev_comm=(ev_cs[i], ev_ce[i]) if world > 1 else None)
         ev_e[i].record(stream)
     torch.cuda.synchronize()
@@ -333,7 +331,7 @@ def run_ours(args, cfg):
     else:
         per_rank = [mine.tolist()]
     total_ms_max = max(r[0] for r in per_rank)
-    launches_per_step = infos_p[0].launches + infos_l[0].launches + (1 if world > 1 else 0)
+    launches_per_step = pencil.last_launches
 
     # ---- end to end from pinned host buffers
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
@@ -411,7 +409,7 @@ def run_ours(args, cfg):
         cm = 1.0 if os.environ.get("PRONY_CMUL", "3m").startswith("4") else 0.75
         # complex MACs of the pencil as this implementation computes it (per rank: k_project's product over
         # its E rows; the reduce U^* Y over those rows for every l; the LS products over its columns)
-        cmac_proj = infos_p[0].main_flops / 8.0
+        cmac_proj = pencil.last_main_flops / 8.0
         rows = cmac_proj / (m * N)
         cmac_step = cmac_proj + d * m * m * rows + m * m * N / world + m * N / world
         real_per_cmac = 8.0 * cm                         # 3M: 3 real products = 6 real flops per complex MAC
@@ -462,7 +460,7 @@ def run_ours(args, cfg):
                          "planning_peak": 37.2, "frac_vs_planning": achieved / 37.2,
                          "avg_launch_ms": proj_avg_s * 1e3, "cmul": "4M" if cm == 1.0 else "3M",
                          "share_of_step": sum(proj_ms) / sum(step_ms),
-                         "grid": list(infos_p[0].main_grid), "split_k": infos_p[0].split_k},
+                         "grid": pencil.last_grid, "split_k": pencil.last_split_k},
             "kernels_ms": {"k_project": statistics.mean(proj_ms), "k_vls": statistics.mean(vls_ms),
                            "outside_k_project": statistics.mean(step_ms) - statistics.mean(proj_ms)},
             "per_rank": [{"rank": r, "step_ms": x[4], "k_project_ms": x[1], "k_vls_ms": x[2], "allreduce_ms": x[3]}

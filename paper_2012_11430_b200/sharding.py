@@ -174,18 +174,27 @@ class DistributedPencil:
         self.side = torch.cuda.Stream(device=device)
         self.ev_in = torch.cuda.Event()
         self.ev_ls = torch.cuda.Event()
+        # recorded by the library right after k_project (N > 1): the LS branch's all-reduce of [G, b] waits
+        # for it, so no rank's NCCL kernel occupies SMs (spinning on its peers) while projections still run
+        self.ev_proj = torch.cuda.Event()
+        self.ev_proj.record(torch.cuda.current_stream(self.device))  # materialize the handle
 
-    def __call__(self, grid, U, V, sigma, z, stream=None, info_p=None, info_l=None, ev_comm=None):
+    def __call__(self, grid, U, V, sigma, z, stream=None, ev_project=None, ev_ls=None, ev_comm=None):
         """Device-resident inputs -> (S, c, t) (views of this object's buffers, valid until the next call).
         Ordered after prior work on `stream` (default: the current stream), which is ordered after all of it
-        on return. ev_comm: optional (begin, end) CUDA events recorded around the collective of S.
+        on return. ev_project / ev_ls: optional (begin, end) timing torch.cuda.Events the library records
+        around k_project / k_vls (each already recorded once so its handle exists); ev_comm: optional
+        (begin, end) events recorded around the collective of S.
 
-        N > 1: the LS branch (side stream) all-reduces its G, b as soon as they are done and solves for c, t
-        there, while the projection (high-priority stream) is still running; only the all-reduce of S is left
-        on the projection's critical path."""
+        N > 1: the LS branch (side stream) all-reduces its G, b once they are done AND k_project has finished
+        (so no rank's NCCL kernel spins on SMs its projection needs) and solves for c, t there, alongside the
+        projection stream's k_reduce_ws, k_finalize and all-reduce of S."""
         pb, d, n, m = self.pb, self.d, self.n, self.m
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
         full = self.world == 1
+        pe = ev_project if ev_project is not None else (None, self.ev_proj)
+        info_p = pb.make_exec_info(pe[0], pe[1])
+        info_l = pb.make_exec_info(*ev_ls) if ev_ls is not None else pb.make_exec_info()
         if full and self.order == UNITS_SHARED:
             # one C call (prony_pencil): the projection on `main`, the LS step on the context's side stream
             if self.ctx is None:
@@ -195,6 +204,7 @@ class DistributedPencil:
                 self.status.zero_()
             pb.pencil(grid, U, V, sigma, z, d, n, m, self.outs, self.ws_pencil, context=self.ctx,
                       dev_status=self.status, stream=main, info_p=info_p, info_l=info_l)
+            self._note(info_p, info_l, 0)
             return self.S, self.c, self.t
         hi, side = self.hi, self.side
         hi.wait_stream(main)
@@ -203,12 +213,14 @@ class DistributedPencil:
             self.ev_in.record(hi)
             pb.project(grid, U, V, sigma, d, n, m, self.u0, self.u1, self.order, out=self.S, workspace=self.ws_p,
                        dev_status=self.status, stream=hi, info=info_p)
+        ev_proj_end = pe[1]  # recorded by the library right after k_project
         side.wait_event(self.ev_in)
         with torch.cuda.stream(side):
             res = pb.vandermonde_ls(z, grid, d, n, m, self.c0, self.c1, want_solution=full,
                                     out={"G": self.G, "b": self.b, "c": self.c, "t": self.t}, workspace=self.ws_l,
                                     dev_status=self.status, stream=side, info=info_l)
             if not full:
+                side.wait_event(ev_proj_end)
                 self._allreduce(self.buf[d * m * m:])            # G, b
                 pb.ls_solve(self.G, self.b, z, d, m, dev_status=self.status, stream=side,
                             out={"c": self.c, "t": self.t})
@@ -222,7 +234,16 @@ class DistributedPencil:
                     ev_comm[1].record(hi)
             hi.wait_event(self.ev_ls)
         main.wait_stream(hi)
+        self._note(info_p, info_l, 0 if full else 1)
         return self.S, (res["c"] if full else self.c), (res["t"] if full else self.t)
+
+    def _note(self, info_p, info_l, extra):
+        """Launch record of the last call (the bench's gpu_launches and roofline fields): libprony kernels
+        launched (+ the separate k_solve at N > 1), the dominant kernel's flops (ZGEMM convention), grid, split-K."""
+        self.last_launches = info_p.launches + info_l.launches + extra
+        self.last_main_flops = info_p.main_flops
+        self.last_grid = list(info_p.main_grid)
+        self.last_split_k = info_p.split_k
 
     def _allreduce(self, x):
         if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
