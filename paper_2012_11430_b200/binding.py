@@ -281,8 +281,18 @@ def pencil(grid, U, V, sigma, z, d: int, n: int, m: int, out: dict, workspace, c
            stream=None, info_p=None, info_l=None):
     """One full pencil on DEVICE buffers in one C call (prony_pencil): S_1..S_d on `stream`, the LS products,
     c and t concurrently on the context's side stream. out: preallocated device tensors "S" (d,m,m), "G" (m,m),
-    "b" (m,), "c" (m,), "t" (m,d); workspace >= WS_PENCIL. Asynchronous; returns `out`. Arguments are passed
-    through unchecked beyond the C ABI's validation (this is the low-overhead path)."""
+    "b" (m,), "c" (m,), "t" (m,d); workspace >= WS_PENCIL. Asynchronous; returns `out`."""
+    for name, x, shape in (("S", out["S"], (d, m, m)), ("G", out["G"], (m, m)), ("b", out["b"], (m,)),
+                           ("c", out["c"], (m,))):
+        _dev_tensor(x, torch.complex128, name)
+        if tuple(x.shape) != shape:
+            raise ValueError(f"out[{name!r}] must have shape {shape}, got {tuple(x.shape)}")
+    _dev_tensor(out["t"], torch.float64, "t")
+    if tuple(out["t"].shape) != (m, d):
+        raise ValueError(f"out['t'] must have shape {(m, d)}")
+    for name, x in (("grid", grid), ("U", U), ("V", V), ("z", z)):
+        _dev_tensor(x, torch.complex128, name)
+    _dev_tensor(sigma, torch.float64, "sigma")
     rc = lib().prony_pencil(None if context is None else context.handle, d, n, m, _ptr(grid), _ptr(U), _ptr(V),
                             _ptr(sigma), _ptr(z), _ptr(out["S"]), _ptr(out["G"]), _ptr(out["b"]), _ptr(out["c"]),
                             _ptr(out["t"]), _ptr(workspace), workspace.numel(), _ptr(dev_status), _stream(stream),
