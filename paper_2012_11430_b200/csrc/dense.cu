@@ -2,7 +2,8 @@
 // measured hot path (NEXT-1): tall-skinny Gram / Cholesky-QR with diagonal pivoting
 // (rank determination of the block power method, Alg. 3), the SVD of the projected
 // r x r matrix Q_k (one-sided Jacobi), the eigendecomposition of C_mu (Hessenberg reduction
-// + shifted QR + back substitution) and the simultaneous diagonalization W^-1 S_l W.
+// + shifted QR eigenvalues + inverse-iteration eigenvectors) and the simultaneous diagonalization
+// W^-1 S_l W.
 // Everything is FP64 complex; the N-sized products use all SMs, the r x r / m x m algorithms run in
 // one CTA (or one warp) on L2-resident matrices. All matrices are row-major.
 #include <algorithm>
@@ -447,88 +448,125 @@ __global__ void k_permute_sigma(int cols, const double* __restrict__ sigma, cons
   for (int j = threadIdx.x; j < cols; j += blockDim.x) out[j] = sigma[order[j]];
 }
 
-// ---------------------------------------------------------------------------- eig (one warp)
-// C (m x m, ld m) -> eigenvalues lam[m] and unit eigenvectors W (m x m, columns), via
-// Householder Hessenberg reduction, complex single-shift QR with Wilkinson shifts and deflation
-// (Schur form T = Z^H C Z), eigenvectors of T by back substitution, W = Z Y, normalized.
-// H and Z are in global memory (L1/L2), the warp updates rows/columns lane-parallel.
-__global__ void __launch_bounds__(32) k_eig(int m, double2* __restrict__ H, double2* __restrict__ Z,
-                                            double2* __restrict__ lam, double2* __restrict__ W,
-                                            int* __restrict__ status, int max_iter_per_eig) {
-  const int lane = threadIdx.x;
-  auto h = [&](int i, int j) -> double2& { return H[(size_t)i * m + j]; };
-  auto zz = [&](int i, int j) -> double2& { return Z[(size_t)i * m + j]; };
-  for (int e = lane; e < m * m; e += 32) Z[e] = make_double2((e / m) == (e % m) ? 1.0 : 0.0, 0.0);
-  __syncwarp();
-  // 1. Hessenberg reduction: for k, Householder on x = H[k+1:m, k]
+// ---------------------------------------------------------------------------- eig, parallel form
+// The eigendecomposition of C_mu in four steps that keep every sequential chain short:
+//   k_hess       one CTA: Householder reduction C = Q H Q^H to upper Hessenberg form, the left update one
+//                thread per column, the right update one thread per row (H and the unit reflectors v_k kept
+//                in global memory, L1-resident);
+//   k_hqr_vals   one warp: complex single-shift QR with Wilkinson shifts on a copy of H, eigenvalues only
+//                (updates restricted to the active block, no Schur vectors);
+//   k_inv_iter   one warp per eigenvalue: inverse iteration (H - lambda_j I) y = b on the Hessenberg matrix
+//                (LU with partial pivoting between consecutive rows: O(m^2)), two solves from b = 1, then
+//                w_j = Q y = H_0 H_1 ... H_{m-3} y, normalized (R23);
+// and the simultaneous diagonalization: k_lu (one CTA, LU with partial pivoting of W), then
+// k_diag_z with one warp per (l, j): x = W^-1 (S_l w_j) by the LU solves, z_j(l) = x_j, t (R4).
+__global__ void __launch_bounds__(256) k_hess(int m, double2* __restrict__ H, double2* __restrict__ Vh) {
+  __shared__ double red[256];
+  __shared__ double2 sv0;
+  __shared__ double sxn, svn;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < m * m; e += nt) Vh[e] = make_double2(0.0, 0.0);
+  __syncthreads();
   for (int k = 0; k + 2 < m; ++k) {
-    double xn2 = 0.0;
-    for (int i = k + 1 + lane; i < m; i += 32) xn2 += cabs2(h(i, k));
-    xn2 = warp_sum(xn2);
-    const double xn = sqrt(xn2);
-    if (xn == 0.0) continue;
-    const double2 x0 = h(k + 1, k);
-    const double ax0 = sqrt(cabs2(x0));
-    const double2 ph = ax0 > 0.0 ? make_double2(x0.x / ax0, x0.y / ax0) : make_double2(1.0, 0.0);
-    // v = x + ph*||x|| e1, H = I - 2 v v^H / (v^H v)
-    const double2 v0 = cadd(x0, cscale(ph, xn));
-    __syncwarp();
-    if (lane == 0) h(k + 1, k) = v0;  // store v in place (column k below the subdiagonal)
-    __syncwarp();
-    double vn2 = 0.0;
-    for (int i = k + 1 + lane; i < m; i += 32) vn2 += cabs2(h(i, k));
-    vn2 = warp_sum(vn2);
-    const double tau = 2.0 / vn2;
-    // H <- P H: rows k+1..m-1, columns k+1..m-1 (column k handled below)
-    for (int j = k + 1; j < m; ++j) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int i = k + 1 + lane; i < m; i += 32) s = cadd(s, cmulc(h(i, k), h(i, j)));  // v^H col
-      s = warp_sum2(s);
-      s = cscale(s, tau);
-      for (int i = k + 1 + lane; i < m; i += 32) h(i, j) = csub(h(i, j), cmul(h(i, k), s));
+    double part = 0.0;
+    for (int i = k + 1 + tid; i < m; i += nt) part += cabs2(H[(size_t)i * m + k]);
+    red[tid] = part;
+    __syncthreads();
+    for (int o = nt / 2; o > 0; o >>= 1) {
+      if (tid < o) red[tid] += red[tid + o];
+      __syncthreads();
     }
-    __syncwarp();
-    // H <- H P: all rows, columns k+1..m-1
-    for (int i = 0; i < m; ++i) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int j = k + 1 + lane; j < m; j += 32) s = cadd(s, cmul(h(i, j), h(j, k)));  // row * v
-      s = warp_sum2(s);
-      s = cscale(s, tau);
-      for (int j = k + 1 + lane; j < m; j += 32) h(i, j) = csub(h(i, j), cmul(s, cconj(h(j, k))));
+    if (tid == 0) {
+      const double xn2 = red[0], xn = sqrt(xn2);
+      const double2 alpha = H[(size_t)(k + 1) * m + k];
+      const double aa = sqrt(cabs2(alpha));
+      const double2 ph = aa > 0.0 ? make_double2(alpha.x / aa, alpha.y / aa) : make_double2(1.0, 0.0);
+      sxn = xn;
+      sv0 = make_double2(alpha.x + ph.x * xn, alpha.y + ph.y * xn);  // v = x - beta e1, beta = -ph ||x||
+      svn = sqrt(xn2 - cabs2(alpha) + cabs2(sv0));
     }
-    __syncwarp();
-    // Z <- Z P
-    for (int i = 0; i < m; ++i) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int j = k + 1 + lane; j < m; j += 32) s = cadd(s, cmul(zz(i, j), h(j, k)));
-      s = warp_sum2(s);
-      s = cscale(s, tau);
-      for (int j = k + 1 + lane; j < m; j += 32) zz(i, j) = csub(zz(i, j), cmul(s, cconj(h(j, k))));
+    __syncthreads();
+    const double xn = sxn, vn = svn;
+    if (xn == 0.0 || vn == 0.0) continue;  // column already reduced (uniform)
+    const double inv = 1.0 / vn;
+    for (int i = k + 1 + tid; i < m; i += nt) {
+      const double2 x = i == k + 1 ? sv0 : H[(size_t)i * m + k];
+      Vh[(size_t)i * m + k] = cscale(x, inv);
     }
-    __syncwarp();
-    // column k: H[k+1][k] = -ph ||x||, zeros below
-    const double2 newsub = cscale(ph, -xn);
-    for (int i = k + 1 + lane; i < m; i += 32) h(i, k) = (i == k + 1) ? newsub : make_double2(0.0, 0.0);
+    __syncthreads();
+    // left: H[k+1:, j] -= 2 v (v^H H[k+1:, j]), j > k (one thread per column)
+    for (int j = k + 1 + tid; j < m; j += nt) {
+      double2 sacc = make_double2(0.0, 0.0);
+      for (int i = k + 1; i < m; ++i) sacc = cadd(sacc, cmulc(Vh[(size_t)i * m + k], H[(size_t)i * m + j]));
+      sacc = cscale(sacc, 2.0);
+      for (int i = k + 1; i < m; ++i) H[(size_t)i * m + j] = csub(H[(size_t)i * m + j], cmul(Vh[(size_t)i * m + k], sacc));
+    }
+    __syncthreads();
+    // right: H[i, k+1:] -= 2 (H[i, k+1:] v) v^H, every row (one thread per row)
+    for (int i = tid; i < m; i += nt) {
+      double2 sacc = make_double2(0.0, 0.0);
+      for (int j = k + 1; j < m; ++j) sacc = cadd(sacc, cmul(H[(size_t)i * m + j], Vh[(size_t)j * m + k]));
+      sacc = cscale(sacc, 2.0);
+      for (int j = k + 1; j < m; ++j)
+        H[(size_t)i * m + j] = csub(H[(size_t)i * m + j], cmul(sacc, cconj(Vh[(size_t)j * m + k])));
+    }
+    __syncthreads();
+    // column k: beta = -ph ||x|| on the subdiagonal (ph = the phase of alpha = the phase of v0), zeros below
+    for (int i = k + 1 + tid; i < m; i += nt) {
+      double2 val = make_double2(0.0, 0.0);
+      if (i == k + 1) {
+        const double av0 = sqrt(cabs2(sv0));
+        const double2 ph = av0 > 0.0 ? make_double2(sv0.x / av0, sv0.y / av0) : make_double2(1.0, 0.0);
+        val = make_double2(-ph.x * xn, -ph.y * xn);
+      }
+      H[(size_t)i * m + k] = val;
+    }
+    __syncthreads();
+  }
+}
+
+// eigenvalues of the upper Hessenberg H (m x m, overwritten) by single-shift QR; one warp. For m <= 119 the
+// matrix is staged in shared memory (<= 226.6 KB); the deflation test runs lane-parallel over the subdiagonal
+// (ballot), without square roots (|h_{l,l-1}|^2 <= eps^2 (|h_{l-1,l-1}|^2 + |h_{l,l}|^2)); the rotations use
+// reciprocal square roots only; updates are restricted to the active block (eigenvalues only).
+constexpr int kHqrSmemMaxM = 119;  // 119^2 x 16 B = 226.6 KB <= 227 KB
+__global__ void __launch_bounds__(32) k_hqr_vals(int m, double2* __restrict__ Hg, double2* __restrict__ lam,
+                                                 int* __restrict__ status, int max_iter_per_eig) {
+  extern __shared__ __align__(16) double2 Hs[];
+  const int lane = threadIdx.x;
+  const bool in_smem = m <= kHqrSmemMaxM;
+  double2* H = in_smem ? Hs : Hg;
+  if (in_smem) {
+    for (int e = lane; e < m * m; e += 32) Hs[e] = Hg[e];
     __syncwarp();
   }
-  // 2. shifted QR on the Hessenberg matrix, active block [lo, hi]
-  double anorm = 0.0;
-  for (int e = lane; e < m * m; e += 32) anorm += cabs2(H[e]);
-  anorm = sqrt(warp_sum(anorm));
-  const double ulp = 2.220446049250313e-16;
+  auto h = [&](int i, int j) -> double2& { return H[(size_t)i * m + j]; };
+  double anorm2 = 0.0;
+  for (int e = lane; e < m * m; e += 32) anorm2 += cabs2(H[e]);
+  anorm2 = warp_sum(anorm2);
+  const double ulp = 2.220446049250313e-16, ulp2 = ulp * ulp;
   int hi = m - 1, iter = 0, total = 0;
   while (hi > 0) {
-    // find lo: smallest l such that subdiagonals lo+1..hi are not negligible
-    int lo = hi;
-    while (lo > 0) {
-      const double s = sqrt(cabs2(h(lo - 1, lo - 1))) + sqrt(cabs2(h(lo, lo)));
-      if (sqrt(cabs2(h(lo, lo - 1))) <= ulp * (s > 0.0 ? s : anorm)) break;
-      --lo;
+    // lo = the largest l in [1, hi] with a negligible subdiagonal h(l, l-1), else 0 (lane-parallel scan down
+    // from hi in chunks of 32)
+    int lo = 0;
+    for (int top = hi; top >= 1; top -= 32) {
+      const int l = top - lane;
+      bool neg = false;
+      if (l >= 1) {
+        const double sd = cabs2(h(l - 1, l - 1)) + cabs2(h(l, l));
+        neg = cabs2(h(l, l - 1)) <= ulp2 * (sd > 0.0 ? sd : anorm2);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, neg);
+      if (bal) {
+        lo = top - (__ffs(bal) - 1);  // the lowest lane = the largest l
+        break;
+      }
     }
     __syncwarp();
-    if (lo > 0 && lane == 0) h(lo, lo - 1) = make_double2(0.0, 0.0);  // negligible: split
+    if (lo > 0 && lane == 0) h(lo, lo - 1) = make_double2(0.0, 0.0);
     __syncwarp();
-    if (lo == hi) {  // deflate one eigenvalue
+    if (lo == hi) {
       --hi;
       iter = 0;
       continue;
@@ -537,7 +575,6 @@ __global__ void __launch_bounds__(32) k_eig(int m, double2* __restrict__ H, doub
       if (lane == 0) set_status(status, PRONY_ERR_NOT_CONVERGED);
       break;
     }
-    // Wilkinson shift from the trailing 2x2 of the active block; exceptional shift every 10 its
     const double2 a = h(hi - 1, hi - 1), b = h(hi - 1, hi), c = h(hi, hi - 1), dd = h(hi, hi);
     double2 mu;
     if (iter % 10 == 0) {
@@ -546,14 +583,12 @@ __global__ void __launch_bounds__(32) k_eig(int m, double2* __restrict__ H, doub
       const double2 tr2 = cscale(cadd(a, dd), 0.5);
       const double2 diff = cscale(csub(a, dd), 0.5);
       const double2 disc = cadd(cmul(diff, diff), cmul(b, c));
-      // complex sqrt
       const double r = sqrt(sqrt(cabs2(disc)));
       const double th = 0.5 * atan2(disc.y, disc.x);
       const double2 sq = make_double2(r * cos(th), r * sin(th));
       const double2 m1 = cadd(tr2, sq), m2 = csub(tr2, sq);
       mu = (cabs2(csub(m1, dd)) < cabs2(csub(m2, dd))) ? m1 : m2;
     }
-    // implicit single-shift QR sweep via Givens rotations on [lo, hi]
     for (int k = lo; k < hi; ++k) {
       double2 x, y;
       if (k == lo) {
@@ -563,39 +598,30 @@ __global__ void __launch_bounds__(32) k_eig(int m, double2* __restrict__ H, doub
         x = h(k, k - 1);
         y = h(k + 1, k - 1);
       }
-      const double nx = sqrt(cabs2(x) + cabs2(y));
-      if (nx == 0.0) continue;
-      // G = [[cc, s], [-conj(s), cc]] with cc real: G [x; y] = [nx'; 0]
-      const double ax = sqrt(cabs2(x));
+      const double x2 = cabs2(x), y2 = cabs2(y);
+      if (x2 + y2 == 0.0) continue;
       double cc;
-      double2 s;
-      if (ax == 0.0) {
+      double2 sg;
+      if (x2 == 0.0) {
         cc = 0.0;
-        s = cscale(cconj(y), 1.0 / sqrt(cabs2(y)));
+        sg = cscale(cconj(y), rsqrt(y2));
       } else {
-        cc = ax / nx;
-        const double2 ph = make_double2(x.x / ax, x.y / ax);
-        s = cscale(cmul(ph, cconj(y)), 1.0 / nx);
+        const double rx = rsqrt(x2), rn = rsqrt(x2 + y2);
+        cc = x2 * rx * rn;                        // |x| / ||(x, y)||
+        sg = cscale(cmul(x, cconj(y)), rx * rn);  // (x/|x|) conj(y) / ||(x, y)||
       }
       __syncwarp();
-      // rows k, k+1 (columns from max(lo, k-1) .. m-1)
-      for (int j = max(lo, k - 1) + lane; j < m; j += 32) {
+      for (int j = max(lo, k - 1) + lane; j <= hi; j += 32) {
         const double2 u = h(k, j), v = h(k + 1, j);
-        h(k, j) = cadd(cscale(u, cc), cmul(s, v));
-        h(k + 1, j) = csub(cscale(v, cc), cmul(cconj(s), u));
+        h(k, j) = cadd(cscale(u, cc), cmul(sg, v));
+        h(k + 1, j) = csub(cscale(v, cc), cmul(cconj(sg), u));
       }
       __syncwarp();
-      // columns k, k+1 (rows 0 .. min(k+2, hi))
       const int rmax = min(k + 2, hi);
-      for (int i = lane; i <= rmax; i += 32) {
+      for (int i = lo + lane; i <= rmax; i += 32) {
         const double2 u = h(i, k), v = h(i, k + 1);
-        h(i, k) = cadd(cscale(u, cc), cmul(cconj(s), v));
-        h(i, k + 1) = csub(cscale(v, cc), cmul(s, u));
-      }
-      for (int i = lane; i < m; i += 32) {
-        const double2 u = zz(i, k), v = zz(i, k + 1);
-        zz(i, k) = cadd(cscale(u, cc), cmul(cconj(s), v));
-        zz(i, k + 1) = csub(cscale(v, cc), cmul(s, u));
+        h(i, k) = cadd(cscale(u, cc), cmul(cconj(sg), v));
+        h(i, k + 1) = csub(cscale(v, cc), cmul(sg, u));
       }
       __syncwarp();
       if (k > lo && lane == 0) h(k + 1, k - 1) = make_double2(0.0, 0.0);
@@ -603,56 +629,182 @@ __global__ void __launch_bounds__(32) k_eig(int m, double2* __restrict__ H, doub
     }
   }
   __syncwarp();
-  // zero below the diagonal (numerically negligible after convergence)
-  for (int e = lane; e < m * m; e += 32)
-    if ((e / m) > (e % m)) H[e] = make_double2(0.0, 0.0);
-  __syncwarp();
   for (int i = lane; i < m; i += 32) lam[i] = h(i, i);
-  __syncwarp();
-  // 3. eigenvectors of T (upper triangular): for each k, y_k = 1, y_i = -(sum_{j=i+1..k} T_ij y_j)/(T_ii - T_kk)
-  //    computed into W's column k (as Y), then W = Z Y in place column by column (Y kept in H's lower part? no:
-  //    use W as Y storage, then multiply).
-  const double small = ulp * (anorm > 0.0 ? anorm : 1.0);
-  for (int k = lane; k < m; k += 32) {
-    for (int i = m - 1; i > k; --i) W[(size_t)i * m + k] = make_double2(0.0, 0.0);
-    W[(size_t)k * m + k] = make_double2(1.0, 0.0);
-    const double2 lk = h(k, k);
-    for (int i = k - 1; i >= 0; --i) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int j = i + 1; j <= k; ++j) s = cadd(s, cmul(h(i, j), W[(size_t)j * m + k]));
-      double2 den = csub(h(i, i), lk);
-      if (sqrt(cabs2(den)) < small) den = make_double2(small, 0.0);
-      W[(size_t)i * m + k] = cscale(cdiv(s, den), -1.0);
+}
+
+// one warp per eigenvalue j: y = (Hh - lam_j I)^-1 b twice (b = 1, then the normalized y), Hessenberg LU with
+// row pivoting between consecutive rows; U rows and the elimination record in the per-warp scratch; then
+// w_j = Q y (reflectors v_{m-3} .. v_0 of k_hess applied in reverse), unit 2-norm, into column j of W
+constexpr int kInvRowsPerLane = (PRONY_MAX_M + 31) / 32;
+__global__ void __launch_bounds__(256) k_inv_iter(int m, const double2* __restrict__ Hh, const double2* __restrict__ lam,
+                                                  const double2* __restrict__ Vh, double2* __restrict__ W,
+                                                  double2* __restrict__ scratch, double anorm_hint) {
+  const int lane = threadIdx.x & 31;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= m) return;
+  double2* U = scratch + (size_t)j * (m * m + 2 * m);  // U rows (m x m), multipliers (m), swap flags (m, as re)
+  double2* fm = U + (size_t)m * m;
+  double2* sw = fm + m;
+  const double2 lj = lam[j];
+  double anorm = 0.0;
+  for (int e = lane; e < m * m; e += 32) anorm += cabs2(Hh[e]);
+  anorm = sqrt(warp_sum(anorm));
+  if (!(anorm > 0.0)) anorm = anorm_hint > 0.0 ? anorm_hint : 1.0;
+  const double small = 2.220446049250313e-16 * anorm;
+  // factorization: cur = row 0 of (Hh - lj I)
+  double2 cur[kInvRowsPerLane];
+#pragma unroll
+  for (int q = 0; q < kInvRowsPerLane; ++q) {
+    const int c = lane + 32 * q;
+    double2 v = c < m ? Hh[c] : make_double2(0.0, 0.0);
+    if (c == 0) v = csub(v, lj);
+    cur[q] = v;
+  }
+  for (int k = 0; k < m - 1; ++k) {
+    double2 nxt[kInvRowsPerLane];
+#pragma unroll
+    for (int q = 0; q < kInvRowsPerLane; ++q) {
+      const int c = lane + 32 * q;
+      double2 v = (c < m && c >= k) ? Hh[(size_t)(k + 1) * m + c] : make_double2(0.0, 0.0);
+      if (c == k + 1) v = csub(v, lj);
+      nxt[q] = v;
+    }
+    // the column-k entries of both rows (lane k % 32, q = k / 32)
+    const int qk = k >> 5, lk = k & 31;
+    double2 ck = make_double2(0.0, 0.0), nk = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < kInvRowsPerLane; ++q)
+      if (q == qk) {
+        ck = cur[q];
+        nk = nxt[q];
+      }
+    ck = make_double2(__shfl_sync(0xffffffffu, ck.x, lk), __shfl_sync(0xffffffffu, ck.y, lk));
+    nk = make_double2(__shfl_sync(0xffffffffu, nk.x, lk), __shfl_sync(0xffffffffu, nk.y, lk));
+    const bool swap = cabs2(nk) > cabs2(ck);
+    if (swap) {
+#pragma unroll
+      for (int q = 0; q < kInvRowsPerLane; ++q) {
+        const double2 tmp = cur[q];
+        cur[q] = nxt[q];
+        nxt[q] = tmp;
+      }
+      const double2 tmp = ck;
+      ck = nk;
+      nk = tmp;
+    }
+    if (sqrt(cabs2(ck)) < small) ck = make_double2(small, 0.0);
+    const double2 f = cdiv(nk, ck);
+#pragma unroll
+    for (int q = 0; q < kInvRowsPerLane; ++q) {
+      const int c = lane + 32 * q;
+      if (c < m) {
+        if (c == k) U[(size_t)k * m + c] = ck;
+        else U[(size_t)k * m + c] = cur[q];
+        if (c > k) nxt[q] = csub(nxt[q], cmul(f, cur[q]));
+      }
+      cur[q] = nxt[q];
+    }
+    if (lane == 0) {
+      fm[k] = f;
+      sw[k] = make_double2(swap ? 1.0 : 0.0, 0.0);
     }
   }
-  __syncwarp();
-  // W = Z Y: Y is upper triangular (column k nonzero in rows 0..k); compute column by column from
-  // the last to the first, writing into H (free now) then copy with normalization
-  for (int k = 0; k < m; ++k) {
-    for (int i = lane; i < m; i += 32) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int j = 0; j <= k; ++j) s = cadd(s, cmul(zz(i, j), W[(size_t)j * m + k]));
-      h(i, k) = s;
+  {
+    const int qk = (m - 1) >> 5, lk = (m - 1) & 31;
+#pragma unroll
+    for (int q = 0; q < kInvRowsPerLane; ++q) {
+      const int c = lane + 32 * q;
+      if (c < m) {
+        double2 v = cur[q];
+        if (c == m - 1 && sqrt(cabs2(v)) < small) v = make_double2(small, 0.0);
+        U[(size_t)(m - 1) * m + c] = v;
+      }
     }
+    (void)qk;
+    (void)lk;
   }
   __syncwarp();
-  for (int k = 0; k < m; ++k) {
+  // two solves: rhs b (in registers, element i on lane i % 32, slot i / 32)
+  double2 y[kInvRowsPerLane];
+#pragma unroll
+  for (int q = 0; q < kInvRowsPerLane; ++q) y[q] = make_double2(lane + 32 * q < m ? 1.0 : 0.0, 0.0);
+  for (int it = 0; it < 2; ++it) {
+    // apply the elimination record: for k: (swap rows k, k+1 of the rhs), rhs[k+1] -= f_k rhs[k]
+    for (int k = 0; k < m - 1; ++k) {
+      const int q0 = k >> 5, l0 = k & 31, q1 = (k + 1) >> 5, l1 = (k + 1) & 31;
+      double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < kInvRowsPerLane; ++q) {
+        if (q == q0) a0 = y[q];
+        if (q == q1) a1 = y[q];
+      }
+      a0 = make_double2(__shfl_sync(0xffffffffu, a0.x, l0), __shfl_sync(0xffffffffu, a0.y, l0));
+      a1 = make_double2(__shfl_sync(0xffffffffu, a1.x, l1), __shfl_sync(0xffffffffu, a1.y, l1));
+      if (sw[k].x != 0.0) {
+        const double2 tmp = a0;
+        a0 = a1;
+        a1 = tmp;
+      }
+      a1 = csub(a1, cmul(fm[k], a0));
+#pragma unroll
+      for (int q = 0; q < kInvRowsPerLane; ++q) {
+        if (q == q0 && lane == l0) y[q] = a0;
+        if (q == q1 && lane == l1) y[q] = a1;
+      }
+    }
+    // back substitution with U (upper triangular)
+    for (int i = m - 1; i >= 0; --i) {
+      double2 sacc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < kInvRowsPerLane; ++q) {
+        const int c = lane + 32 * q;
+        if (c > i && c < m) sacc = cadd(sacc, cmul(U[(size_t)i * m + c], y[q]));
+      }
+      sacc = warp_sum2(sacc);
+      const int qi = i >> 5, li = i & 31;
+#pragma unroll
+      for (int q = 0; q < kInvRowsPerLane; ++q)
+        if (q == qi && lane == li) y[q] = cdiv(csub(y[q], sacc), U[(size_t)i * m + i]);
+    }
+    // normalize (unit max-modulus keeps the second solve's scale sane)
     double nn = 0.0;
-    for (int i = lane; i < m; i += 32) nn += cabs2(h(i, k));
+#pragma unroll
+    for (int q = 0; q < kInvRowsPerLane; ++q) nn += cabs2(y[q]);
     nn = sqrt(warp_sum(nn));
     const double inv = nn > 0.0 ? 1.0 / nn : 0.0;
-    for (int i = lane; i < m; i += 32) W[(size_t)i * m + k] = cscale(h(i, k), inv);
+#pragma unroll
+    for (int q = 0; q < kInvRowsPerLane; ++q) y[q] = cscale(y[q], inv);
+  }
+  // w = Q y = H_0 H_1 ... H_{m-3} y, H_k = I - 2 v_k v_k^H
+  for (int k = m - 3; k >= 0; --k) {
+    double2 sacc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < kInvRowsPerLane; ++q) {
+      const int c = lane + 32 * q;
+      if (c > k && c < m) sacc = cadd(sacc, cmulc(Vh[(size_t)c * m + k], y[q]));
+    }
+    sacc = cscale(warp_sum2(sacc), 2.0);
+#pragma unroll
+    for (int q = 0; q < kInvRowsPerLane; ++q) {
+      const int c = lane + 32 * q;
+      if (c > k && c < m) y[q] = csub(y[q], cmul(Vh[(size_t)c * m + k], sacc));
+    }
+  }
+  double nn = 0.0;
+#pragma unroll
+  for (int q = 0; q < kInvRowsPerLane; ++q) nn += cabs2(y[q]);
+  nn = sqrt(warp_sum(nn));
+  const double inv = nn > 0.0 ? 1.0 / nn : 0.0;
+#pragma unroll
+  for (int q = 0; q < kInvRowsPerLane; ++q) {
+    const int c = lane + 32 * q;
+    if (c < m) W[(size_t)c * m + j] = cscale(y[q], inv);
   }
 }
 
-// ---------------------------------------------------------------------------- W^-1 S_l W diagonals
-// One CTA. LU with partial pivoting of W (m x m, in the scratch `LU`), then for every l:
-// X = W^-1 (S_l W) column by column, z[j][l] = X[j][j]. Also t = (-arg z / 2 pi) mod 1 (R4).
-__global__ void __launch_bounds__(256) k_diag_pencil(int d, int m, const double2* __restrict__ W,
-                                                    const double2* __restrict__ S, double2* __restrict__ LU,
-                                                    int* __restrict__ pv, double2* __restrict__ col,
-                                                    double2* __restrict__ z, double* __restrict__ t,
-                                                    int* __restrict__ status) {
+// LU with partial pivoting of W (one CTA): LU (m x m) and the row permutation pv; status SINGULAR on a zero pivot
+__global__ void __launch_bounds__(256) k_lu(int m, const double2* __restrict__ W, double2* __restrict__ LU,
+                                           int* __restrict__ pv, int* __restrict__ status) {
   __shared__ double sval[256];
   __shared__ int sidx[256];
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -672,10 +824,10 @@ __global__ void __launch_bounds__(256) k_diag_pencil(int d, int m, const double2
     sval[tid] = best;
     sidx[tid] = bi;
     __syncthreads();
-    for (int s = nt / 2; s > 0; s >>= 1) {
-      if (tid < s && sval[tid + s] > sval[tid]) {
-        sval[tid] = sval[tid + s];
-        sidx[tid] = sidx[tid + s];
+    for (int o = nt / 2; o > 0; o >>= 1) {
+      if (tid < o && sval[tid + o] > sval[tid]) {
+        sval[tid] = sval[tid + o];
+        sidx[tid] = sidx[tid + o];
       }
       __syncthreads();
     }
@@ -708,44 +860,71 @@ __global__ void __launch_bounds__(256) k_diag_pencil(int d, int m, const double2
     }
     __syncthreads();
   }
-  // z[jj][l] = e_jj^T W^-1 S_l W e_jj: solve W x = S_l w_jj (w_jj = column jj of W), take x[jj]
-  for (int l = 0; l < d; ++l) {
-    for (int jj = 0; jj < m; ++jj) {
-      // col = P (S_l w_jj)
-      for (int i = tid; i < m; i += nt) {
-        const int src = pv[i];
-        double2 s = make_double2(0.0, 0.0);
-        for (int k = 0; k < m; ++k) s = cadd(s, cmul(S[((size_t)l * m + src) * m + k], W[(size_t)k * m + jj]));
-        col[i] = s;
-      }
-      __syncthreads();
-      if (tid < 32) {  // forward (unit L) and backward (U) substitution, one warp
-        for (int i = 0; i < m; ++i) {
-          double2 s = make_double2(0.0, 0.0);
-          for (int k = tid; k < i; k += 32) s = cadd(s, cmul(LU[(size_t)i * m + k], col[k]));
-          s = warp_sum2(s);
-          if (tid == 0) col[i] = csub(col[i], s);
-          __syncwarp();
-        }
-        for (int i = m - 1; i >= jj; --i) {
-          double2 s = make_double2(0.0, 0.0);
-          for (int k = i + 1 + tid; k < m; k += 32) s = cadd(s, cmul(LU[(size_t)i * m + k], col[k]));
-          s = warp_sum2(s);
-          if (tid == 0) col[i] = cdiv(csub(col[i], s), LU[(size_t)i * m + i]);
-          __syncwarp();
-        }
-        if (tid == 0) {
-          const double2 zz = col[jj];
-          z[(size_t)jj * d + l] = zz;
-          if (t) {
-            double v = -atan2(zz.y, zz.x) * 0.15915494309189533577;
-            v = v - floor(v);
-            if (v >= 1.0) v = 0.0;
-            t[(size_t)jj * d + l] = v;
-          }
-        }
-      }
-      __syncthreads();
+}
+
+// one warp per (l, jj): x = P S_l w_jj, L u = x, U v = u down to row jj, z[jj][l] = v[jj], t (R4)
+__global__ void __launch_bounds__(256) k_diag_z(int d, int m, const double2* __restrict__ LU,
+                                               const int* __restrict__ pv, const double2* __restrict__ W,
+                                               const double2* __restrict__ S, double2* __restrict__ z,
+                                               double* __restrict__ t, const int* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (wid >= d * m) return;
+  if (status && *status == PRONY_ERR_SINGULAR) return;
+  const int l = wid / m, jj = wid % m;
+  double2 x[kInvRowsPerLane];
+#pragma unroll
+  for (int q = 0; q < kInvRowsPerLane; ++q) {
+    const int i = lane + 32 * q;
+    double2 sacc = make_double2(0.0, 0.0);
+    if (i < m) {
+      const int src = pv[i];
+      for (int k = 0; k < m; ++k)
+        sacc = cadd(sacc, cmul(S[((size_t)l * m + src) * m + k], W[(size_t)k * m + jj]));
+    }
+    x[q] = sacc;
+  }
+  // forward: unit lower L
+  for (int i = 1; i < m; ++i) {
+    double2 sacc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < kInvRowsPerLane; ++q) {
+      const int k = lane + 32 * q;
+      if (k < i) sacc = cadd(sacc, cmul(LU[(size_t)i * m + k], x[q]));
+    }
+    sacc = warp_sum2(sacc);
+    const int qi = i >> 5, li = i & 31;
+#pragma unroll
+    for (int q = 0; q < kInvRowsPerLane; ++q)
+      if (q == qi && lane == li) x[q] = csub(x[q], sacc);
+  }
+  // backward: U, rows m-1 .. jj
+  for (int i = m - 1; i >= jj; --i) {
+    double2 sacc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < kInvRowsPerLane; ++q) {
+      const int k = lane + 32 * q;
+      if (k > i && k < m) sacc = cadd(sacc, cmul(LU[(size_t)i * m + k], x[q]));
+    }
+    sacc = warp_sum2(sacc);
+    const int qi = i >> 5, li = i & 31;
+#pragma unroll
+    for (int q = 0; q < kInvRowsPerLane; ++q)
+      if (q == qi && lane == li) x[q] = cdiv(csub(x[q], sacc), LU[(size_t)i * m + i]);
+  }
+  const int qj = jj >> 5, lj = jj & 31;
+  double2 zz = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int q = 0; q < kInvRowsPerLane; ++q)
+    if (q == qj) zz = x[q];
+  zz = make_double2(__shfl_sync(0xffffffffu, zz.x, lj), __shfl_sync(0xffffffffu, zz.y, lj));
+  if (lane == 0) {
+    z[(size_t)jj * d + l] = zz;
+    if (t) {
+      double v = -atan2(zz.y, zz.x) * 0.15915494309189533577;
+      v = v - floor(v);
+      if (v >= 1.0) v = 0.0;
+      t[(size_t)jj * d + l] = v;
     }
   }
 }

@@ -24,10 +24,14 @@ __global__ void k_gather_cols(int N, int k, const int* piv, const double2* Xin, 
 __global__ void k_jacobi_svd(int rows, int cols, double2* A, double2* Vm, double* sigma, double2* Uout, double2* Vout,
                              int* order, int max_sweeps);
 __global__ void k_permute_sigma(int cols, const double* sigma, const int* order, double* out);
-__global__ void k_eig(int m, double2* H, double2* Z, double2* lam, double2* W, int* status, int max_iter_per_eig);
-__global__ void k_diag_pencil(int d, int m, const double2* W, const double2* S, double2* LU, int* pv, double2* col,
-                              double2* z, double* t, int* status);
 __global__ void k_combine(int d, int m, const double2* mu, const double2* S, double2* C);
+__global__ void k_hess(int m, double2* H, double2* Vh);
+__global__ void k_hqr_vals(int m, double2* H, double2* lam, int* status, int max_iter_per_eig);
+__global__ void k_inv_iter(int m, const double2* Hh, const double2* lam, const double2* Vh, double2* W,
+                           double2* scratch, double anorm_hint);
+__global__ void k_lu(int m, const double2* W, double2* LU, int* pv, int* status);
+__global__ void k_diag_z(int d, int m, const double2* LU, const int* pv, const double2* W, const double2* S,
+                         double2* z, double* t, const int* status);
 
 size_t svd_workspace_bytes(int d, int n, int N, int m);
 int block_power_svd(int d, int n, int N, const double2* grid, int m, double tol, int max_iter, uint64_t seed,

@@ -229,7 +229,7 @@ int block_power_svd(int d, int n, int N, const double2* grid, int m, double tol,
 // ---------------------------------------------------------------------------- diagonalization
 namespace {
 struct DiagLayout {
-  size_t C, Z, lam, LU, pv, col, total;
+  size_t C, Hh, Vh, lam, LU, pv, scratch, total;
 };
 DiagLayout diag_layout(int d, int m) {
   (void)d;
@@ -241,11 +241,12 @@ DiagLayout diag_layout(int d, int m) {
     return o;
   };
   s.C = take((size_t)m * m * sizeof(double2));
-  s.Z = take((size_t)m * m * sizeof(double2));
+  s.Hh = take((size_t)m * m * sizeof(double2));
+  s.Vh = take((size_t)m * m * sizeof(double2));
   s.lam = take((size_t)m * sizeof(double2));
   s.LU = take((size_t)m * m * sizeof(double2));
   s.pv = take((size_t)m * sizeof(int));
-  s.col = take((size_t)m * sizeof(double2));
+  s.scratch = take((size_t)m * ((size_t)m * m + 2 * m) * sizeof(double2));  // per-eigenvalue inverse iteration
   s.total = off;
   return s;
 }
@@ -259,9 +260,21 @@ int diagonalize_launch(int d, int m, const double2* S, const double2* mu, double
   char* w = (char*)ws;
   double2* C = (double2*)(w + L.C);
   k_combine<<<(m * m + 255) / 256, 256, 0, st>>>(d, m, mu, S, C);
-  k_eig<<<1, 32, 0, st>>>(m, C, (double2*)(w + L.Z), (double2*)(w + L.lam), W, status, 60);
-  k_diag_pencil<<<1, 256, 0, st>>>(d, m, W, S, (double2*)(w + L.LU), (int*)(w + L.pv), (double2*)(w + L.col), z, t,
-                                   status);
+  double2* Hh = (double2*)(w + L.Hh);
+  double2* Vh = (double2*)(w + L.Vh);
+  double2* lam = (double2*)(w + L.lam);
+  k_hess<<<1, 256, 0, st>>>(m, C, Vh);  // C <- Hessenberg H (in place)
+  if (cudaMemcpyAsync(Hh, C, (size_t)m * m * sizeof(double2), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return PRONY_ERR_CUDA;
+  {
+    const size_t hsm = m <= 119 ? (size_t)m * m * sizeof(double2) : 0;  // kHqrSmemMaxM (dense.cu)
+    if (hsm && cudaFuncSetAttribute(k_hqr_vals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm) != cudaSuccess)
+      return PRONY_ERR_CUDA;
+    k_hqr_vals<<<1, 32, hsm, st>>>(m, C, lam, status, 60);  // eigenvalues (C overwritten)
+  }
+  k_inv_iter<<<(m + 7) / 8, 256, 0, st>>>(m, Hh, lam, Vh, W, (double2*)(w + L.scratch), 0.0);
+  k_lu<<<1, 256, 0, st>>>(m, W, (double2*)(w + L.LU), (int*)(w + L.pv), status);
+  k_diag_z<<<(d * m + 7) / 8, 256, 0, st>>>(d, m, (double2*)(w + L.LU), (int*)(w + L.pv), W, S, z, t, status);
   return cudaGetLastError() == cudaSuccess ? PRONY_OK : PRONY_ERR_CUDA;
 }
 

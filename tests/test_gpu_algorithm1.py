@@ -127,7 +127,7 @@ def test_build_pencil_svd_vs_oracle(pb, orc, d, n, m, noise):
         assert rel(S[l], S_or[l]) <= 1e-10
 
 
-@pytest.mark.parametrize("d,m", [(1, 4), (2, 5), (3, 12), (2, 40)])
+@pytest.mark.parametrize("d,m", [(1, 4), (2, 5), (3, 12), (2, 40), (2, 100), (4, 128)])
 def test_diagonalize_vs_oracle(pb, orc, d, m):
     """C_mu eig + W^-1 S_l W on the device vs the oracle's Hessenberg-QR eig + LU solves on the same S, mu:
     the nodes z element by element (matched), and both equal to the planted nodes."""
