@@ -329,10 +329,9 @@ int prony_pencil_host_part(int d, int n, int m, const prony_c128* grid, const pr
 /*
  * prony_build_pencil — Algorithm 1 lines 1-3 on the device: the reduced SVD T = U Sigma V*
  * (eq_T_svd) by the block power method of Alg. 3 with starting dimension 2m
- * (P:595), T V and T^H U applied by the implicit-Toeplitz gather of prony_project, Cholesky-QR steps,
- * rank determination by diagonal-pivoted Cholesky of the Gram of Vbar_1 (equivalent to the pivoted QR
- * of P:193/P:203 in exact arithmetic; trailing-norm tolerance max(tol, 1e-7), R22), and the
- * SVD of Q_k by one-sided Jacobi; then S_1..S_d = U* T_l V Sigma^-1 over all units (prony_project).
+ * (P:595), T V and T^H U applied by the implicit-Toeplitz gather of prony_project, Householder QR of
+ * every block, column-pivoted for Vbar_1 with rank = the first k with ||R(k:,k:)||_F <= tol ||R||_F
+ * (R22), and the SVD of Q_k by one-sided Jacobi; then S_1..S_d = U* T_l V Sigma^-1 over all units (prony_project).
  * SYNCHRONOUS: the stream is synchronized once per power iteration (the rank and the residual steer it).
  *   grid            device L^d samples (as prony_project)
  *   seed            seeds the random starting block V_0 (counter-based generator, R14)

@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "dense.cuh"
 
@@ -200,143 +202,384 @@ __global__ void k_sum_doubles(int count, const double* __restrict__ parts, doubl
   }
 }
 
-// ---------------------------------------------------------------------------- Cholesky with pivoting
-// One CTA. A (r x r, ld r) Hermitian PSD is overwritten: on exit its lower triangle holds L with
-// P^T A P = L L^H for the first `rank` columns. With pivot = 1 the largest remaining diagonal is
-// chosen at each step and the factorization stops at the first j where the trace of the remaining
-// Schur complement (= ||R(j:, j:)||_F^2 of the pivoted QR of the tall matrix) is
-// <= tol^2 * trace(A). Without pivoting it stops at a non-positive pivot. out[0] = rank, piv[r].
-__global__ void __launch_bounds__(512) k_chol_piv(int r, double2* __restrict__ A, int pivot, double tol,
-                                                  int* __restrict__ piv, int* __restrict__ rank_out) {
-  __shared__ double sval[512];
-  __shared__ int sidx[512];
-  __shared__ int s_stop;
-  __shared__ double s_tr0;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int i = tid; i < r; i += nt) piv[i] = i;
-  // trace
-  double t = 0.0;
-  for (int i = tid; i < r; i += nt) t += A[(size_t)i * r + i].x;
-  sval[tid] = t;
-  __syncthreads();
-  for (int s = nt / 2; s > 0; s >>= 1) {
-    if (tid < s) sval[tid] += sval[tid + s];
-    __syncthreads();
+// ---------------------------------------------------------------------------- Householder QR (tall)
+// Reduced QR of a tall N x r matrix X (row-major, ld ldx, r <= kHouseMaxCols) by Householder reflectors
+// ("QR factorization implemented with Householder reflectors"), optionally with column pivoting
+// (the column with the largest remaining norm first; the rank is the first k with
+// ||R(k:, k:)||_F <= tol ||R||_F, P:193 / P:203, the rule of Alg. 3 line 10), and the explicit
+// Q(:, :rank) = H_0 ... H_{rank-1} [I; 0] in logical (pivoted) column order.
+// ONE cooperative launch: CTA c owns the rows [c rows_per_cta, (c+1) rows_per_cta); one pass over the
+// trailing rows and one two-level grid reduction (two barriers) per factorization step and per Q step.
+// The pass leaves per-CTA column partials (warp accumulators summed in a fixed warp order) in a
+// column-major buffer; the columns are then summed over the CTAs in a fixed order by warps spread over
+// the grid and broadcast back to every CTA, so the pivot choice and the rank decision are bitwise
+// identical in all CTAs and the result is deterministic. The trailing norms are recomputed
+// exactly at every step from the updated entries (the pivot of step k + 1 is chosen from them downdated by
+// row k of R, so that step k's pass can already accumulate step k + 1's products). Pivoting is logical: a done[] flag
+// per physical column, X is never permuted, so every row access stays coalesced.
+// On exit X holds the reflector tails below the diagonal of the pivot columns (row k keeps its values before
+// H_k: R itself is not needed by the callers).
+namespace cg = cooperative_groups;
+constexpr int kHqThreads = 512;
+constexpr int kHqWarps = kHqThreads / 32;
+constexpr int kHqT = kHouseMaxCols / 32;  // column chunks per lane
+
+template <typename T>
+__device__ __forceinline__ T hq_zero();
+template <>
+__device__ __forceinline__ double hq_zero<double>() { return 0.0; }
+template <>
+__device__ __forceinline__ double2 hq_zero<double2>() { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ double hq_add(double a, double b) { return a + b; }
+__device__ __forceinline__ double2 hq_add(double2 a, double2 b) { return cadd(a, b); }
+__device__ __forceinline__ double hq_shfl(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ double2 hq_shfl(double2 v, int o) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));
+}
+
+// CTA column partials: part[j * G + blockIdx.x] = sum over the warps (fixed order) of acc[t] (j = lane + 32 t)
+template <typename T>
+__device__ __forceinline__ void hq_cta_part(const T (&acc)[kHqT], T* red, int r, int j0, T* part) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < kHqT; ++t) {
+    const int j = lane + 32 * t;
+    if (j < r) red[warp * r + j] = acc[t];
   }
-  if (tid == 0) s_tr0 = sval[0];
   __syncthreads();
-  const double tr0 = s_tr0;
-  int rank = r;
-  for (int j = 0; j < r; ++j) {
-    // remaining trace and (optional) pivot = argmax remaining diagonal
-    double best = -1.0, tr = 0.0;
-    int bi = j;
-    for (int i = j + tid; i < r; i += nt) {
-      const double v = A[(size_t)i * r + i].x;
-      tr += v;
-      if (v > best) {
-        best = v;
-        bi = i;
+  for (int j = j0 + threadIdx.x; j < r; j += kHqThreads) {
+    T s = red[j];
+    for (int w = 1; w < kHqWarps; ++w) s = hq_add(s, red[w * r + j]);
+    part[(size_t)j * gridDim.x + blockIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+// Two-level grid reduction of the column partials, deterministic: phase A (after the barrier that published
+// the partials) spreads the columns over the warps of the whole grid, fin[j] = sum_c part[j * G + c] in a
+// fixed order (lanes over CTAs, then a fixed shuffle tree); phase B (after the next barrier) copies the
+// finished columns into every CTA's shared memory. Both phases skip the columns flagged in skip[].
+template <typename T>
+__device__ __forceinline__ void hq_reduce_a(const T* part, T* fin, int r, int j0, const unsigned char* skip) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x;
+  for (int j = j0 + blockIdx.x * kHqWarps + warp; j < r; j += G * kHqWarps) {
+    if (skip && skip[j]) continue;
+    T s = hq_zero<T>();
+    for (int c = lane; c < G; c += 32) s = hq_add(s, __ldcg(part + (size_t)j * G + c));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = hq_add(s, hq_shfl(s, o));
+    if (lane == 0) fin[j] = s;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void hq_reduce_b(const T* fin, int r, int j0, const unsigned char* skip, T* out) {
+  for (int j = j0 + threadIdx.x; j < r; j += kHqThreads)
+    if (!(skip && skip[j])) out[j] = __ldcg(fin + j);
+  __syncthreads();
+}
+
+// argmax over the columns not done of val[] (ties: lowest column), warp 0 only; identical in every CTA
+__device__ __forceinline__ int hq_argmax(const double* val, const unsigned char* done, int r, int skip) {
+  const int lane = threadIdx.x & 31;
+  double best = -1.0;
+  int bj = r;
+  for (int j = lane; j < r; j += 32) {
+    if (done[j] || j == skip) continue;
+    if (val[j] > best) {
+      best = val[j];
+      bj = j;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+    if (ob > best || (ob == best && oj < bj)) {
+      best = ob;
+      bj = oj;
+    }
+  }
+  return bj;
+}
+
+__global__ void __launch_bounds__(kHqThreads, 1) k_house_qr(HouseQrArgs a) {
+  extern __shared__ double2 red2[];  // [kHqWarps][r] warp partials
+  double* red1 = reinterpret_cast<double*>(red2);
+  __shared__ double nrm[kHouseMaxCols];  // exact norms^2 of the remaining columns over rows >= k
+  __shared__ double nd[kHouseMaxCols];   // the same, downdated by row k (next pivot choice)
+  __shared__ double2 sv[kHouseMaxCols];  // s_j = x^H X(k:, j), x = X(k:, p_k)
+  __shared__ double2 wv[kHouseMaxCols];  // w_j = v^H X(k:, j) (factorization) / y_c (Q accumulation)
+  __shared__ double2 vh[kHouseMaxCols];  // v_k(k) = alpha - beta
+  __shared__ double tau[kHouseMaxCols];
+  __shared__ int perm[kHouseMaxCols];
+  __shared__ unsigned char done[kHouseMaxCols];
+  __shared__ int s_p, s_stop;
+  __shared__ double s_tr;
+  cg::grid_group grid = cg::this_grid();
+  const int N = a.N, r = a.r, K = min(N, r);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x;
+  const int per = (N + G - 1) / G;
+  const int lo = blockIdx.x * per, hi = min(N, lo + per);
+  double2* X = a.X;
+  const size_t ldx = a.ldx;
+  for (int j = tid; j < r; j += kHqThreads) done[j] = 0;
+
+  // exact column norms and ||X||_F^2 (= ||R||_F^2)
+  {
+    double an[kHqT];
+#pragma unroll
+    for (int t = 0; t < kHqT; ++t) an[t] = 0.0;
+    for (int i = lo + warp; i < hi; i += kHqWarps) {
+      const double2* row = X + (size_t)i * ldx;
+#pragma unroll
+      for (int t = 0; t < kHqT; ++t) {
+        const int j = lane + 32 * t;
+        if (j < r) an[t] += cabs2(row[j]);
       }
     }
-    sval[tid] = best;
-    sidx[tid] = bi;
-    __syncthreads();
-    for (int s = nt / 2; s > 0; s >>= 1) {
-      if (tid < s && (sval[tid + s] > sval[tid] || (sval[tid + s] == sval[tid] && sidx[tid + s] < sidx[tid]))) {
-        sval[tid] = sval[tid + s];
-        sidx[tid] = sidx[tid + s];
+    hq_cta_part<double>(an, red1, r, 0, a.npart);
+    grid.sync();
+    hq_reduce_a<double>(a.npart, a.nfin, r, 0, nullptr);
+    grid.sync();
+    hq_reduce_b<double>(a.nfin, r, 0, nullptr, nrm);
+  }
+  if (warp == 0) {
+    double sum = 0.0;
+    for (int j = lane; j < r; j += 32) sum += nrm[j];
+    sum = warp_sum(sum);
+    const int p0 = a.pivot ? hq_argmax(nrm, done, r, -1) : 0;
+    if (lane == 0) {
+      s_tr = sum;
+      s_p = p0;
+    }
+  }
+  __syncthreads();
+  const double fro2 = s_tr;
+  // s_j for the first pivot column
+  {
+    const int p = s_p;
+    double2 as[kHqT];
+#pragma unroll
+    for (int t = 0; t < kHqT; ++t) as[t] = make_double2(0.0, 0.0);
+    for (int i = lo + warp; i < hi; i += kHqWarps) {
+      const double2* row = X + (size_t)i * ldx;
+      const double2 xp = row[p];
+#pragma unroll
+      for (int t = 0; t < kHqT; ++t) {
+        const int j = lane + 32 * t;
+        if (j < r) as[t] = cfma(cconj(xp), row[j], as[t]);
       }
-      __syncthreads();
     }
-    const int p = pivot ? sidx[0] : j;
-    __syncthreads();
-    sval[tid] = tr;
-    __syncthreads();
-    for (int s = nt / 2; s > 0; s >>= 1) {
-      if (tid < s) sval[tid] += sval[tid + s];
-      __syncthreads();
-    }
-    if (tid == 0) {
-      const double trem = sval[0];
-      const double dj = A[(size_t)p * r + p].x;
-      s_stop = (pivot && trem <= tol * tol * tr0) || !(dj > 0.0);
+    hq_cta_part<double2>(as, red2, r, 0, a.wpart);
+    grid.sync();
+    hq_reduce_a<double2>(a.wpart, a.wfin, r, 0, nullptr);
+    grid.sync();
+    hq_reduce_b<double2>(a.wfin, r, 0, nullptr, sv);
+  }
+
+  // Factorization: ONE pass over the trailing rows and one grid barrier per step. Step k applies H_k and,
+  // in the same pass, accumulates the exact norms and s_j of step k + 1, whose pivot p_{k+1} is chosen
+  // beforehand from the norms downdated by row k of R (exact norms are restored every step).
+  int rank = K;
+  for (int k = 0; k < K; ++k) {
+    const int p = s_p;
+    if (warp == 0) {
+      double tr = 0.0;
+      for (int j = lane; j < r; j += 32)
+        if (!done[j]) tr += nrm[j];
+      tr = warp_sum(tr);
+      if (lane == 0) s_stop = a.pivot && !(tr > a.tol * a.tol * fro2);
     }
     __syncthreads();
     if (s_stop) {
-      rank = j;
+      rank = k;
       break;
     }
-    if (p != j) {  // symmetric swap of rows/columns j and p (full rows: L part included)
-      for (int c = tid; c < r; c += nt) {
-        const double2 x = A[(size_t)j * r + c];
-        A[(size_t)j * r + c] = A[(size_t)p * r + c];
-        A[(size_t)p * r + c] = x;
-      }
-      __syncthreads();
-      for (int c = tid; c < r; c += nt) {
-        const double2 x = A[(size_t)c * r + j];
-        A[(size_t)c * r + j] = A[(size_t)c * r + p];
-        A[(size_t)c * r + p] = x;
-      }
-      if (tid == 0) {
-        const int x = piv[j];
-        piv[j] = piv[p];
-        piv[p] = x;
-      }
-      __syncthreads();
+    // the reflector of column p over rows k..N-1: H x = beta e_1 (oracle_householder_qr's convention)
+    const double xn = sqrt(nrm[p]);
+    const double2 alpha = __ldcg(X + (size_t)k * ldx + p);
+    double tk = 0.0;
+    double2 v0 = make_double2(0.0, 0.0);
+    if (xn > 0.0) {
+      const double aa = hypot(alpha.x, alpha.y);
+      const double2 ph = aa > 0.0 ? make_double2(alpha.x / aa, alpha.y / aa) : make_double2(1.0, 0.0);
+      v0 = make_double2(alpha.x + ph.x * xn, alpha.y + ph.y * xn);  // alpha - beta, beta = -ph xn
+      tk = 1.0 / (xn * (xn + aa));                                  // 2 / v^H v
     }
-    const double ljj = sqrt(A[(size_t)j * r + j].x);
-    const double inv = 1.0 / ljj;
-    __syncthreads();
-    if (tid == 0) A[(size_t)j * r + j] = make_double2(ljj, 0.0);
-    for (int i = j + 1 + tid; i < r; i += nt) A[(size_t)i * r + j] = cscale(A[(size_t)i * r + j], inv);
-    __syncthreads();
-    // trailing update of the full Hermitian block: A[i][k] -= L[i][j] conj(L[k][j])
-    const int w = r - j - 1;
-    for (int e = tid; e < w * w; e += nt) {
-      const int i = j + 1 + e / w, k = j + 1 + e % w;
-      const double2 li = A[(size_t)i * r + j], lk = A[(size_t)k * r + j];
-      double2 v = A[(size_t)i * r + k];
-      v.x -= li.x * lk.x + li.y * lk.y;
-      v.y -= li.y * lk.x - li.x * lk.y;
-      A[(size_t)i * r + k] = v;
+    // w_j = v^H X(k:, j) = s_j + conj(v0 - alpha) X(k, j); R(k, j) = X(k, j) - tau v0 w_j; downdated norms
+    const double2 dv = make_double2(v0.x - alpha.x, v0.y - alpha.y);
+    for (int j = tid; j < r; j += kHqThreads) {
+      if (done[j] || j == p) continue;
+      const double2 xk = __ldcg(X + (size_t)k * ldx + j);
+      const double2 w = cfma(cconj(dv), xk, sv[j]);
+      wv[j] = w;
+      const double2 tvw = make_double2(tk * (v0.x * w.x - v0.y * w.y), tk * (v0.x * w.y + v0.y * w.x));
+      nd[j] = nrm[j] - cabs2(csub(xk, tvw));
     }
     __syncthreads();
-  }
-  if (tid == 0) *rank_out = rank;
-}
-
-// Rinv (k x k, ld ldr) = inverse of the upper-triangular R = L^H, L = lower triangle of A (ld r).
-// One thread per column c: back substitution R x = e_c.
-__global__ void k_trinv_from_lower(int r, int k, const double2* __restrict__ A, double2* __restrict__ Rinv, int ldr) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
-    for (int i = k - 1; i >= 0; --i) {
-      double2 s = make_double2(i == c ? 1.0 : 0.0, 0.0);
-      if (i < c) s = make_double2(0.0, 0.0);
-      if (i <= c) {
-        for (int q = i + 1; q <= c; ++q) {
-          // R[i][q] = conj(L[q][i])
-          const double2 Riq = cconj(A[(size_t)q * r + i]);
-          const double2 x = Rinv[(size_t)q * ldr + c];
-          s = csub(s, cmul(Riq, x));
+    if (tid == 0) {
+      done[p] = 1;
+      perm[k] = p;
+      vh[k] = v0;
+      tau[k] = tk;
+    }
+    if (warp == 0) {
+      int pn = -1;
+      if (k + 1 < K) pn = a.pivot ? hq_argmax(nd, done, r, p) : k + 1;
+      if (lane == 0) s_p = pn;
+    }
+    __syncthreads();
+    const int pn = s_p;
+    const double2 wpn = pn >= 0 ? wv[pn] : make_double2(0.0, 0.0);
+    uint32_t act = 0;
+#pragma unroll
+    for (int t = 0; t < kHqT; ++t) {
+      const int j = lane + 32 * t;
+      if (j < r && !done[j]) act |= 1u << t;
+    }
+    double an[kHqT];
+    double2 as[kHqT];
+#pragma unroll
+    for (int t = 0; t < kHqT; ++t) {
+      an[t] = 0.0;
+      as[t] = make_double2(0.0, 0.0);
+    }
+    // rows > k only: row k of R is never read again, and leaving X(k, :) untouched lets every CTA read it
+    // (alpha, w_j above) while its owner has already moved on to this pass
+    for (int i = lo + warp; i < hi; i += kHqWarps) {
+      if (i <= k) continue;
+      double2* row = X + (size_t)i * ldx;
+      const double2 vi = row[p];
+      const double2 tv = make_double2(tk * vi.x, tk * vi.y);
+      double2 xpn = make_double2(0.0, 0.0);
+      if (pn >= 0) {
+        xpn = row[pn];
+        xpn.x -= tv.x * wpn.x - tv.y * wpn.y;
+        xpn.y -= tv.x * wpn.y + tv.y * wpn.x;
+      }
+      double2 x[kHqT];
+#pragma unroll
+      for (int t = 0; t < kHqT; ++t)
+        if (act >> t & 1) x[t] = row[lane + 32 * t];
+      __syncwarp();  // every lane has read row[pn] before its owner overwrites it
+#pragma unroll
+      for (int t = 0; t < kHqT; ++t) {
+        if (act >> t & 1) {
+          const double2 w = wv[lane + 32 * t];
+          x[t].x -= tv.x * w.x - tv.y * w.y;
+          x[t].y -= tv.x * w.y + tv.y * w.x;
+          row[lane + 32 * t] = x[t];
+          an[t] += cabs2(x[t]);
+          as[t] = cfma(cconj(xpn), x[t], as[t]);
         }
-        s = cscale(s, 1.0 / A[(size_t)i * r + i].x);  // R[i][i] real positive
       }
-      Rinv[(size_t)i * ldr + c] = s;
     }
+    hq_cta_part<double>(an, red1, r, 0, a.npart);
+    hq_cta_part<double2>(as, red2, r, 0, a.wpart);
+    grid.sync();
+    hq_reduce_a<double>(a.npart, a.nfin, r, 0, done);
+    hq_reduce_a<double2>(a.wpart, a.wfin, r, 0, done);
+    grid.sync();
+    hq_reduce_b<double>(a.nfin, r, 0, done, nrm);
+    hq_reduce_b<double2>(a.wfin, r, 0, done, sv);
+  }
+  if (blockIdx.x == 0) {
+    for (int j = tid; j < rank; j += kHqThreads) a.perm[j] = perm[j];
+    if (tid == 0) *a.rank = rank;
+  }
+
+  // Q(:, :rank) = H_0 ... H_{rank-1} [I; 0], accumulated backward: H_j acts on rows >= j and columns >= j
+  // (columns < j are still e_c there). One pass per step applies H_j and accumulates y for H_{j-1}.
+  double2* Q = a.Q;
+  const size_t ldq = a.ldq;
+  for (int i = lo + warp; i < hi; i += kHqWarps)
+    for (int c = lane; c < rank; c += 32) Q[(size_t)i * ldq + c] = make_double2(i == c ? 1.0 : 0.0, 0.0);
+  if (rank > 0) {  // y for H_{rank-1} on [I; 0]: y_c = conj(v(c)), c >= rank - 1
+    const int j = rank - 1;
+    if (tid == 0) wv[j] = cconj(vh[j]);
+    for (int c = j + 1 + tid; c < rank; c += kHqThreads) wv[c] = cconj(__ldcg(X + (size_t)c * ldx + perm[j]));
+  }
+  __syncthreads();
+  for (int j = rank - 1; j >= 0; --j) {
+    const int p = perm[j];
+    const double2 v0 = vh[j];
+    const double tj = tau[j];
+    const int pm = j > 0 ? perm[j - 1] : 0;
+    double2 ay[kHqT];
+#pragma unroll
+    for (int t = 0; t < kHqT; ++t) ay[t] = make_double2(0.0, 0.0);
+    for (int i = lo + warp; i < hi; i += kHqWarps) {
+      if (i < j) continue;
+      double2* qrow = Q + (size_t)i * ldq;
+      const double2 vi = (i == j) ? v0 : X[(size_t)i * ldx + p];
+      const double2 tv = make_double2(tj * vi.x, tj * vi.y);
+      const double2 vm = j > 0 ? X[(size_t)i * ldx + pm] : make_double2(0.0, 0.0);  // v_{j-1}(i), i >= j
+#pragma unroll
+      for (int t = 0; t < kHqT; ++t) {
+        const int c = lane + 32 * t;
+        if (c >= j && c < rank) {
+          const double2 y = wv[c];
+          double2 q = qrow[c];
+          q.x -= tv.x * y.x - tv.y * y.y;
+          q.y -= tv.x * y.y + tv.y * y.x;
+          qrow[c] = q;
+          ay[t] = cfma(cconj(vm), q, ay[t]);
+        }
+      }
+    }
+    if (j == 0) break;
+    hq_cta_part<double2>(ay, red2, r, j, a.wpart);
+    grid.sync();
+    hq_reduce_a<double2>(a.wpart, a.wfin, rank, j, nullptr);
+    grid.sync();
+    hq_reduce_b<double2>(a.wfin, rank, j, nullptr, wv);
+    // row j-1 of Q is still e_{j-1}: it adds conj(v_{j-1}(j-1)) to y_{j-1} (rows >= j hold 0 in column j-1)
+    if (tid == 0) wv[j - 1] = cconj(vh[j - 1]);
+    __syncthreads();
   }
 }
 
-// Xout[:, j] = Xin[:, piv[j]] for j < k (column gather), row stride ld
-__global__ void k_gather_cols(int N, int k, const int* __restrict__ piv, const double2* __restrict__ Xin, int ldin,
-                              double2* __restrict__ Xout, int ldout) {
-  const int64_t tot = (int64_t)N * k;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = e / k;
-    const int j = (int)(e % k);
-    Xout[row * ldout + j] = Xin[row * ldin + piv[j]];
-  }
+size_t house_qr_workspace_bytes(int r) {
+  return align_up((size_t)r * kHouseMaxGrid * sizeof(double2), 256) +
+         align_up((size_t)r * kHouseMaxGrid * sizeof(double), 256) + align_up((size_t)r * sizeof(double2), 256) +
+         (size_t)r * sizeof(double);
+}
+
+int house_qr_launch(int N, int r, double2* X, int ldx, int pivot, double tol, double2* Q, int ldq, int* perm,
+                    int* rank_dev, void* ws, int sm_count, cudaStream_t st) {
+  if (N < 1 || r < 1 || r > kHouseMaxCols) return PRONY_ERR_INVALID;
+  HouseQrArgs a{};
+  a.N = N;
+  a.r = r;
+  a.X = X;
+  a.ldx = ldx;
+  a.pivot = pivot;
+  a.tol = tol;
+  a.Q = Q;
+  a.ldq = ldq;
+  a.perm = perm;
+  a.rank = rank_dev;
+  char* w = (char*)ws;
+  a.wpart = (double2*)w;
+  w += align_up((size_t)r * kHouseMaxGrid * sizeof(double2), 256);
+  a.npart = (double*)w;
+  w += align_up((size_t)r * kHouseMaxGrid * sizeof(double), 256);
+  a.wfin = (double2*)w;
+  w += align_up((size_t)r * sizeof(double2), 256);
+  a.nfin = (double*)w;
+  const size_t smem = (size_t)kHqWarps * r * sizeof(double2);
+  if (cudaFuncSetAttribute(k_house_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return PRONY_ERR_CUDA;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_house_qr, kHqThreads, smem) != cudaSuccess || per_sm < 1)
+    return PRONY_ERR_CUDA;
+  // at least ~32 rows per CTA; never more CTAs than can be co-resident (cooperative launch)
+  const int G = std::max(1, std::min({sm_count * per_sm, kHouseMaxGrid, (N + 31) / 32}));
+  void* args[] = {&a};
+  if (cudaLaunchCooperativeKernel((const void*)k_house_qr, dim3(G), dim3(kHqThreads), args, smem, st) != cudaSuccess)
+    return PRONY_ERR_CUDA;
+  return PRONY_OK;
 }
 
 // ---------------------------------------------------------------------------- one-sided Jacobi SVD

@@ -18,9 +18,28 @@ __global__ void k_gemm_nm(int N, int r, int c, const double2* X, int ldx, const 
 __global__ void k_fro2_parts(int N, int c, const double2* X, int ldx, double* parts);
 __global__ void k_normT2_parts(int d, int n, int64_t box, const double2* grid, double* parts);
 __global__ void k_sum_doubles(int count, const double* parts, double* out);
-__global__ void k_chol_piv(int r, double2* A, int pivot, double tol, int* piv, int* rank_out);
-__global__ void k_trinv_from_lower(int r, int k, const double2* A, double2* Rinv, int ldr);
-__global__ void k_gather_cols(int N, int k, const int* piv, const double2* Xin, int ldin, double2* Xout, int ldout);
+
+// Householder QR of a tall N x r matrix in one cooperative launch (dense.cu, k_house_qr)
+constexpr int kHouseMaxCols = 256;  // r0 = 2m <= 256 (m <= kMaxM = 128)
+constexpr int kHouseMaxGrid = 256;  // CTAs of the cooperative launch (partial buffers are sized for it)
+struct HouseQrArgs {
+  int N, r, pivot;
+  double tol;
+  double2* X;  // N x r, ld ldx: overwritten (reflector tails / R)
+  int ldx;
+  double2* Q;  // out: N x rank, ld ldq, orthonormal columns in pivoted order
+  int ldq;
+  int* perm;   // out: perm[k] = column of X in column k of Q R (k < rank)
+  int* rank;   // out: rank (pivot) or min(N, r)
+  double2* wpart;  // [r][G] per-CTA column partials
+  double* npart;
+  double2* wfin;   // [r] reduced columns
+  double* nfin;
+};
+__global__ void k_house_qr(HouseQrArgs a);
+size_t house_qr_workspace_bytes(int r);
+int house_qr_launch(int N, int r, double2* X, int ldx, int pivot, double tol, double2* Q, int ldq, int* perm,
+                    int* rank_dev, void* ws, int sm_count, cudaStream_t st);
 __global__ void k_jacobi_svd(int rows, int cols, double2* A, double2* Vm, double* sigma, double2* Uout, double2* Vout,
                              int* order, int max_sweeps);
 __global__ void k_permute_sigma(int cols, const double* sigma, const int* order, double* out);

@@ -3,9 +3,9 @@
 //
 //   block_power_svd     reduced SVD T = U Sigma V* by the block power method of Alg. 3
 //                       (P:179-201), with T V and T^H U from toeplitz_apply (the k_project gather),
-//                       Cholesky-QR (Gram on all SMs, factor in one CTA) for the QR steps and
-//                       diagonal-pivoted Cholesky of the Gram for the pivoted-QR rank determination
-//                       (R22), one-sided Jacobi SVD of Q_k.
+//                       Householder QR of the tall blocks in one cooperative launch (k_house_qr,
+//                       P:203), column-pivoted in the first iteration for the rank (
+//                       DESIGN.md R22), one-sided Jacobi SVD of Q_k.
 //   diagonalize_launch  C_mu = sum mu_l S_l, W from eig(C_mu), z_j(l) = (W^-1 S_l W)_jj
 //                       (P:34-37, 57), t = (-arg z / 2 pi) mod 1 (R4).
 //
@@ -27,7 +27,7 @@ namespace {
 constexpr int kGramKS = 32;  // K splits of the Gram products
 
 struct SvdLayout {
-  size_t V0, A1, A2, A3, A4, Gp, G, Rinv, Q, Jv, Ju, Jvv, piv, ints, dparts, dscal, sig, apply, total;
+  size_t V0, A1, A2, A3, A4, Gp, Q, Jv, Ju, Jvv, piv, ints, dparts, dscal, sig, hq, apply, total;
 };
 
 SvdLayout svd_layout(int d, int n, int N, int m) {
@@ -46,8 +46,6 @@ SvdLayout svd_layout(int d, int n, int N, int m) {
   s.A3 = take(nr);
   s.A4 = take(nr);
   s.Gp = take((size_t)kGramKS * r0 * r0 * sizeof(double2));
-  s.G = take((size_t)r0 * r0 * sizeof(double2));
-  s.Rinv = take((size_t)r0 * r0 * sizeof(double2));
   s.Q = take((size_t)r0 * r0 * sizeof(double2));
   s.Jv = take((size_t)r0 * r0 * sizeof(double2));
   s.Ju = take((size_t)r0 * r0 * sizeof(double2));
@@ -57,6 +55,7 @@ SvdLayout svd_layout(int d, int n, int N, int m) {
   s.dparts = take(4096 * sizeof(double));
   s.dscal = take(64 * sizeof(double));
   s.sig = take((size_t)(r0 + 8) * sizeof(double));
+  s.hq = take(house_qr_workspace_bytes(r0));
   s.apply = take(apply_workspace_bytes(d, n, N));
   s.total = off;
   return s;
@@ -86,39 +85,21 @@ void fro2(const Ctx& c, const double2* X, int ldx, int cols, double* out) {
   k_sum_doubles<<<1, 32, 0, c.st>>>(nb, (double*)(c.w + c.L.dparts), out);
 }
 
-// Orthonormal basis of the range of X (N x r): diagonal-pivoted Cholesky of X^H X (rank by the
-// trailing-trace criterion when pivot = 1), Xout = X(:, piv(1:rank)) R11^-1. Returns rank (host).
-int chol_basis(const Ctx& c, const double2* X, int ldx, int r, int pivot, double tol, double2* Xout, int ldout,
-               int* rank_host) {
-  double2* G = c.P(c.L.G);
-  gram(c, X, ldx, r, X, ldx, r, G);
+// Orthonormal basis of the range of X (N x r) into Xout: Q(:, :rank) of the Householder QR (X is
+// overwritten); with pivot = 1 the rank is the first k with ||R(k:, k:)||_F <= tol ||R||_F,
+// otherwise rank = r. Returns the rank on the host.
+int house_basis(const Ctx& c, double2* X, int ldx, int r, int pivot, double tol, double2* Xout, int ldout,
+                int* rank_host) {
   int* piv = (int*)(c.w + c.L.piv);
   int* rk = (int*)(c.w + c.L.ints);
-  k_chol_piv<<<1, 512, 0, c.st>>>(r, G, pivot, tol, piv, rk);
+  int rc = house_qr_launch(c.N, r, X, ldx, pivot, tol, Xout, ldout, piv, rk, c.w + c.L.hq, c.sms, c.st);
+  if (rc) return rc;
   int rank = 0;
   if (cudaMemcpyAsync(&rank, rk, sizeof(int), cudaMemcpyDeviceToHost, c.st) != cudaSuccess) return PRONY_ERR_CUDA;
   if (cudaStreamSynchronize(c.st) != cudaSuccess) return PRONY_ERR_CUDA;
   if (rank < 1) return PRONY_ERR_RANK;
-  double2* Rinv = c.P(c.L.Rinv);
-  k_trinv_from_lower<<<(rank + 127) / 128, 128, 0, c.st>>>(r, rank, G, Rinv, rank);
-  // Xp = X(:, piv(1:rank)) into Xout, then Xout = Xp Rinv needs a separate buffer: use A4
-  double2* Xp = c.P(c.L.A4);
-  k_gather_cols<<<grid1((int64_t)c.N * rank, c.sms), 256, 0, c.st>>>(c.N, rank, piv, X, ldx, Xp, rank);
-  dim3 g((c.N + 63) / 64, (rank + 31) / 32);
-  k_gemm_nm<<<g, 256, 0, c.st>>>(c.N, rank, rank, Xp, rank, Rinv, rank, Xout, ldout, 1.0, 0.0);
   *rank_host = rank;
-  return cudaGetLastError() == cudaSuccess ? PRONY_OK : PRONY_ERR_CUDA;
-}
-
-// CholeskyQR2 of a full-rank X (N x r) into Xout (the second pass restores orthogonality)
-int cholqr2(const Ctx& c, const double2* X, int ldx, int r, double2* Xout, int ldout, double2* tmp) {
-  int rank = 0;
-  int rc = chol_basis(c, X, ldx, r, 0, 0.0, tmp, r, &rank);
-  if (rc) return rc;
-  if (rank != r) return PRONY_ERR_RANK;
-  rc = chol_basis(c, tmp, r, r, 0, 0.0, Xout, ldout, &rank);
-  if (rc) return rc;
-  return rank == r ? PRONY_OK : PRONY_ERR_RANK;
+  return PRONY_OK;
 }
 
 }  // namespace
@@ -138,8 +119,6 @@ int block_power_svd(int d, int n, int N, const double2* grid, int m, double tol,
   void* aws = c.w + c.L.apply;
   double2 *Vk = c.P(c.L.V0), *A1 = c.P(c.L.A1), *A2 = c.P(c.L.A2), *A3 = c.P(c.L.A3);
   double* dscal = (double*)(c.w + c.L.dscal);
-  // the Gram-based trailing norm resolves ||R(i:,i:)|| / ||R|| only down to ~sqrt(eps_M) (R22)
-  const double rank_tol = std::max(tol, 1e-7);
   const double res_tol = std::max(tol, 1e-12);
 
   // ||T||_F^2 from the grid
@@ -148,10 +127,10 @@ int block_power_svd(int d, int n, int N, const double2* grid, int m, double tol,
   const int nb = std::min(4096, 2 * sm_count);
   k_normT2_parts<<<nb, 256, 0, st>>>(d, n, box, grid, (double*)(c.w + c.L.dparts));
   k_sum_doubles<<<1, 32, 0, st>>>(nb, (double*)(c.w + c.L.dparts), dscal);
-  // V0: seeded complex Gaussian, orthonormalized (R14)
+  // V0: seeded complex Gaussian, orthonormalized by Householder QR (R14)
   k_fill_random<<<grid1((int64_t)N * r0, sm_count), 256, 0, st>>>((int64_t)N * r0, seed, A1, N, r0, r0);
   int rv = 0, ru = 0, rc;
-  rc = chol_basis(c, A1, r0, r0, 1, rank_tol, Vk, r0, &rv);  // (also guards a rank-deficient random block)
+  rc = house_basis(c, A1, r0, r0, 0, 0.0, Vk, r0, &rv);
   if (rc) return rc;
   double normT2 = 0.0;
   if (cudaMemcpyAsync(&normT2, dscal, sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess) return PRONY_ERR_CUDA;
@@ -164,22 +143,14 @@ int block_power_svd(int d, int n, int N, const double2* grid, int m, double tol,
   double resid = -1.0;
   int it = 0;
   for (it = 1; it <= max_iter; ++it) {
-    // U_k = basis of T V_{k-1} (A1 -> A2)
-    if (it == 1) rc = chol_basis(c, A1, r0, rv, 1, rank_tol, A2, r0, &ru);
-    else {
-      rc = cholqr2(c, A1, r0, rv, A2, r0, A3);
-      ru = rv;
-    }
+    // U_k = Q factor of Ubar_k = T V_{k-1} (A1 -> A2; Alg. 3 line 7: plain QR, rank-deficient blocks allowed)
+    rc = house_basis(c, A1, r0, rv, 0, 0.0, A2, r0, &ru);
     if (rc) return rc;
     // Vbar_k = T^H U_k (A2 -> A3)
     rc = toeplitz_apply_launch(d, n, N, grid, 0, 1, A2, r0, ru, A3, r0, aws, sm_count, st);
     if (rc) return rc;
-    // V_k = pivoted (first iteration, rank determination P:203) or plain QR basis (A3 -> Vk)
-    if (it == 1) rc = chol_basis(c, A3, r0, ru, 1, rank_tol, Vk, r0, &rv);
-    else {
-      rc = cholqr2(c, A3, r0, ru, Vk, r0, A1);
-      rv = ru;
-    }
+    // V_k = Q factor of Vbar_k, column-pivoted in the first iteration (rank determination)
+    rc = house_basis(c, A3, r0, ru, it == 1 ? 1 : 0, tol, Vk, r0, &rv);
     if (rc) return rc;
     // T V_k (Vk -> A1): next Ubar and the residual
     rc = toeplitz_apply_launch(d, n, N, grid, 0, 0, Vk, r0, rv, A1, r0, aws, sm_count, st);
