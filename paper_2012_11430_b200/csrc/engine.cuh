@@ -28,7 +28,9 @@ __device__ __forceinline__ void mma16x8x4(double (&c)[4], double a0, double a1, 
 // computed as Ar [Br | Bi] (acc0) and Ai [Br | Bi] (acc1) on ONE 8-wide B fragment — lane column g reads
 // column (g & 3) of the tile, the real part for g < 4 and the imaginary part for g >= 4 — so 2 real DMMA
 // products instead of the 3 of a half-empty 3M tile; acc_packed_to_complex recombines (4M form).
-template <int NT, int NA, int MODE, bool CONJB = false, bool PK = false>
+// SREG (MODE 3): the sum operands Re+Im of A and Re+Im (Re-Im for CONJB) of B are formed in registers from
+// the complex fragments (As, Bs unused): no sum planes in shared memory, one DADD per n-tile per k-step.
+template <int NT, int NA, int MODE, bool CONJB = false, bool PK = false, bool SREG = false>
 __device__ __forceinline__ void warp_cmma_k4(double (&acc)[3][NT][4], const double2* __restrict__ Ac,
                                              const double* __restrict__ As, int lda, int ldas,
                                              const double2* __restrict__ Bc, const double* __restrict__ Bs,
@@ -38,11 +40,16 @@ __device__ __forceinline__ void warp_cmma_k4(double (&acc)[3][NT][4], const doub
   const double2 a1 = Ac[q * lda + g + 8];
   double s0 = 0.0, s1 = 0.0;
   if constexpr (MODE == 3) {
-    s0 = As[q * ldas + g];
-    s1 = As[q * ldas + g + 8];
+    if constexpr (SREG) {
+      s0 = a0.x + a0.y;
+      s1 = a1.x + a1.y;
+    } else {
+      s0 = As[q * ldas + g];
+      s1 = As[q * ldas + g + 8];
+    }
   }
   const double2* brow = Bc + q * ldb + g;
-  const double* bsrow = Bs + q * ldbs + g;
+  const double* bsrow = SREG ? nullptr : Bs + q * ldbs + g;
   constexpr double sb = CONJB ? -1.0 : 1.0;
 #pragma unroll
   for (int j = 0; j < NA; ++j) {
@@ -58,7 +65,9 @@ __device__ __forceinline__ void warp_cmma_k4(double (&acc)[3][NT][4], const doub
     {
       const double2 b = brow[8 * j];
       if constexpr (MODE == 3) {
-        const double bs = bsrow[8 * j];
+        double bs;
+        if constexpr (SREG) bs = CONJB ? b.x - b.y : b.x + b.y;
+        else bs = bsrow[8 * j];
         mma16x8x4(acc[0][j], a0.x, a1.x, b.x);
         mma16x8x4(acc[1][j], sb * a0.y, sb * a1.y, b.y);  // Ai (sb Bi): sign folded into the A operand
         mma16x8x4(acc[2][j], s0, s1, bs);

@@ -149,6 +149,11 @@ constexpr int kGatherThreads = 96;  // producer threads doing the A gather (warp
 #ifndef PRONY_GATHER_UNROLL
 #define PRONY_GATHER_UNROLL 2
 #endif
+#ifndef PRONY_PROJ_SREG
+#define PRONY_PROJ_SREG 0
+#endif
+// SREG: the 3M sum operands formed in the consumers' registers (no gsum / Vsum planes gathered or copied)
+constexpr bool kProjSreg = PRONY_PROJ_SREG != 0;
 constexpr int kKkUnroll = PRONY_KK_UNROLL;
 constexpr int kGatherUnroll = PRONY_GATHER_UNROLL;
 constexpr int kConsumerRegs = PRONY_CONSUMER_REGS;  // 384 x 160 + 128 x 32 = 65536 (12 warps); 256 x 240 + 4096 (8)
@@ -244,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
           int idx = ok ? pa - phc : 0;
           PRONY_CHECK_INDEX(idx, 0, p.box);
           cp_async16(st + (uint32_t)(T::A_C + 2 * (kc * T::LDA + ra)) * 8u, grid + idx, ok ? 16 : 0);
-          if constexpr (MODE == 3)
+          if constexpr (MODE == 3 && !kProjSreg)
             cp_async8(st + (uint32_t)(T::A_S + kc * T::LDAS + ra) * 8u, gsum + idx, ok ? 8 : 0);
         }
         mbar_arrive_cp_async(full0 + 8u * s);
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
         const int h0 = h_begin + kt * kBK;
         if (kt >= kStages) mbar_wait(empty0 + 8u * s, (uint32_t)((kt / kStages) - 1) & 1u);
         const int nrows = min(kBK, h_end - h0);
-        const uint32_t bytes_row = (uint32_t)m * 16u + (MODE == 3 ? (uint32_t)NP * 8u : 0u);
+        const uint32_t bytes_row = (uint32_t)m * 16u + (MODE == 3 && !kProjSreg ? (uint32_t)NP * 8u : 0u);
         if (plane == 0) mbar_arrive_expect_tx(full0 + 8u * s, bytes_row * (uint32_t)nrows);
         __syncwarp();
         const uint32_t st = sbase + (uint32_t)(s * T::STAGE) * 8u;
@@ -270,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
           if (!sum_plane) {
             bulk_g2s(st + (uint32_t)(T::B_C + 2 * kr * T::LDB) * 8u, V + (size_t)h * p.ldv, (uint32_t)m * 16u,
                      full0 + 8u * s);
-          } else if constexpr (MODE == 3) {
+          } else if constexpr (MODE == 3 && !kProjSreg) {
             bulk_g2s(st + (uint32_t)(T::B_S + kr * T::LDBS) * 8u, vsum + (size_t)h * NP, (uint32_t)NP * 8u,
                      full0 + 8u * s);
           }
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
         const double* Bs = st + T::B_S + t0 * 8;
 #pragma unroll kKkUnroll
         for (int kk = 0; kk < kBK / 4; ++kk)
-          warp_cmma_k4<NT, NA, MODE, false, PK>(acc, Ac + kk * 4 * T::LDA, As + kk * 4 * T::LDAS, T::LDA, T::LDAS,
+          warp_cmma_k4<NT, NA, MODE, false, PK, kProjSreg>(acc, Ac + kk * 4 * T::LDA, As + kk * 4 * T::LDAS, T::LDA, T::LDAS,
                                                 Bc + kk * 4 * T::LDB, Bs + kk * 4 * T::LDBS, T::LDB, T::LDBS, g, q);
       }
       __syncwarp();
@@ -576,42 +581,37 @@ __global__ void __launch_bounds__(kReduceThreads, 1) k_reduce(RedParams p) {
 // ---------------------------------------------------------------------------- warp-specialized reduce
 // k_reduce_ws (3M, the default): the same S_part[l][P] = U[rows_P]^* Y[rows_P] (computed transposed,
 // S^T = Y^T conj(U)) with 8 consumer warps of 232 registers (WM = 4 along j -> 64-row j-blocks, WN = 2 along
-// i with up to 8 n-tiles per warp; the last n-tile packed when m % 8 <= 4) and the producer warpgroup feeding a kRedWsStages-deep ring of 16-row slabs: producer warp 0 moves each slab with
-// one bulk copy per Y row (columns [j0, j0 + BJ)) and per U row (through the row map; lanes 16..31 load the
-// map entries in parallel), completing on the slab's "landed" mbarrier (expect_tx); then the 4 producer
-// warps form the 3M sum planes (Re+Im of Y, Re-Im of U for the conj-B operand), zero the rows that have no
-// data, and arrive on "full"; consumers release slabs on "empty". No CTA-wide barrier in the loop, no DADD
-// on the consumer warps. Grid (RP, d, nj): every j-block takes the same row partitions (the U rows, which
-// dominate the traffic, cost the same for each); rp_j[z] < RP would make the extra CTAs write zero partials.
-constexpr int kRedWsStages = 3;
+// i with up to 8 n-tiles per warp; the last n-tile packed when m % 8 <= 4) fed by ONE producer warp through a
+// kRedWsStages-deep ring of 16-row slabs: lanes 0..15 move the slab's Y rows (columns [j0, j0 + BJ)) and
+// lanes 16..31 its U rows (through the row map) with one bulk copy each, completing on the stage's "full"
+// mbarrier (expect_tx); a U row with no data (no row of T_l, or past the partition) is zeroed in place
+// first. The 3M sum operands are formed in the consumers' registers (warp_cmma_k4 SREG), so the producer
+// does no arithmetic and nothing waits for a sum plane; consumers release slabs on "empty". Grid
+// (RP, d, nj): every j-block takes the same row partitions (the U rows, which dominate the traffic, cost
+// the same for each); rp_j[z] < RP would make the extra CTAs write zero partials.
+constexpr int kRedWsStages = 4;
 constexpr int kRwsCons = 8;                        // consumer warps: WM = 4 along j x WN = 2 along i
-constexpr int kRwsThreads = 32 * (kRwsCons + 4);   // + the producer warpgroup
+constexpr int kRwsThreads = 32 * (kRwsCons + 4);   // + the producer warpgroup (warp 0 of it copies)
 constexpr int kRwsConsRegs = 232, kRwsProdRegs = 40;  // 256 x 232 + 128 x 40 = 64512 <= 65536
 template <int NT, int WN>
 struct RedWsTile {
   static constexpr int WM = kRwsCons / WN;
   static constexpr int BJ = 16 * WM;       // rows j of S^T per CTA
   static constexpr int NPU = 8 * NT * WN;  // capacity of the i dimension
-  static constexpr int LDA = BJ + 2, LDAS = BJ + 4, LDB = NPU + 2, LDBS = NPU + 4;
-  static constexpr int A_C = 0, A_S = A_C + 2 * kRedSlab * LDA, B_C = A_S + kRedSlab * LDAS,
-                       B_S = B_C + 2 * kRedSlab * LDB, STAGE = B_S + kRedSlab * LDBS;
-  static constexpr int BAR = kRedWsStages * STAGE;                  // 3 mbarriers per stage
-  static constexpr int VAL = BAR + 3 * kRedWsStages;                // per stage: 16 U-row flags (ints)
-  static constexpr size_t SMEM = (size_t)VAL * sizeof(double) + (size_t)kRedWsStages * kRedSlab * sizeof(int);
-  static_assert(STAGE % 2 == 0 && A_S % 2 == 0 && B_C % 2 == 0 && B_S % 2 == 0, "16-byte alignment");
-  static_assert((2 * LDA) % 2 == 0 && (2 * LDB) % 2 == 0, "bulk-copy rows stay 16-byte aligned");
+  static constexpr int LDA = BJ + 2, LDB = NPU + 2;
+  static constexpr int A_C = 0, B_C = A_C + 2 * kRedSlab * LDA, STAGE = B_C + 2 * kRedSlab * LDB;
+  static constexpr int BAR = kRedWsStages * STAGE;  // 2 mbarriers per stage
+  static constexpr size_t SMEM = (size_t)(BAR + 2 * kRedWsStages) * sizeof(double);
+  static_assert(STAGE % 2 == 0 && B_C % 2 == 0, "16-byte alignment");
 };
 
 template <int NT, int WN>
 __global__ void __launch_bounds__(kRwsThreads, 1) k_reduce_ws(RedParams p) {
   using T = RedWsTile<NT, WN>;
   constexpr int WM = T::WM, BJ = T::BJ;
-  constexpr int kProd = kRwsThreads - kRwsCons * 32;  // producer threads
   extern __shared__ __align__(16) double smem[];
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  const uint32_t full0 = sbase + (uint32_t)T::BAR * 8u, empty0 = full0 + (uint32_t)kRedWsStages * 8u,
-                 landed0 = empty0 + (uint32_t)kRedWsStages * 8u;
-  int* uval = reinterpret_cast<int*>(smem + T::VAL);  // [stage][16]: U row of the slab row, or -1
+  const uint32_t full0 = sbase + (uint32_t)T::BAR * 8u, empty0 = full0 + (uint32_t)kRedWsStages * 8u;
   const int tid = threadIdx.x;
   const int l = blockIdx.y, P = blockIdx.x, jb = blockIdx.z;
   const int j0 = jb * BJ;
@@ -630,88 +630,59 @@ __global__ void __launch_bounds__(kRwsThreads, 1) k_reduce_ws(RedParams p) {
   const int nslab = (rend - rbeg + kRedSlab - 1) / kRedSlab;
   const int ny = min(BJ, NP - j0);  // Y columns this j-block reads
 
+  // zero once: padding columns (i >= m, j >= ny) are never written by the copies
   for (int e = tid; e < kRedWsStages * T::STAGE; e += kRwsThreads) smem[e] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < kRedWsStages; ++s) {
-      mbar_init(full0 + 8u * s, kProd);
+      mbar_init(full0 + 8u * s, 1);
       mbar_init(empty0 + 8u * s, kRwsCons);
-      mbar_init(landed0 + 8u * s, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
   if (tid >= kRwsCons * 32) {
-    // ================================================================== producer warpgroup
+    // ================================================================== producer warp
     setmaxnreg_dec<kRwsProdRegs>();
-    const int pt = tid - kRwsCons * 32;
-    const int plane = pt & 31;
-    for (int st = 0; st <= nslab; ++st) {
-      if (st < nslab && pt < 32) {  // producer warp 0 issues slab st
-        const int s = st % kRedWsStages;
-        if (st >= kRedWsStages) mbar_wait(empty0 + 8u * s, (uint32_t)((st / kRedWsStages) - 1) & 1u);
-        const int r = plane & (kRedSlab - 1);
-        const int row = rbeg + st * kRedSlab + r;
-        uint32_t bytes = 0;
-        const double2* src = nullptr;
-        uint32_t dst = sbase + (uint32_t)(s * T::STAGE) * 8u;
-        if (plane < kRedSlab) {  // Y row
-          if (row < rend) {
-            bytes = (uint32_t)ny * 16u;
-            src = p.Y + ((size_t)p.yoff[l] + row) * NP + j0;
-          }
-          dst += (uint32_t)(T::A_C + 2 * r * T::LDA) * 8u;
-        } else {  // U row through the map
-          int urow = -1;
-          if (row < rend) {
-            urow = p.kb[l] + row;
-            if (p.umap) urow = __ldg(p.umap + (size_t)l * p.E + urow);  // -1: no row of T_l
-          }
-          uval[s * kRedSlab + r] = urow;
-          if (urow >= 0) {
-            bytes = (uint32_t)m * 16u;
-            src = p.U + (size_t)urow * m;
-          }
-          dst += (uint32_t)(T::B_C + 2 * r * T::LDB) * 8u;
+    if (tid >= kRwsCons * 32 + 32) return;
+    const int lane = tid & 31;
+    const int r = lane & (kRedSlab - 1);
+    for (int st = 0; st < nslab; ++st) {
+      const int s = st % kRedWsStages;
+      if (st >= kRedWsStages) mbar_wait(empty0 + 8u * s, (uint32_t)((st / kRedWsStages) - 1) & 1u);
+      const int row = rbeg + st * kRedSlab + r;
+      uint32_t bytes = 0;
+      const double2* src = nullptr;
+      uint32_t dst = sbase + (uint32_t)(s * T::STAGE) * 8u;
+      if (lane < kRedSlab) {  // Y row (a row past the partition keeps stale finite data: its U row is zero)
+        if (row < rend) {
+          bytes = (uint32_t)ny * 16u;
+          src = p.Y + ((size_t)p.yoff[l] + row) * NP + j0;
         }
-        uint32_t tot = bytes;
+        dst += (uint32_t)(T::A_C + 2 * r * T::LDA) * 8u;
+      } else {  // U row through the map
+        int urow = -1;
+        if (row < rend) {
+          urow = p.kb[l] + row;
+          if (p.umap) urow = __ldg(p.umap + (size_t)l * p.E + urow);  // -1: no row of T_l
+        }
+        double2* Urow = reinterpret_cast<double2*>(smem + s * T::STAGE + T::B_C) + r * T::LDB;
+        if (urow >= 0) {
+          bytes = (uint32_t)m * 16u;
+          src = p.U + (size_t)urow * m;
+        } else {
+          for (int i = 0; i < m; ++i) Urow[i] = make_double2(0.0, 0.0);
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // before later bulk writes of the row
+        }
+        dst += (uint32_t)(T::B_C + 2 * r * T::LDB) * 8u;
+      }
+      uint32_t tot = bytes;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
-        if (plane == 0) mbar_arrive_expect_tx(landed0 + 8u * s, tot);  // also publishes uval (release)
-        __syncwarp();
-        if (bytes) bulk_g2s(dst, src, bytes, landed0 + 8u * s);
-      }
-      if (st >= 1) {  // all producer warps: sum planes of slab st-1
-        const int s = (st - 1) % kRedWsStages;
-        mbar_wait(landed0 + 8u * s, (uint32_t)((st - 1) / kRedWsStages) & 1u);
-        const int r0 = rbeg + (st - 1) * kRedSlab;
-        double* sp = smem + s * T::STAGE;
-        double2* Yc = reinterpret_cast<double2*>(sp + T::A_C);
-        double2* Uc = reinterpret_cast<double2*>(sp + T::B_C);
-        for (int e = pt; e < kRedSlab * BJ; e += kProd) {
-          const int r = e / BJ, jj = e % BJ;
-          double v = 0.0;
-          if (r0 + r < rend) {
-            const double2 y = Yc[r * T::LDA + jj];
-            v = y.x + y.y;
-          } else {
-            Yc[r * T::LDA + jj] = make_double2(0.0, 0.0);  // no row: stale data of an earlier slab
-          }
-          sp[T::A_S + r * T::LDAS + jj] = v;
-        }
-        for (int e = pt; e < kRedSlab * T::NPU; e += kProd) {
-          const int r = e / T::NPU, i = e % T::NPU;
-          double v = 0.0;
-          if (uval[s * kRedSlab + r] >= 0) {
-            const double2 u = Uc[r * T::LDB + i];
-            v = u.x - u.y;  // the B operand is conj(U)
-          } else {
-            Uc[r * T::LDB + i] = make_double2(0.0, 0.0);
-          }
-          sp[T::B_S + r * T::LDBS + i] = v;
-        }
-        mbar_arrive(full0 + 8u * s);
-      }
+      for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+      __syncwarp();  // the zeroed rows are ordered before the release below
+      if (lane == 0) mbar_arrive_expect_tx(full0 + 8u * s, tot);
+      __syncwarp();
+      if (bytes) bulk_g2s(dst, src, bytes, full0 + 8u * s);
     }
     return;
   }
@@ -744,13 +715,11 @@ __global__ void __launch_bounds__(kRwsThreads, 1) k_reduce_ws(RedParams p) {
       if constexpr (NA > 0) {
         const double* sp = smem + s * T::STAGE;
         const double2* Ac = reinterpret_cast<const double2*>(sp + T::A_C) + wm * 16;
-        const double* As = sp + T::A_S + wm * 16;
         const double2* Bc = reinterpret_cast<const double2*>(sp + T::B_C) + t0 * 8;
-        const double* Bs = sp + T::B_S + t0 * 8;
 #pragma unroll
         for (int kk = 0; kk < kRedSlab / 4; ++kk)
-          warp_cmma_k4<NT, NA, 3, true, PK>(acc, Ac + kk * 4 * T::LDA, As + kk * 4 * T::LDAS, T::LDA, T::LDAS,
-                                            Bc + kk * 4 * T::LDB, Bs + kk * 4 * T::LDBS, T::LDB, T::LDBS, g, q);
+          warp_cmma_k4<NT, NA, 3, true, PK, true>(acc, Ac + kk * 4 * T::LDA, nullptr, T::LDA, 0,
+                                                  Bc + kk * 4 * T::LDB, nullptr, T::LDB, 0, g, q);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8u * s);

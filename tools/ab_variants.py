@@ -23,6 +23,9 @@ VARIANTS = {
     "vt64": ["PRONY_VLS_TILE=64"],
     "bk8s5": ["PRONY_BK=8", "PRONY_STAGES=5"],
     "solvet": ["PRONY_SOLVE_TIMING"],
+    "sreg": ["PRONY_PROJ_SREG=1"],
+    "sregkk2": ["PRONY_PROJ_SREG=1", "PRONY_KK_UNROLL=2"],
+    "sregkk1": ["PRONY_PROJ_SREG=1", "PRONY_KK_UNROLL=1"],
 }
 
 if __name__ == "__main__":
