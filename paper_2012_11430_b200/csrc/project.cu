@@ -32,6 +32,50 @@ static int cmul_mode() {
 }
 
 // ---------------------------------------------------------------------------- prep
+// Vsum[h][c] = Re+Im of V[h][c] (0 for the padding columns c >= m), rows [r0, r1), with 4 independent loads in
+// flight per thread (the loop is HBM-latency bound otherwise); 32-bit index arithmetic when (r1 - r0) NP fits
+template <typename I>
+__device__ __forceinline__ void vsum_rows_t(int r0, int r1, int m, int ldv, int NP, const double2* __restrict__ V,
+                                            double* __restrict__ vsum) {
+  const I nv = (I)(r1 - r0) * NP;
+  const I stride = (I)gridDim.x * blockDim.x;
+  I e = (I)blockIdx.x * blockDim.x + threadIdx.x;
+  double* out = vsum + (size_t)r0 * NP;
+  for (; e + 3 * stride < nv; e += 4 * stride) {
+    double sv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const I eu = e + u * stride;
+      const I h = r0 + eu / NP;
+      const int c = (int)(eu % NP);
+      sv[u] = 0.0;
+      if (c < m) {
+        const double2 v = __ldg(V + (size_t)h * ldv + c);
+        sv[u] = v.x + v.y;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) out[e + u * stride] = sv[u];
+  }
+  for (; e < nv; e += stride) {
+    const I h = r0 + e / NP;
+    const int c = (int)(e % NP);
+    double sv = 0.0;
+    if (c < m) {
+      const double2 v = __ldg(V + (size_t)h * ldv + c);
+      sv = v.x + v.y;
+    }
+    out[e] = sv;
+  }
+}
+__device__ __forceinline__ void vsum_rows(int r0, int r1, int m, int ldv, int NP, const double2* __restrict__ V,
+                                          double* __restrict__ vsum) {
+  if ((int64_t)(r1 - r0) * NP + 4LL * gridDim.x * blockDim.x < 2147483647LL)
+    vsum_rows_t<int>(r0, r1, m, ldv, NP, V, vsum);
+  else
+    vsum_rows_t<int64_t>(r0, r1, m, ldv, NP, V, vsum);
+}
+
 __global__ void k_prep(int d, int n, int N, int m, int ldv, int NP, int64_t box, const double2* __restrict__ grid,
                        const double2* __restrict__ V, int32_t* __restrict__ ptab, double* __restrict__ gsum,
                        double* __restrict__ vsum, int vrows) {
@@ -55,32 +99,12 @@ __global__ void k_prep(int d, int n, int N, int m, int ldv, int NP, int64_t box,
     const double2 v = grid[e];
     gsum[e] = v.x + v.y;
   }
-  const int64_t nv = (int64_t)vrows * NP;  // Vsum rows [0, vrows) (the rest: k_vsum)
-  for (int64_t e = t0; e < nv; e += stride) {
-    const int64_t h = e / NP;
-    const int c = (int)(e % NP);
-    double s = 0.0;
-    if (c < m) {
-      const double2 v = V[h * ldv + c];
-      s = v.x + v.y;
-    }
-    vsum[e] = s;
-  }
+  vsum_rows(0, vrows, m, ldv, NP, V, vsum);
 }
 
 // Vsum rows [r0, r1) (the part of V that arrives after k_prep ran, prony_pencil_host)
 __global__ void k_vsum(int r0, int r1, int m, int ldv, int NP, const double2* __restrict__ V, double* __restrict__ vsum) {
-  const int64_t nv = (int64_t)(r1 - r0) * NP;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nv; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t h = r0 + e / NP;
-    const int c = (int)(e % NP);
-    double sv = 0.0;
-    if (c < m) {
-      const double2 v = V[h * ldv + c];
-      sv = v.x + v.y;
-    }
-    vsum[h * NP + c] = sv;
-  }
+  vsum_rows(r0, r1, m, ldv, NP, V, vsum);
 }
 
 // Shared-row tables (F8): for e in E = {0..n+1}^d with coordinates c (base n+2, last
@@ -1012,7 +1036,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
     return PRONY_ERR_CUDA;
   const bool split = sp && pl.KC > 1;
   const int vrows0 = split ? std::min(pl.chunk_w, g.N) : g.N;
-  k_prep<<<2 * sm_count, 256, 0, st>>>(g.d, g.n, g.N, g.m, g.m, pl.shape.NP, box, grid, V, ptab, gsum, vsum,
+  k_prep<<<8 * sm_count, 256, 0, st>>>(g.d, g.n, g.N, g.m, g.m, pl.shape.NP, box, grid, V, ptab, gsum, vsum,
                                        vrows0);
   if (g.shared) k_prep_ext<<<sm_count, 256, 0, st>>>(g.d, g.n, E, etab, umap);
 
@@ -1099,7 +1123,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
       return PRONY_ERR_CUDA;
     lrc = launch_main(p, dim3(grd.x, 1, grd.z), st, info);
     if (lrc != PRONY_OK) return lrc;
-    k_vsum<<<2 * sm_count, 256, 0, sp->s_rest>>>(vrows0, g.N, g.m, g.m, pl.shape.NP, V, vsum);
+    k_vsum<<<8 * sm_count, 256, 0, sp->s_rest>>>(vrows0, g.N, g.m, g.m, pl.shape.NP, V, vsum);
     ProjParams pr = p;
     pr.chunk_base = 1;
     lrc = launch_main(pr, dim3(grd.x, pl.KC - 1, grd.z), sp->s_rest, nullptr);
@@ -1456,7 +1480,7 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
     project_plan(gg, sm_count, &pl);
     const int nrb = (pl.max_rows + pl.shape.BM - 1) / pl.shape.BM;
     if (pl.KC > 1 && cudaMemsetAsync(counters, 0, (size_t)nrb * sizeof(int), st) != cudaSuccess) return PRONY_ERR_CUDA;
-    k_prep<<<2 * sm_count, 256, 0, st>>>(d, n, N, wcols, ldx, pl.shape.NP, box, g, X + c0, ptab, gsum, vsum, N);
+    k_prep<<<8 * sm_count, 256, 0, st>>>(d, n, N, wcols, ldx, pl.shape.NP, box, g, X + c0, ptab, gsum, vsum, N);
     ProjParams p{};
     p.grid = g;
     p.gsum = gsum;
