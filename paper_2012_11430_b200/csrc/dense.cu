@@ -583,19 +583,28 @@ int house_qr_launch(int N, int r, double2* X, int ldx, int pivot, double tol, do
 }
 
 // ---------------------------------------------------------------------------- one-sided Jacobi SVD
-// One CTA. A (rows x cols, ld cols, rows >= cols) is overwritten by A V = U Sigma; V (cols x cols)
-// accumulates the rotations. Round-robin column pairs (one warp per pair), sweeps until every pair
+// One CTA. A (rows x cols, ld cols, rows >= cols; overwritten by U) is rotated into A V = U Sigma; V
+// (cols x cols) accumulates the rotations. Round-robin column pairs (one warp per pair), sweeps until every pair
 // satisfies |a_p^H a_q| <= eps * ||a_p|| ||a_q||. Then sigma_j = ||a_j||, U = a_j / sigma_j, sorted
 // descending (perm applied to U and V columns). Used for Q_k = U_Q Sigma V_Q^H (Alg. 3).
 __global__ void __launch_bounds__(1024) k_jacobi_svd(int rows, int cols, double2* __restrict__ A,
                                                      double2* __restrict__ Vm, double* __restrict__ sigma,
                                                      double2* __restrict__ Uout, double2* __restrict__ Vout,
                                                      int* __restrict__ order, int max_sweeps) {
+  // The sweeps run on column-major copies (At = A^T in Uout, Vt in Vm: column p contiguous), so a warp's
+  // lanes read consecutive entries of a column (coalesced) instead of one row-strided element each; the
+  // arithmetic and its order are unchanged. A (row-major) is the input and scratch for the final U.
   __shared__ int s_rot;
   __shared__ int pairs[2][256];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int cp = cols + (cols & 1);  // even number of players (a virtual zero column if odd)
-  for (int e = tid; e < cols * cols; e += blockDim.x) Vm[e] = make_double2((e / cols) == (e % cols) ? 1.0 : 0.0, 0.0);
+  double2* At = Uout;
+  double2* Vt = Vm;
+  for (int e = tid; e < rows * cols; e += blockDim.x) {
+    const int i = e / cols, j = e % cols;
+    At[(size_t)j * rows + i] = A[e];
+  }
+  for (int e = tid; e < cols * cols; e += blockDim.x) Vt[e] = make_double2((e / cols) == (e % cols) ? 1.0 : 0.0, 0.0);
   __syncthreads();
   const double eps = 1e-15;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
@@ -613,10 +622,12 @@ __global__ void __launch_bounds__(1024) k_jacobi_svd(int rows, int cols, double2
       for (int k = warp; k < cp / 2; k += nw) {
         const int p = pairs[0][k], q = pairs[1][k];
         if (q >= cols) continue;  // virtual column
+        double2* ap = At + (size_t)p * rows;
+        double2* aq = At + (size_t)q * rows;
         double al = 0.0, be = 0.0;
         double2 ga = make_double2(0.0, 0.0);
         for (int i = lane; i < rows; i += 32) {
-          const double2 x = A[(size_t)i * cols + p], y = A[(size_t)i * cols + q];
+          const double2 x = ap[i], y = aq[i];
           al += cabs2(x);
           be += cabs2(y);
           ga = cadd(ga, cmulc(x, y));  // conj(a_p) a_q
@@ -632,18 +643,19 @@ __global__ void __launch_bounds__(1024) k_jacobi_svd(int rows, int cols, double2
         const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
         const double2 ph = make_double2(ga.x / ag, ga.y / ag);  // e^{i phi}, ga = |ga| e^{i phi}
+        const double2 phc = cconj(ph);
         // a_p' = c a_p - s conj(ph) a_q ; a_q' = s ph a_p + c a_q
         for (int i = lane; i < rows; i += 32) {
-          const double2 x = A[(size_t)i * cols + p], y = A[(size_t)i * cols + q];
-          const double2 phc = cconj(ph);
-          A[(size_t)i * cols + p] = csub(cscale(x, c), cscale(cmul(phc, y), s));
-          A[(size_t)i * cols + q] = cadd(cscale(cmul(ph, x), s), cscale(y, c));
+          const double2 x = ap[i], y = aq[i];
+          ap[i] = csub(cscale(x, c), cscale(cmul(phc, y), s));
+          aq[i] = cadd(cscale(cmul(ph, x), s), cscale(y, c));
         }
+        double2* vp = Vt + (size_t)p * cols;
+        double2* vq = Vt + (size_t)q * cols;
         for (int i = lane; i < cols; i += 32) {
-          const double2 x = Vm[(size_t)i * cols + p], y = Vm[(size_t)i * cols + q];
-          const double2 phc = cconj(ph);
-          Vm[(size_t)i * cols + p] = csub(cscale(x, c), cscale(cmul(phc, y), s));
-          Vm[(size_t)i * cols + q] = cadd(cscale(cmul(ph, x), s), cscale(y, c));
+          const double2 x = vp[i], y = vq[i];
+          vp[i] = csub(cscale(x, c), cscale(cmul(phc, y), s));
+          vq[i] = cadd(cscale(cmul(ph, x), s), cscale(y, c));
         }
       }
       __syncthreads();
@@ -654,7 +666,7 @@ __global__ void __launch_bounds__(1024) k_jacobi_svd(int rows, int cols, double2
   // singular values and sort (descending, stable), U = A V columns normalized
   for (int j = warp; j < cols; j += nw) {
     double s2 = 0.0;
-    for (int i = lane; i < rows; i += 32) s2 += cabs2(A[(size_t)i * cols + j]);
+    for (int i = lane; i < rows; i += 32) s2 += cabs2(At[(size_t)j * rows + i]);
     s2 = warp_sum(s2);
     if (lane == 0) sigma[j] = sqrt(s2);
   }
@@ -672,17 +684,20 @@ __global__ void __launch_bounds__(1024) k_jacobi_svd(int rows, int cols, double2
     }
   }
   __syncthreads();
+  // U (row-major) into A, then back into Uout (which held At)
   for (int e = tid; e < rows * cols; e += blockDim.x) {
     const int i = e / cols, j = e % cols;
     const int src = order[j];
     const double sv = sigma[src];
-    const double2 a = A[(size_t)i * cols + src];
-    Uout[(size_t)i * cols + j] = sv > 0.0 ? cscale(a, 1.0 / sv) : make_double2(0.0, 0.0);
+    const double2 a = At[(size_t)src * rows + i];
+    A[e] = sv > 0.0 ? cscale(a, 1.0 / sv) : make_double2(0.0, 0.0);
   }
   for (int e = tid; e < cols * cols; e += blockDim.x) {
     const int i = e / cols, j = e % cols;
-    Vout[(size_t)i * cols + j] = Vm[(size_t)i * cols + order[j]];
+    Vout[(size_t)i * cols + j] = Vt[(size_t)order[j] * cols + i];
   }
+  __syncthreads();
+  for (int e = tid; e < rows * cols; e += blockDim.x) Uout[e] = A[e];
 }
 
 // sigma_sorted[j] = sigma[order[j]]

@@ -128,6 +128,30 @@ def test_build_pencil_svd_vs_oracle(pb, orc, d, n, m, noise):
         assert rel(S[l], S_or[l]) <= 1e-10
 
 
+@pytest.mark.parametrize("d,n,m", [(1, 3, 2), (1, 5, 3), (2, 1, 2), (1, 40, 7)])
+def test_build_pencil_tiny_and_square(pb, orc, d, n, m):
+    """Degenerate shapes of the Householder QR (k_house_qr): r0 = 2m = N (a square block, K = N reflectors) and
+    a one-CTA launch (N < 32 rows per CTA); sigma and the subspaces against the oracle's dense Jacobi SVD."""
+    cfg = W.custom_config(d, n, m, 0.0, 700 + d + n + m)
+    prob = W.make_problem(cfg, with_svd=False)
+    out = pb.build_pencil(dev(prob.grid), d, n, m, seed=2)
+    assert out["status"] == pb.PRONY_OK and out["rank"] == m, (out["status"], out["rank"])
+    U_j, V_j, s_j, _ = orc.svd_reduced(orc.T_dense(prob.grid, d, n, 0), rank=m)
+    s = out["sigma"].cpu().numpy()
+    assert np.max(np.abs(s - s_j) / s_j[0]) <= 1e-12
+    assert np.linalg.norm(proj(out["U"].cpu().numpy()) - proj(U_j)) <= 1e-9
+    assert np.linalg.norm(proj(out["V"].cpu().numpy()) - proj(V_j)) <= 1e-9
+
+
+def test_build_pencil_zero_signal_reports_rank(pb):
+    """T = 0: every Householder column norm is 0 (H = I, no division), the pivoted QR of Vbar_1 finds rank 0 and
+    prony_build_pencil returns PRONY_ERR_RANK without touching S (no NaN from the empty spectrum)."""
+    d, n, m = 2, 6, 3
+    grid = torch.zeros((2 * n + 2) ** d, dtype=torch.complex128, device="cuda")
+    out = pb.build_pencil(grid, d, n, m, seed=1, check=False)
+    assert out["status"] == pb.PRONY_ERR_RANK and out["rank"] == 0
+
+
 @pytest.mark.parametrize("d,m,rank", [(2, 5, 5), (2, 10, 10), (2, 15, 14), (2, 20, 17), (3, 15, 15), (3, 20, 20)])
 def test_block_power_paper_family_rank(pb, orc, d, m, rank):
     """The pivoted Householder QR of Alg. 3's first iteration with tol = N eps_M on the paper's
