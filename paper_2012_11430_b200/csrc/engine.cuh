@@ -6,8 +6,19 @@
 #include <stdint.h>
 
 #include <type_traits>
+#include <utility>
 
 namespace prony {
+
+// compile-time loop: f(std::integral_constant<int, 0>{}) ... f(std::integral_constant<int, N - 1>{})
+template <typename F, int... J>
+__device__ __forceinline__ void static_for_impl(F& f, std::integer_sequence<int, J...>) {
+  (f(std::integral_constant<int, J>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
 
 // ---------------------------------------------------------------------------- warp engine
 // non-volatile so ptxas may interleave independent MMAs
@@ -143,6 +154,15 @@ __device__ __forceinline__ void cp_async16(uint32_t sdst, const void* gsrc, int 
 }
 __device__ __forceinline__ void cp_async8(uint32_t sdst, const void* gsrc, int src_bytes) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(src_bytes));
+}
+// the same with a compile-time byte offset folded into the shared address (an immediate of the LDGSTS)
+template <int OFF>
+__device__ __forceinline__ void cp_async16_at(uint32_t sdst, const void* gsrc, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0+%3], [%1], 16, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(src_bytes), "n"(OFF));
+}
+template <int OFF>
+__device__ __forceinline__ void cp_async8_at(uint32_t sdst, const void* gsrc, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0+%3], [%1], 8, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(src_bytes), "n"(OFF));
 }
 __device__ __forceinline__ void cp_async16_cg(uint32_t sdst, const void* gsrc, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(src_bytes));

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
+#include <utility>
 
 #include "common.cuh"
 #include "engine.cuh"
@@ -170,16 +171,12 @@ constexpr int kGatherThreads = 96;  // producer threads doing the A gather (warp
 #ifndef PRONY_KK_UNROLL
 #define PRONY_KK_UNROLL 4
 #endif
-#ifndef PRONY_GATHER_UNROLL
-#define PRONY_GATHER_UNROLL 2
-#endif
 #ifndef PRONY_PROJ_SREG
 #define PRONY_PROJ_SREG 0
 #endif
 // SREG: the 3M sum operands formed in the consumers' registers (no gsum / Vsum planes gathered or copied)
 constexpr bool kProjSreg = PRONY_PROJ_SREG != 0;
 constexpr int kKkUnroll = PRONY_KK_UNROLL;
-constexpr int kGatherUnroll = PRONY_GATHER_UNROLL;
 constexpr int kConsumerRegs = PRONY_CONSUMER_REGS;  // 384 x 160 + 128 x 32 = 65536 (12 warps); 256 x 240 + 4096 (8)
 constexpr int kProducerRegs = PRONY_PRODUCER_REGS;
 // setmaxnreg only redistributes the CTA's launch-time register pool (kThreads x the per-thread count
@@ -205,6 +202,14 @@ struct ProjTile {
   static constexpr int PAT = BAR + 2 * kStages;      // row table P(k_r) + s_l + C0 (BM ints)
   static constexpr size_t SMEM = (size_t)PAT * sizeof(double) + (size_t)(BM + 4) * sizeof(int);
   static_assert(STAGE % 2 == 0, "stage must keep 16-byte alignment");
+  // A-gather threads of the producer warpgroup: warps 0-2 (warp 3 issues the B bulk copies). ROWOWNER: BM divides
+  // them (BM = 96, 48: the m <= 80 shapes), so every gather thread owns whole rows of the tile. For BM = 64 (m > 80)
+  // the element-strided gather is kept: the row-owner forms measured slower there (64 owners: 29.0 ms, all 128
+  // producer threads with warp 3 also gathering: 29.4 ms, vs 28.5 ms at cfg4) — that producer already runs ahead
+  // of the DMMA-bound consumers, and the variants changed the consumers' register allocation (spills in the loop)
+  static constexpr bool ROWOWNER = 96 % BM == 0 && kBK % (96 / BM) == 0;
+  static constexpr int GT = 96;
+  static_assert(!ROWOWNER || (GT % BM == 0 && kBK % (GT / BM) == 0), "gather threads must own whole tile rows");
 };
 
 template <int NT, int WN, int MODE>
@@ -236,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
     sPA[r] = (rb0 + r < rows) ? p.rtab[p.kb[l] + rb0 + r] + p.shift[l] : -1;  // -1: row outside
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full0 + 8u * s, kGatherThreads + 1);  // A-gather cp.async arrivals + B expect_tx
+      mbar_init(full0 + 8u * s, T::GT + 1);  // A-gather cp.async arrivals + B expect_tx
       mbar_init(empty0 + 8u * s, kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -249,11 +254,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
     const int pt = tid - kConsumerWarps * 32;  // 0..127
     const int plane = pt & 31;
     const int32_t* __restrict__ ptab = p.ptab;
-    if (pt < kGatherThreads) {
-      // A gather over the kBK x BM tile: element e = pt + kGatherThreads * j -> (kc = e / BM, ra = e % BM);
-      // P(k_ra) + shift comes from the shared row table sPA, P(h0 + kc) from lane kc (shfl)
+    if constexpr (T::ROWOWNER) {
+      // A gather, row-owner form (BM = 96, 48): gather thread pt < GT owns row ra = pt % BM of the tile for the whole CTA (its
+      // P(k_ra) + shift read once from the row table) and columns kc0, kc0 + TPR, ... of every stage; P(h0 + kc)
+      // comes from lane kc (shfl). Per element: one shfl, one subtraction, the two cp.async (immediate smem
+      // offsets). (The round-1/2 form decomposed e = pt + 96 j into (kc, ra) and re-read the row table per
+      // element, ~30 instructions per element: at m = 30 its consumers waited on the full barrier 7.8% of
+      // their samples.) Warp 3 first issues the stage's B rows: one bulk copy per V row (lanes 0..15) and per
+      // Vsum row (lanes 16..31), completing on the same full barrier (expect_tx).
       const double2* __restrict__ grid = p.grid;
       const double* __restrict__ gsum = p.gsum;
+      const double2* __restrict__ V = p.V;
+      const double* __restrict__ vsum = p.vsum;
+      constexpr int TPR = T::GT / BM, KPT = kBK / TPR;
+      const bool gather = pt < T::GT, bwarp = pt >= 96;
+      const int ra = pt % BM, kc0 = (pt / BM) % TPR;
+      const int pa = sPA[ra];
+      const uint32_t dA = (uint32_t)(T::A_C + 2 * (kc0 * T::LDA + ra)) * 8u;
+      const uint32_t dS = (uint32_t)(T::A_S + kc0 * T::LDAS + ra) * 8u;
+      const int kr = plane & (kBK - 1);
+      const bool sum_plane = plane >= kBK;
+      const uint32_t bytes_row = (uint32_t)m * 16u + (MODE == 3 && !kProjSreg ? (uint32_t)NP * 8u : 0u);
       // lane i < kBK holds P(h0 + i) of the stage being issued (prefetched one stage ahead)
       int ph_next = (plane < kBK && h_begin + plane < N) ? __ldg(ptab + h_begin + plane) : 0;
       for (int kt = 0; kt < KT; ++kt) {
@@ -264,44 +285,94 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
         ph_next = (plane < kBK && hn < N) ? __ldg(ptab + hn) : 0;
         if (kt >= kStages) mbar_wait(empty0 + 8u * s, (uint32_t)((kt / kStages) - 1) & 1u);
         const uint32_t st = sbase + (uint32_t)(s * T::STAGE) * 8u;
-#pragma unroll kGatherUnroll
-        for (int e = pt; e < kBK * BM; e += kGatherThreads) {
-          const int kc = e / BM, ra = e % BM;
-          const int phc = __shfl_sync(0xffffffffu, ph, kc);
-          const int pa = sPA[ra];
-          const bool ok = (pa >= 0) && (h0 + kc < h_end);
-          int idx = ok ? pa - phc : 0;
-          PRONY_CHECK_INDEX(idx, 0, p.box);
-          cp_async16(st + (uint32_t)(T::A_C + 2 * (kc * T::LDA + ra)) * 8u, grid + idx, ok ? 16 : 0);
-          if constexpr (MODE == 3 && !kProjSreg)
-            cp_async8(st + (uint32_t)(T::A_S + kc * T::LDAS + ra) * 8u, gsum + idx, ok ? 8 : 0);
+        if (bwarp) {
+          const int nrows = min(kBK, h_end - h0);
+          if (plane == 0) mbar_arrive_expect_tx(full0 + 8u * s, bytes_row * (uint32_t)nrows);
+          __syncwarp();
+          if (plane < 2 * kBK && kr < nrows) {
+            const int h = h0 + kr;
+            if (!sum_plane) {
+              bulk_g2s(st + (uint32_t)(T::B_C + 2 * kr * T::LDB) * 8u, V + (size_t)h * p.ldv, (uint32_t)m * 16u,
+                       full0 + 8u * s);
+            } else if constexpr (MODE == 3 && !kProjSreg) {
+              bulk_g2s(st + (uint32_t)(T::B_S + kr * T::LDBS) * 8u, vsum + (size_t)h * NP, (uint32_t)NP * 8u,
+                       full0 + 8u * s);
+            }
+          }
         }
-        mbar_arrive_cp_async(full0 + 8u * s);
+        if (gather) {
+          const uint32_t stA = st + dA, stS = st + dS;
+          const int kcut = pa >= 0 ? h_end - h0 : 0;  // columns kc < kcut hold data (zero-filled otherwise)
+          auto elem = [&](auto j_c) {
+            constexpr int j = decltype(j_c)::value;
+            const int kc = kc0 + TPR * j;
+            const int phc = __shfl_sync(0xffffffffu, ph, kc);
+            const bool ok = kc < kcut;
+            int idx = ok ? pa - phc : 0;
+            PRONY_CHECK_INDEX(idx, 0, p.box);
+            cp_async16_at<TPR * j * T::LDA * 16>(stA, grid + idx, ok ? 16 : 0);
+            if constexpr (MODE == 3 && !kProjSreg) cp_async8_at<TPR * j * T::LDAS * 8>(stS, gsum + idx, ok ? 8 : 0);
+          };
+          static_for<KPT>(elem);
+          mbar_arrive_cp_async(full0 + 8u * s);
+        }
       }
-      cp_async_wait<0>();
+      if (gather) cp_async_wait<0>();
     } else {
-      // B rows: one bulk copy per V row (lanes 0..15) and per Vsum row (lanes 16..31)
-      const int kr = plane & (kBK - 1);
-      const bool sum_plane = plane >= kBK;
-      const double2* __restrict__ V = p.V;
-      const double* __restrict__ vsum = p.vsum;
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % kStages;
-        const int h0 = h_begin + kt * kBK;
-        if (kt >= kStages) mbar_wait(empty0 + 8u * s, (uint32_t)((kt / kStages) - 1) & 1u);
-        const int nrows = min(kBK, h_end - h0);
-        const uint32_t bytes_row = (uint32_t)m * 16u + (MODE == 3 && !kProjSreg ? (uint32_t)NP * 8u : 0u);
-        if (plane == 0) mbar_arrive_expect_tx(full0 + 8u * s, bytes_row * (uint32_t)nrows);
-        __syncwarp();
-        const uint32_t st = sbase + (uint32_t)(s * T::STAGE) * 8u;
-        if (plane < 2 * kBK && kr < nrows) {
-          const int h = h0 + kr;
-          if (!sum_plane) {
-            bulk_g2s(st + (uint32_t)(T::B_C + 2 * kr * T::LDB) * 8u, V + (size_t)h * p.ldv, (uint32_t)m * 16u,
-                     full0 + 8u * s);
-          } else if constexpr (MODE == 3 && !kProjSreg) {
-            bulk_g2s(st + (uint32_t)(T::B_S + kr * T::LDBS) * 8u, vsum + (size_t)h * NP, (uint32_t)NP * 8u,
-                     full0 + 8u * s);
+      if (pt < kGatherThreads) {
+        // element-strided A gather over the kBK x BM tile: element e = pt + kGatherThreads * j -> (kc = e / BM,
+        // ra = e % BM); P(k_ra) + shift from the shared row table sPA, P(h0 + kc) from lane kc (shfl)
+        const double2* __restrict__ grid = p.grid;
+        const double* __restrict__ gsum = p.gsum;
+        // lane i < kBK holds P(h0 + i) of the stage being issued (prefetched one stage ahead)
+        int ph_next = (plane < kBK && h_begin + plane < N) ? __ldg(ptab + h_begin + plane) : 0;
+        for (int kt = 0; kt < KT; ++kt) {
+          const int s = kt % kStages;
+          const int h0 = h_begin + kt * kBK;
+          const int ph = ph_next;
+          const int hn = h0 + kBK + plane;
+          ph_next = (plane < kBK && hn < N) ? __ldg(ptab + hn) : 0;
+          if (kt >= kStages) mbar_wait(empty0 + 8u * s, (uint32_t)((kt / kStages) - 1) & 1u);
+          const uint32_t st = sbase + (uint32_t)(s * T::STAGE) * 8u;
+#pragma unroll 2
+          for (int e = pt; e < kBK * BM; e += kGatherThreads) {
+            const int kc = e / BM, ra = e % BM;
+            const int phc = __shfl_sync(0xffffffffu, ph, kc);
+            const int pa = sPA[ra];
+            const bool ok = (pa >= 0) && (h0 + kc < h_end);
+            int idx = ok ? pa - phc : 0;
+            PRONY_CHECK_INDEX(idx, 0, p.box);
+            cp_async16(st + (uint32_t)(T::A_C + 2 * (kc * T::LDA + ra)) * 8u, grid + idx, ok ? 16 : 0);
+            if constexpr (MODE == 3 && !kProjSreg)
+              cp_async8(st + (uint32_t)(T::A_S + kc * T::LDAS + ra) * 8u, gsum + idx, ok ? 8 : 0);
+          }
+          mbar_arrive_cp_async(full0 + 8u * s);
+        }
+        cp_async_wait<0>();
+      } else {
+        // B rows: one bulk copy per V row (lanes 0..15) and per Vsum row (lanes 16..31)
+        const int kr = plane & (kBK - 1);
+        const bool sum_plane = plane >= kBK;
+        const double2* __restrict__ V = p.V;
+        const double* __restrict__ vsum = p.vsum;
+        for (int kt = 0; kt < KT; ++kt) {
+          const int s = kt % kStages;
+          const int h0 = h_begin + kt * kBK;
+          if (kt >= kStages) mbar_wait(empty0 + 8u * s, (uint32_t)((kt / kStages) - 1) & 1u);
+          const int nrows = min(kBK, h_end - h0);
+          const uint32_t bytes_row = (uint32_t)m * 16u + (MODE == 3 && !kProjSreg ? (uint32_t)NP * 8u : 0u);
+          if (plane == 0) mbar_arrive_expect_tx(full0 + 8u * s, bytes_row * (uint32_t)nrows);
+          __syncwarp();
+          const uint32_t st = sbase + (uint32_t)(s * T::STAGE) * 8u;
+          if (plane < 2 * kBK && kr < nrows) {
+            const int h = h0 + kr;
+            if (!sum_plane) {
+              bulk_g2s(st + (uint32_t)(T::B_C + 2 * kr * T::LDB) * 8u, V + (size_t)h * p.ldv, (uint32_t)m * 16u,
+                       full0 + 8u * s);
+            } else if constexpr (MODE == 3 && !kProjSreg) {
+              bulk_g2s(st + (uint32_t)(T::B_S + kr * T::LDBS) * 8u, vsum + (size_t)h * NP, (uint32_t)NP * 8u,
+                       full0 + 8u * s);
+            }
           }
         }
       }
