@@ -263,7 +263,17 @@ def run_ours(args, cfg):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    if world > 1:
+    # --force-dist: the N > 1 code path (process group, collectives, per-rank gather) on a one-rank group
+    dist_on = world > 1 or args.force_dist
+    if dist_on:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if "MASTER_PORT" not in os.environ:
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:  # gloo: functional check of the N>1 path with several ranks on one GPU (no waiting kernels)
@@ -276,7 +286,7 @@ def run_ours(args, cfg):
     tg = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     grid, U, V, sigma, z = tg(prob.grid), tg(prob.U), tg(prob.V), tg(prob.sigma), tg(prob.z)
     order_arg = {"l-major": 0, "row-major": 1, "shared": 2}[args.units]
-    pencil = sharding.DistributedPencil(d, n, m, dev, world, rank, unit_order=order_arg)
+    pencil = sharding.DistributedPencil(d, n, m, dev, world, rank, unit_order=order_arg, collective=dist_on)
     order = pencil.order
     st = pencil.status
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -303,17 +313,17 @@ def run_ours(args, cfg):
 
     clocks = ClockSampler(local)
     clocks.start()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     for i in range(K):
         flush.fill_(i & 0xFF)                  # L2 flush outside the timed interval
         ev_s[i].record(stream)
         pencil(grid, U, V, sigma, z, stream=stream, ev_project=(ev_ps[i], ev_pe[i]), ev_ls=(ev_ls[i], ev_le[i]),
-               ev_comm=(ev_cs[i], ev_ce[i]) if world > 1 else None)
+               ev_comm=(ev_cs[i], ev_ce[i]) if dist_on else None)
         ev_e[i].record(stream)
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     clk = clocks.stop()
     assert int(st.item()) == 0, f"device status {int(st.item())}"
@@ -321,10 +331,10 @@ def run_ours(args, cfg):
     step_ms = [ev_s[i].elapsed_time(ev_e[i]) for i in range(K)]
     proj_ms = [ev_ps[i].elapsed_time(ev_pe[i]) for i in range(K)]
     vls_ms = [ev_ls[i].elapsed_time(ev_le[i]) for i in range(K)]
-    comm_ms = [ev_cs[i].elapsed_time(ev_ce[i]) for i in range(K)] if world > 1 else [0.0] * K
+    comm_ms = [ev_cs[i].elapsed_time(ev_ce[i]) for i in range(K)] if dist_on else [0.0] * K
     mine = torch.tensor([sum(step_ms), statistics.mean(proj_ms), statistics.mean(vls_ms), statistics.mean(comm_ms),
                          statistics.mean(step_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist_on:
         allr = [torch.empty_like(mine) for _ in range(world)]
         dist.all_gather(allr, mine)
         per_rank = [x.tolist() for x in allr]
@@ -339,7 +349,7 @@ def run_ours(args, cfg):
     h2d_full = sum(x.numel() * x.element_size() for x in (hg, hU, hV, hs, hz))
     Ke = max(2, min(K, 5))
     e_ms = []
-    if world == 1:
+    if not dist_on:
         outs = {k: torch.empty(s, dtype=dt).pin_memory() for k, s, dt in
                 [("S", (d, m, m), torch.complex128), ("G", (m, m), torch.complex128), ("b", (m,), torch.complex128),
                  ("c", (m,), torch.complex128), ("t", (m, d), torch.float64)]}
@@ -394,7 +404,7 @@ def run_ours(args, cfg):
         api = ("sharding.DistributedPencil.from_host (per rank: pinned H2D of the grid, its 1/N slice of V and its "
                "U rows; all_gather of V over the device interconnect; pencil; all-reduce; D2H of S, c, t on rank 0)")
     te = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist_on:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = {"value": Ke / (float(te[0]) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": sum(h2d_rank),
            "h2d_bytes_per_rank": h2d_rank, "d2h_bytes_per_step": d2h, "ms_per_step": float(te[0]) / Ke, "api": api}
@@ -435,8 +445,8 @@ def run_ours(args, cfg):
                        "d": d, "n": n, "N": N, "m": m, "parallelism": f"dp{world} ({['l-major', 'row-major', 'shared'][order]} units)",
                        "l2": "flushed (256 MiB write) before every timed step, outside the timed interval",
                        "pencils_per_step": 1,
-                       "comm": "1 x all_reduce(SUM) of packed [S,G,b] per step" if world > 1 else "none",
-                       "dist_backend": args.dist_backend if world > 1 else None},
+                       "comm": "1 x all_reduce(SUM) of packed [S,G,b] per step" if dist_on else "none",
+                       "dist_backend": args.dist_backend if dist_on else None},
             # physical rates: real FP64 flops the implementation executes per pencil (3M products) / time
             "tflops": tflops,
             "pct_peak": tflops / (peak * world) if peak else None,
@@ -472,7 +482,7 @@ def run_ours(args, cfg):
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(prob)
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.barrier()
         dist.destroy_process_group()
 
@@ -511,6 +521,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--force-dist", action="store_true",
+                    help="test hook: run the N > 1 path (process group + collectives) even with one rank")
     ap.add_argument("--units", default="shared", choices=["shared", "l-major", "row-major"],
                     help="prony_unit_order of the projection (shared: one extended product for all l, F8)")
     args = ap.parse_args()

@@ -120,14 +120,15 @@ def h2d_bytes(d: int, n: int, m: int, world: int, rank: int, order: int = UNITS_
     return ((2 * n + 2) ** d + (vrows + (uhi - ulo)) * m + m * d) * 16 + m * 8
 
 
-def allgather_rows(buf: torch.Tensor, world: int, rank: int, mine: torch.Tensor | None = None) -> None:
+def allgather_rows(buf: torch.Tensor, world: int, rank: int, mine: torch.Tensor | None = None,
+                   collective: bool | None = None) -> None:
     """buf: (chunk * world, ...); this rank's rows are in `mine` (chunk, ...) — or already at
     [rank * chunk, (rank + 1) * chunk) of buf when mine is None. Afterwards every rank holds all of them
-    in buf (one all_gather, out of place from `mine`)."""
+    in buf (one all_gather, out of place from `mine`). collective=False (default at world 1): a local copy."""
     chunk = buf.shape[0] // world
     if mine is None:
         mine = buf[rank * chunk:(rank + 1) * chunk].clone()
-    if world == 1:
+    if not (world > 1 if collective is None else collective):
         buf.copy_(mine)
         return
     real = (lambda x: torch.view_as_real(x)) if buf.is_complex() else (lambda x: x)
@@ -147,12 +148,16 @@ class DistributedPencil:
     `stream` (default: the current stream): the projection, the packing, the collective and the solve
     are all ordered on it; the LS products run on a side stream that joins it before the collective."""
 
-    def __init__(self, d: int, n: int, m: int, device, world: int = 1, rank: int = 0, unit_order: int | None = None):
+    def __init__(self, d: int, n: int, m: int, device, world: int = 1, rank: int = 0, unit_order: int | None = None,
+                 collective: bool | None = None):
+        """collective: run the partial path with its collectives (default: world > 1). collective=True at
+        world 1 drives the N > 1 code path, NCCL calls included, on a one-rank process group (tested)."""
         from . import binding as pb
         self.pb = pb
         self.d, self.n, self.m = d, n, m
         self.N = (n + 1) ** d
         self.world, self.rank = world, rank
+        self.collective = world > 1 if collective is None else collective
         self.device = torch.device(device)
         self.order = default_unit_order(d, world) if unit_order is None else unit_order
         self.u0, self.u1 = unit_range(d, n, world, rank, self.order)
@@ -191,7 +196,7 @@ class DistributedPencil:
         projection stream's k_reduce_ws, k_finalize and all-reduce of S."""
         pb, d, n, m = self.pb, self.d, self.n, self.m
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
-        full = self.world == 1
+        full = not self.collective
         pe = ev_project if ev_project is not None else (None, self.ev_proj)
         info_p = pb.make_exec_info(pe[0], pe[1])
         info_l = pb.make_exec_info(*ev_ls) if ev_ls is not None else pb.make_exec_info()
@@ -246,7 +251,7 @@ class DistributedPencil:
         self.last_split_k = info_p.split_k
 
     def _allreduce(self, x):
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        if self.collective and dist.is_available() and dist.is_initialized():
             dist.all_reduce(torch.view_as_real(x), op=dist.ReduceOp.SUM)
 
     def _reduce_and_solve(self, z, st, ev_comm=None):
@@ -292,7 +297,7 @@ class DistributedPencil:
                 if not hasattr(self, "ws_h"):
                     self.ws_h = pb.alloc_workspace(pb.WS_PENCIL_HOST, d, n, m, dev)
                     self.hctx = pb.HostContext()
-                if self.world == 1:
+                if not self.collective:
                     raise ValueError("scatter_v=False is the N > 1 partial path")
                 self.status.zero_()
                 pb.pencil_host_part(grid_h, U_h, V_h, sigma_h, z_h, d, n, m, self.u0, self.u1, self.c0, self.c1,
@@ -306,6 +311,6 @@ class DistributedPencil:
                 self.dU[ulo:uhi].copy_(U_h[ulo:uhi], non_blocking=True)
             if v1 > v0:
                 self.dVmine[:v1 - v0].copy_(V_h[v0:v1], non_blocking=True)
-            allgather_rows(self.dVpad, self.world, self.rank, self.dVmine)
+            allgather_rows(self.dVpad, self.world, self.rank, self.dVmine, collective=self.collective)
             V = self.dVpad[:self.N]
         return self(self.dgrid, self.dU, V, self.dsig, self.dz, stream=main, ev_comm=ev_comm)

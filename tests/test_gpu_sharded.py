@@ -27,7 +27,7 @@ def _free_port():
     return p
 
 
-def _rank(rank, world, port, name, out, mode):
+def _rank(rank, world, port, name, out, mode, backend="gloo"):
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
 
@@ -35,13 +35,17 @@ def _rank(rank, world, port, name, out, mode):
     from paper_2012_11430_b200 import sharding
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     prob = W.make_problem(name)
     c = prob.cfg
     tg = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-    pencil = sharding.DistributedPencil(c.d, c.n, c.m, torch.device("cuda", 0), world, rank)
+    # collective=True: the partial path with its collectives even on a one-rank NCCL group
+    pencil = sharding.DistributedPencil(c.d, c.n, c.m, torch.device("cuda", 0), world, rank, collective=True)
     side = torch.cuda.Stream()          # a non-current stream: the call must order everything on it
     if mode == "device":
         S, cc, t = pencil(tg(prob.grid), tg(prob.U), tg(prob.V), tg(prob.sigma), tg(prob.z), stream=side)
@@ -56,14 +60,10 @@ def _rank(rank, world, port, name, out, mode):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,mode", [("cfg2", "device"), ("cfg3", "device"), ("cfg2", "scatter"),
-                                       ("cfg3", "scatter"), ("cfg2", "full_v")])
-def test_distributed_pencil_two_ranks_vs_oracle(tmp_path, name, mode):
+def _check_vs_oracle(out, name):
     sys.path.insert(0, ROOT)
     import oracle
     import workload as W
-    out = str(tmp_path / "r.npz")
-    mp.spawn(_rank, args=(2, _free_port(), name, out, mode), nprocs=2, join=True)
     r = np.load(out)
     prob = W.make_problem(name)
     c = prob.cfg
@@ -81,6 +81,25 @@ def test_distributed_pencil_two_ranks_vs_oracle(tmp_path, name, mode):
     assert W.torus_dist_inf(r["t"], prob.t).max() <= 1e-8
 
 
+@pytest.mark.parametrize("name,mode", [("cfg2", "device"), ("cfg3", "device"), ("cfg2", "scatter"),
+                                       ("cfg3", "scatter"), ("cfg2", "full_v")])
+def test_distributed_pencil_two_ranks_vs_oracle(tmp_path, name, mode):
+    out = str(tmp_path / "r.npz")
+    mp.spawn(_rank, args=(2, _free_port(), name, out, mode), nprocs=2, join=True)
+    _check_vs_oracle(out, name)
+
+
+@pytest.mark.parametrize("name,mode", [("cfg2", "device"), ("cfg2", "scatter"), ("cfg2", "full_v"),
+                                       ("cfg3", "device")])
+def test_distributed_pencil_nccl_one_rank_vs_oracle(tmp_path, name, mode):
+    """The N > 1 code path over REAL NCCL (one rank: NCCL refuses two ranks on one GPU): the partial
+    projection, the all_reduce of [G, b] on the LS side stream after k_project's end event, the all_reduce
+    of S, the V all_gather of the scatter path and prony_pencil_host_part, against the oracle."""
+    out = str(tmp_path / "r.npz")
+    mp.spawn(_rank, args=(1, _free_port(), name, out, mode, "nccl"), nprocs=1, join=True)
+    _check_vs_oracle(out, name)
+
+
 def test_bench_launcher_two_ranks_gloo():
     """`python bench.py --gpus 2` starts its own 2 ranks (torchrun re-exec) exactly as the driver's N = 1 form
     runs; over gloo two ranks can share this environment's one GPU. One JSON line with n_gpus = 2."""
@@ -95,3 +114,19 @@ def test_bench_launcher_two_ranks_gloo():
     assert j["n_gpus"] == 2 and j["value"] > 0 and len(j["per_rank"]) == 2
     assert j["pct_peak"] <= 1.0 and j["roofline"]["frac"] <= 1.0
     assert len(j["e2e"]["h2d_bytes_per_rank"]) == 2 and j["e2e"]["value"] > 0
+
+
+def test_bench_force_dist_nccl_one_rank():
+    """`bench.py --force-dist` at --gpus 1: the bench's N > 1 branch (NCCL process group, the two all_reduces
+    with their comm events, the per-rank all_gather of times, the V-scatter e2e through from_host) over real
+    NCCL on this environment's one GPU."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--force-dist", "--cfg", "cfg2",
+           "--steps", "3", "--warmup", "3", "--no-cpu-baseline"]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_PORT")}
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 1 and j["value"] > 0 and j["config"]["dist_backend"] == "nccl"
+    assert j["per_rank"][0]["allreduce_ms"] > 0 and j["e2e"]["value"] > 0
