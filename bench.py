@@ -472,7 +472,10 @@ def run_ours(args, cfg):
                          "share_of_step": sum(proj_ms) / sum(step_ms),
                          "grid": pencil.last_grid, "split_k": pencil.last_split_k},
             "kernels_ms": {"k_project": statistics.mean(proj_ms), "k_vls": statistics.mean(vls_ms),
-                           "outside_k_project": statistics.mean(step_ms) - statistics.mean(proj_ms)},
+                           "outside_k_project": statistics.mean(step_ms) - statistics.mean(proj_ms),
+                           "note": "k_vls = the event interval around k_vls on the LS side stream, released right "
+                                   "before k_project: its CTAs wait for the SMs k_project's last wave leaves idle, "
+                                   "so the interval spans that wait (its own run time is ~0.13 ms at cfg4)"},
             "per_rank": [{"rank": r, "step_ms": x[4], "k_project_ms": x[1], "k_vls_ms": x[2], "allreduce_ms": x[3]}
                          for r, x in enumerate(per_rank)],
             "gpu_launches": launches_per_step * K,

@@ -532,11 +532,13 @@ int prony_pencil(prony_host_context ctx, int d, int n, int m, const prony_c128* 
   ProjPlan pl{};
   project_plan(g, sms, &pl);
   char* w = (char*)workspace;
-  rc = (cudaEventRecord(ev_in, st) == cudaSuccess && cudaStreamWaitEvent(side, ev_in, 0) == cudaSuccess)
-           ? PRONY_OK : PRONY_ERR_CUDA;
-  if (rc == PRONY_OK)
-    rc = project_launch(g, pl, (const double2*)grid, (const double2*)U, (const double2*)V, sigma, (double2*)S, w,
-                        sms, st, info_project, nullptr, 1, dev_status);
+  // the LS side stream starts once the prep kernels are done and k_project is enqueued (ev_in, recorded by
+  // project_launch): were it released at the call's start, back-to-back calls would let k_vls (one CTA per SM)
+  // take the SMs ahead of k_project's first wave (measured: k_project delayed 0.1 ms per pencil at cfg4); this
+  // way k_project is served first and the LS CTAs fill the SMs its last wave leaves idle
+  rc = project_launch(g, pl, (const double2*)grid, (const double2*)U, (const double2*)V, sigma, (double2*)S, w,
+                      sms, st, info_project, nullptr, 1, dev_status, nullptr, ev_in);
+  if (rc == PRONY_OK && cudaStreamWaitEvent(side, ev_in, 0) != cudaSuccess) rc = PRONY_ERR_CUDA;
   if (rc == PRONY_OK)
     rc = ls_launch(d, n, m, (int)N, (const double2*)z, (const double2*)grid, 0, N, nullptr, (double2*)G, (double2*)b,
                    (double2*)c, t, w + off_ls, dev_status, sms, side, info_ls);

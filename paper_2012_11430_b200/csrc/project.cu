@@ -1075,7 +1075,7 @@ static int launch_reduce_ws_t(const RedParams& r, dim3 rgrid, cudaStream_t st) {
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
                    const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
                    prony_exec_info* info, cudaEvent_t wait_before_reduce, int ell_base, int32_t* dev_status,
-                   const ProjSplit* sp) {
+                   const ProjSplit* sp, cudaEvent_t ev_prepped) {
   const WsLayout wl = ws_layout(g.d, g.n, g.N, g.m, sm_count);
   char* w = (char*)ws;
   int32_t* ptab = (int32_t*)(w + wl.ptab);
@@ -1098,6 +1098,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   }
   if (pl.R_tot == 0) {
     if (cudaMemsetAsync(S, 0, (size_t)g.d * g.m * g.m * sizeof(double2), st) != cudaSuccess) return PRONY_ERR_CUDA;
+    if (ev_prepped && cudaEventRecord(ev_prepped, st) != cudaSuccess) return PRONY_ERR_CUDA;
     return PRONY_OK;
   }
   int64_t box = 1;
@@ -1110,6 +1111,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   k_prep<<<8 * sm_count, 256, 0, st>>>(g.d, g.n, g.N, g.m, g.m, pl.shape.NP, box, grid, V, ptab, gsum, vsum,
                                        vrows0);
   if (g.shared) k_prep_ext<<<sm_count, 256, 0, st>>>(g.d, g.n, E, etab, umap);
+  if (ev_prepped && cudaEventRecord(ev_prepped, st) != cudaSuccess) return PRONY_ERR_CUDA;
 
   ProjParams p{};
   p.grid = grid;

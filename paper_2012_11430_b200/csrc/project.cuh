@@ -80,6 +80,9 @@ struct RedParams {
 // caller has made V rows [0, chunk_w) resident in stream order on `st` and enqueues the rest on
 // `s_rest` BEFORE calling project_launch; split-K chunk 0 then runs on `st` while chunks 1..KC-1 (and
 // their Vsum rows) run on `s_rest`; `ev_a` / `ev_b` are caller-owned scratch events.
+// ev_prepped (optional): recorded on `st` after the prep kernels, right before k_project is enqueued. A side
+// stream that waits on it (instead of on the call's start) cannot dispatch its CTAs ahead of k_project's:
+// the hardware then serves the earlier-enqueued k_project first and the side kernels fill its last wave.
 struct ProjSplit {
   cudaStream_t s_rest;
   cudaEvent_t ev_a, ev_b;
@@ -91,7 +94,8 @@ size_t project_workspace_bytes(int d, int n, int N, int m, int sm_count);
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
                    const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
                    prony_exec_info* info, cudaEvent_t wait_before_reduce = nullptr, int ell_base = 1,
-                   int32_t* dev_status = nullptr, const ProjSplit* split = nullptr);
+                   int32_t* dev_status = nullptr, const ProjSplit* split = nullptr,
+                   cudaEvent_t ev_prepped = nullptr);
 __global__ void k_combine_grid(int d, int n, int64_t box, const double2* grid, const double2* mu, double2* out);
 
 size_t apply_workspace_bytes(int d, int n, int N);

@@ -183,6 +183,10 @@ class DistributedPencil:
         # for it, so no rank's NCCL kernel occupies SMs (spinning on its peers) while projections still run
         self.ev_proj = torch.cuda.Event()
         self.ev_proj.record(torch.cuda.current_stream(self.device))  # materialize the handle
+        # recorded by the library right BEFORE k_project (after the prep kernels): the LS branch starts there, so
+        # in back-to-back calls its CTAs cannot take the SMs ahead of k_project's first wave
+        self.ev_pbeg = torch.cuda.Event()
+        self.ev_pbeg.record(torch.cuda.current_stream(self.device))
 
     def __call__(self, grid, U, V, sigma, z, stream=None, ev_project=None, ev_ls=None, ev_comm=None):
         """Device-resident inputs -> (S, c, t) (views of this object's buffers, valid until the next call).
@@ -197,7 +201,7 @@ class DistributedPencil:
         pb, d, n, m = self.pb, self.d, self.n, self.m
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
         full = not self.collective
-        pe = ev_project if ev_project is not None else (None, self.ev_proj)
+        pe = ev_project if ev_project is not None else (self.ev_pbeg, self.ev_proj)
         info_p = pb.make_exec_info(pe[0], pe[1])
         info_l = pb.make_exec_info(*ev_ls) if ev_ls is not None else pb.make_exec_info()
         if full and self.order == UNITS_SHARED:
@@ -220,6 +224,7 @@ class DistributedPencil:
                        dev_status=self.status, stream=hi, info=info_p)
         ev_proj_end = pe[1]  # recorded by the library right after k_project
         side.wait_event(self.ev_in)
+        side.wait_event(pe[0])  # recorded by the library right before k_project (stale only if it had no rows)
         with torch.cuda.stream(side):
             res = pb.vandermonde_ls(z, grid, d, n, m, self.c0, self.c1, want_solution=full,
                                     out={"G": self.G, "b": self.b, "c": self.c, "t": self.t}, workspace=self.ws_l,
