@@ -5,6 +5,8 @@
 #include <algorithm>
 #include <cstdint>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -357,7 +359,10 @@ void shared_u_rows(int d, int n, int64_t e0, int64_t e1, int64_t* lo, int64_t* h
 struct prony_host_context_s {
   int device = -1;
   cudaStream_t s2 = nullptr, s3 = nullptr, s4 = nullptr;
+  cudaStream_t sl[kSplitStreams] = {};     // launch streams of the later split-K chunk groups
   cudaEvent_t ev[8] = {};  // in, grid, v0, u, done, split a, split b, v rest
+  cudaEvent_t ev_chunk[kMaxChunkEv] = {};  // V rows of split-K chunk c >= 1 copied
+  cudaEvent_t ev_join[kSplitStreams] = {};
 };
 
 namespace {
@@ -368,7 +373,13 @@ void host_ctx_release(prony_host_context_s* c) {
       cudaEventDestroy(e);
       e = nullptr;
     }
-  for (cudaStream_t* s : {&c->s2, &c->s3, &c->s4})
+  for (cudaEvent_t* arr : {c->ev_chunk, c->ev_join})
+    for (int i = 0; i < (arr == c->ev_chunk ? kMaxChunkEv : kSplitStreams); ++i)
+      if (arr[i]) {
+        cudaEventDestroy(arr[i]);
+        arr[i] = nullptr;
+      }
+  for (cudaStream_t* s : {&c->s2, &c->s3, &c->s4, &c->sl[0], &c->sl[1], &c->sl[2]})
     if (*s) {
       cudaStreamDestroy(*s);
       *s = nullptr;
@@ -380,7 +391,12 @@ int host_ctx_init(prony_host_context_s* c) {
   bool good = cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) == cudaSuccess &&
               cudaStreamCreateWithFlags(&c->s3, cudaStreamNonBlocking) == cudaSuccess &&
               cudaStreamCreateWithFlags(&c->s4, cudaStreamNonBlocking) == cudaSuccess;
+  for (int i = 0; i < kSplitStreams && good; ++i)
+    good = cudaStreamCreateWithFlags(&c->sl[i], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming) == cudaSuccess;
   for (int i = 0; i < 8 && good; ++i) good = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming) == cudaSuccess;
+  for (int i = 0; i < kMaxChunkEv && good; ++i)
+    good = cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDisableTiming) == cudaSuccess;
   if (!good) {
     host_ctx_release(c);
     return PRONY_ERR_CUDA;
@@ -388,12 +404,34 @@ int host_ctx_init(prony_host_context_s* c) {
   return PRONY_OK;
 }
 
-// Host-input pencil on the device (prony_pencil_host / prony_pencil_host_part). `st` carries grid, the
-// V rows of split-K chunk 0 and sigma -> k_prep -> chunk 0 of the projection; `s2` carries the rest of V
-// (after chunk 0's rows: the link is not shared) -> its Vsum rows -> chunks 1..KC-1; `s4` carries the U rows
-// after the rest of V (needed only by k_reduce, so the chunks on s2 never wait for them); `s3` carries z ->
-// the LS step. So only chunk 0's V rows are copied before the first DMMA. On return `st` is ordered after
-// everything. The streams / events come from `ctx` (a caller's context) or are created for this call.
+// PRONY_HOST_TIMELINE=1 (diagnostic): timing events at the stages of host_pencil, printed to stderr by
+// prony_pencil_host_ctx after its synchronize (ms from the call's start on `st`)
+struct HostTimeline {
+  bool on = false;
+  cudaEvent_t e[10] = {};
+  const char* name[10] = {"grid+V0+sigma", "-", "proj0_begin", "proj0_end", "Vrest", "proj_reduced", "U", "LS_end",
+                          "end", "start"};
+};
+HostTimeline& host_timeline() {
+  static HostTimeline t = [] {
+    HostTimeline x;
+    const char* e = getenv("PRONY_HOST_TIMELINE");
+    x.on = e && atoi(e) > 0;
+    if (x.on)
+      for (auto& ev : x.e) cudaEventCreate(&ev);
+    return x;
+  }();
+  return t;
+}
+
+// Host-input pencil on the device (prony_pencil_host / prony_pencil_host_part). The link carries, in order:
+// on `st` the grid, the V rows of the narrow split-K chunk 0 (project_plan_lead) and sigma -> k_prep ->
+// chunk 0 of the projection; on the copy stream `s2` the V rows of chunk 1, 2, ... (an event after each);
+// on `s4` the U rows after all of V (first needed by k_reduce); `s3` carries z and, once the prep kernels are
+// done, the LS step. The later chunks of the projection run in groups on the context's launch streams, each
+// as soon as ITS rows are in, so only chunk 0's rows (about 1/24 of V) are copied before the first DMMA and
+// each later chunk's copy hides behind the chunks before it. On return `st` is ordered after everything. The streams / events come from `ctx` (a
+// caller's context) or are created for this call.
 int host_pencil(int d, int n, int m, int64_t N, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
                 const double* sigma, const prony_c128* z, int64_t e0, int64_t e1, int64_t c0, int64_t c1, bool solve,
                 double2* S_dev, double2* G_dev, double2* b_dev, double2* c_dev, double* t_dev, int32_t* dst,
@@ -408,8 +446,9 @@ int host_pencil(int d, int n, int m, int64_t N, const prony_c128* grid, const pr
   unit_rows(d, n, N, e0, e1, PRONY_UNITS_SHARED, &g);
   ProjPlan pl{};
   project_plan(g, sms, &pl);
+  project_plan_lead(g, &pl);  // a narrow chunk 0: only its V rows are copied before the first DMMA
   const bool split = pl.KC > 1;
-  const int64_t v0 = split ? std::min<int64_t>(pl.chunk_w, N) : N;
+  const int64_t v0 = split ? std::min<int64_t>(pl.chunk0_w, N) : N;
   int64_t ulo = 0, uhi = N;
   if (e0 != 0 || e1 != ext_rows(d, n)) shared_u_rows(d, n, e0, e1, &ulo, &uhi);
   prony_host_context_s local;
@@ -424,45 +463,59 @@ int host_pencil(int d, int n, int m, int64_t N, const prony_c128* grid, const pr
   }
   cudaStream_t s2 = ctx->s2, s3 = ctx->s3, s4 = ctx->s4;
   cudaEvent_t* ev = ctx->ev;
-  cudaEvent_t ev_in = ev[0], ev_grid = ev[1], ev_v0 = ev[2], ev_u = ev[3], ev_done = ev[4], ev_vrest = ev[7];
+  cudaEvent_t ev_prep = ev[0], ev_grid = ev[1], ev_v0 = ev[2], ev_u = ev[3], ev_done = ev[4], ev_vrest = ev[7];
   auto ok = [](cudaError_t e) { return e == cudaSuccess; };
   const size_t vrow = (size_t)m * sizeof(double2);
-  bool good = ok(cudaEventRecord(ev_in, st)) && ok(cudaStreamWaitEvent(s2, ev_in, 0)) &&
-              ok(cudaStreamWaitEvent(s3, ev_in, 0)) &&
-              ok(cudaMemcpyAsync(w + h.grid, grid, box * sizeof(double2), cudaMemcpyHostToDevice, st)) &&
+  HostTimeline& tl = host_timeline();
+  if (tl.on) cudaEventRecord(tl.e[9], st);
+  bool good = ok(cudaMemcpyAsync(w + h.grid, grid, box * sizeof(double2), cudaMemcpyHostToDevice, st)) &&
               ok(cudaEventRecord(ev_grid, st)) &&
               ok(cudaMemcpyAsync(w + h.V, V, v0 * vrow, cudaMemcpyHostToDevice, st)) &&
               ok(cudaMemcpyAsync(w + h.sigma, sigma, m * sizeof(double), cudaMemcpyHostToDevice, st)) &&
-              ok(cudaEventRecord(ev_v0, st)) && ok(cudaStreamWaitEvent(s2, ev_v0, 0)) &&
-              (v0 == N || ok(cudaMemcpyAsync(w + h.V + v0 * vrow, (const char*)V + v0 * vrow, (N - v0) * vrow,
-                                             cudaMemcpyHostToDevice, s2))) &&
-              ok(cudaEventRecord(ev_vrest, s2)) && ok(cudaStreamWaitEvent(s4, ev_vrest, 0)) &&
-              (uhi <= ulo || ok(cudaMemcpyAsync(w + h.U + ulo * vrow, (const char*)U + ulo * vrow,
-                                                (uhi - ulo) * vrow, cudaMemcpyHostToDevice, s4))) &&
-              ok(cudaEventRecord(ev_u, s4)) && ok(cudaStreamWaitEvent(s3, ev_grid, 0)) &&
-              ok(cudaMemcpyAsync(w + h.z, z, (size_t)m * d * sizeof(double2), cudaMemcpyHostToDevice, s3));
-  int rc = good ? PRONY_OK : PRONY_ERR_CUDA;
-  if (rc == PRONY_OK) {
-    ProjSplit sp{s2, ev[5], ev[6]};
-    rc = project_launch(g, pl, (const double2*)(w + h.grid), (const double2*)(w + h.U), (const double2*)(w + h.V),
-                        (const double*)(w + h.sigma), S_dev, w + h.inner, sms, st, nullptr, ev_u, 1, dst,
-                        split ? &sp : nullptr);
+              ok(cudaEventRecord(ev_v0, st)) && ok(cudaStreamWaitEvent(s2, ev_v0, 0));
+  for (int c = 1; good && split && c < pl.KC; ++c) {  // chunk c's V rows, then its event
+    const int64_t r0 = pl.chunk0_w + (int64_t)(c - 1) * pl.chunk_w, r1 = std::min<int64_t>(r0 + pl.chunk_w, N);
+    good = ok(cudaMemcpyAsync(w + h.V + r0 * vrow, (const char*)V + r0 * vrow, (r1 - r0) * vrow,
+                              cudaMemcpyHostToDevice, s2)) &&
+           ok(cudaEventRecord(ctx->ev_chunk[std::min(c - 1, kMaxChunkEv - 1)], s2));
   }
+  good = good && ok(cudaEventRecord(ev_vrest, s2)) && ok(cudaStreamWaitEvent(s4, ev_vrest, 0)) &&
+         (uhi <= ulo || ok(cudaMemcpyAsync(w + h.U + ulo * vrow, (const char*)U + ulo * vrow, (uhi - ulo) * vrow,
+                                           cudaMemcpyHostToDevice, s4))) &&
+         ok(cudaEventRecord(ev_u, s4)) && ok(cudaStreamWaitEvent(s3, ev_grid, 0)) &&
+         ok(cudaMemcpyAsync(w + h.z, z, (size_t)m * d * sizeof(double2), cudaMemcpyHostToDevice, s3));
+  int rc = good ? PRONY_OK : PRONY_ERR_CUDA;
+  prony_exec_info tinfo{};
+  if (tl.on) {
+    cudaEventRecord(tl.e[0], st);
+    cudaEventRecord(tl.e[4], s2);
+    cudaEventRecord(tl.e[6], s4);
+    tinfo.ev_main_begin = tl.e[2];
+    tinfo.ev_main_end = tl.e[3];
+  }
+  if (rc == PRONY_OK) {
+    ProjSplit sp{{ctx->sl[0], ctx->sl[1], ctx->sl[2]}, ev[5], {ctx->ev_join[0], ctx->ev_join[1], ctx->ev_join[2]},
+                 ctx->ev_chunk};
+    rc = project_launch(g, pl, (const double2*)(w + h.grid), (const double2*)(w + h.U), (const double2*)(w + h.V),
+                        (const double*)(w + h.sigma), S_dev, w + h.inner, sms, st, tl.on ? &tinfo : nullptr, ev_u, 1,
+                        dst, split ? &sp : nullptr, ev_prep);
+    if (tl.on) cudaEventRecord(tl.e[5], st);
+  }
+  // the LS step starts once the prep kernels are done and chunk 0 is enqueued (as in prony_pencil): its CTAs
+  // then fill the SMs the projection leaves idle instead of delaying its first wave
+  if (rc == PRONY_OK && !ok(cudaStreamWaitEvent(s3, ev_prep, 0))) rc = PRONY_ERR_CUDA;
   if (rc == PRONY_OK)
     rc = ls_launch(d, n, m, (int)N, (const double2*)(w + h.z), (const double2*)(w + h.grid), c0, c1, nullptr, G_dev,
                    b_dev, solve ? c_dev : nullptr, solve ? t_dev : nullptr, w + h.inner_ls, dst, sms, s3, nullptr);
-  // `st` ends after everything the call enqueued on s2, s3 and s4 (also when the projection had nothing to
-  // do and never waited on them): the host buffers may be released once `st` is synchronized, and a
-  // context's streams are idle for the next call once `st` reaches this point
+  if (tl.on) cudaEventRecord(tl.e[7], s3);
+  // `st` ends after everything the call enqueued on s2..s4 and the launch streams (s2 through s4's U copy, the
+  // launch streams through project_launch's joins; also when the projection had nothing to do and never waited on them): the host buffers may be
+  // released once `st` is synchronized, and a context's streams are idle for the next call once `st` gets here
   if (rc == PRONY_OK && !(ok(cudaEventRecord(ev_done, s3)) && ok(cudaStreamWaitEvent(st, ev_done, 0)) &&
-                          ok(cudaEventRecord(ev[6], s2)) && ok(cudaStreamWaitEvent(st, ev[6], 0)) &&
                           ok(cudaEventRecord(ev_u, s4)) && ok(cudaStreamWaitEvent(st, ev_u, 0))))
     rc = PRONY_ERR_CUDA;
-  if (rc != PRONY_OK) {
-    cudaStreamSynchronize(s2);
-    cudaStreamSynchronize(s3);
-    cudaStreamSynchronize(s4);
-  }
+  if (rc != PRONY_OK)
+    for (cudaStream_t s : {s2, s3, s4, ctx->sl[0], ctx->sl[1], ctx->sl[2]}) cudaStreamSynchronize(s);
   if (own) host_ctx_release(&local);
   return rc;
 }
@@ -487,7 +540,7 @@ int prony_host_context_create(prony_host_context* out) {
 
 int prony_host_context_destroy(prony_host_context ctx) {
   if (!ctx) return PRONY_ERR_INVALID;
-  for (cudaStream_t s : {ctx->s2, ctx->s3, ctx->s4})
+  for (cudaStream_t s : {ctx->s2, ctx->s3, ctx->s4, ctx->sl[0], ctx->sl[1], ctx->sl[2]})
     if (s) cudaStreamSynchronize(s);
   host_ctx_release(ctx);
   delete ctx;
@@ -584,9 +637,21 @@ int prony_pencil_host_ctx(prony_host_context ctx, int d, int n, int m, const pro
   };
   const bool good = d2h(S, h.S, (size_t)d * m * m * sizeof(double2)) && d2h(G, h.G, (size_t)m * m * sizeof(double2)) &&
                     d2h(b, h.b, m * sizeof(double2)) && d2h(c, h.c, m * sizeof(double2)) &&
-                    d2h(t, h.t, (size_t)m * d * sizeof(double)) && d2h(status_out, h.status, sizeof(int32_t)) &&
-                    cudaStreamSynchronize(st) == cudaSuccess;
-  return good ? PRONY_OK : PRONY_ERR_CUDA;
+                    d2h(t, h.t, (size_t)m * d * sizeof(double)) && d2h(status_out, h.status, sizeof(int32_t));
+  HostTimeline& tl = host_timeline();
+  if (tl.on) cudaEventRecord(tl.e[8], st);
+  const bool synced = good && cudaStreamSynchronize(st) == cudaSuccess;
+  if (synced && tl.on) {
+    fprintf(stderr, "PRONY_HOST_TIMELINE");
+    for (int i = 0; i < 9; ++i) {
+      float ms = -1.0f;
+      if (i != 1) cudaEventElapsedTime(&ms, tl.e[9], tl.e[i]);  // e[1] unused (the prep event is the context's)
+      if (i != 1) fprintf(stderr, " %s=%.3f", tl.name[i], ms);
+    }
+    fprintf(stderr, "\n");
+    (void)cudaGetLastError();
+  }
+  return synced ? PRONY_OK : PRONY_ERR_CUDA;
 }
 
 int prony_pencil_host_part(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,

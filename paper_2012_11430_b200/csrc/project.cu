@@ -227,8 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
   const int rb0 = blockIdx.x * BM;
   if (rb0 >= rows) return;  // whole CTA exits together
   const int chunk = blockIdx.y + p.chunk_base;
-  const int h_begin = chunk * p.chunk_w;
-  const int h_end = min(h_begin + p.chunk_w, p.N);
+  const int h_begin = chunk == 0 ? 0 : p.chunk0_w + (chunk - 1) * p.chunk_w;
+  const int h_end = min(h_begin + (chunk == 0 ? p.chunk0_w : p.chunk_w), p.N);
   const int KT = (h_end - h_begin + kBK - 1) / kBK;
   const int m = p.m, N = p.N, NP = p.NP;
 
@@ -978,9 +978,12 @@ int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl) {
       best_kc = kc;
     }
   }
+  const char* ekc = getenv("PRONY_KC");  // experiments: force the chunk count (1 .. kc_max)
+  if (ekc && atoi(ekc) >= 1) best_kc = std::min(atoi(ekc), kc_max);
   int chunk_w = (g.N + best_kc - 1) / best_kc;
   chunk_w = (chunk_w + kBK - 1) / kBK * kBK;
   pl->chunk_w = chunk_w;
+  pl->chunk0_w = chunk_w;
   pl->KC = (g.N + chunk_w - 1) / chunk_w;  // every chunk non-empty
   // reduce partition: about 1 CTA per SM in total
   const int slabs = std::max(1, (max_rows + 15) / 16);
@@ -1034,6 +1037,19 @@ WsLayout ws_layout(int d, int n, int N, int m, int sm_count) {
   return w;
 }
 }  // namespace
+
+void project_plan_lead(const ProjGeom& g, ProjPlan* pl) {
+  if (pl->KC < 2) return;
+  const int64_t cap_rows = (int64_t)kYCap * std::max<int64_t>((int64_t)g.d * g.N, ext_rows(g.d, g.n));
+  if ((int64_t)(pl->KC + 1) * std::max(pl->R_tot, 1) > cap_rows) return;  // no Y slot for one more chunk
+  const int w0 = (pl->chunk_w / 8 + kBK - 1) / kBK * kBK;
+  if (w0 < kBK || w0 >= g.N) return;
+  int w = (g.N - w0 + pl->KC - 1) / pl->KC;
+  w = (w + kBK - 1) / kBK * kBK;
+  pl->chunk0_w = w0;
+  pl->chunk_w = w;
+  pl->KC = 1 + (g.N - w0 + w - 1) / w;
+}
 
 size_t project_workspace_bytes(int d, int n, int N, int m, int sm_count) {
   return ws_layout(d, n, N, m, sm_count).total;
@@ -1107,7 +1123,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   if (pl.KC > 1 && cudaMemsetAsync(counters, 0, (size_t)pslots * nrb * sizeof(int), st) != cudaSuccess)
     return PRONY_ERR_CUDA;
   const bool split = sp && pl.KC > 1;
-  const int vrows0 = split ? std::min(pl.chunk_w, g.N) : g.N;
+  const int vrows0 = split ? std::min(pl.chunk0_w, g.N) : g.N;
   k_prep<<<8 * sm_count, 256, 0, st>>>(g.d, g.n, g.N, g.m, g.m, pl.shape.NP, box, grid, V, ptab, gsum, vsum,
                                        vrows0);
   if (g.shared) k_prep_ext<<<sm_count, 256, 0, st>>>(g.d, g.n, E, etab, umap);
@@ -1126,6 +1142,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   p.m = g.m;
   p.NP = pl.shape.NP;
   p.chunk_w = pl.chunk_w;
+  p.chunk0_w = pl.chunk0_w;
   p.R_tot = pl.R_tot;
   p.KC = pl.KC;
   p.nrb = nrb;
@@ -1190,19 +1207,28 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   };
   int lrc = PRONY_OK;
   if (split) {
-    // chunk 0 (V rows [0, chunk_w), already resident) on st; chunks 1..KC-1 on s_rest once the rest of V
-    // (enqueued there by the caller) and its Vsum rows are in; the fixup counts arrivals across both
-    if (cudaEventRecord(sp->ev_a, st) != cudaSuccess || cudaStreamWaitEvent(sp->s_rest, sp->ev_a, 0) != cudaSuccess)
-      return PRONY_ERR_CUDA;
+    // chunk 0 (V rows [0, chunk0_w), already resident) on st; chunks 1..KC-1 in up to kSplitStreams groups, each
+    // on its own stream once its V rows are in (the caller's copy events) and its Vsum rows are formed
+    if (cudaEventRecord(sp->ev_a, st) != cudaSuccess) return PRONY_ERR_CUDA;
     lrc = launch_main(p, dim3(grd.x, 1, grd.z), st, info);
     if (lrc != PRONY_OK) return lrc;
-    k_vsum<<<8 * sm_count, 256, 0, sp->s_rest>>>(vrows0, g.N, g.m, g.m, pl.shape.NP, V, vsum);
-    ProjParams pr = p;
-    pr.chunk_base = 1;
-    lrc = launch_main(pr, dim3(grd.x, pl.KC - 1, grd.z), sp->s_rest, nullptr);
-    if (lrc != PRONY_OK) return lrc;
-    if (cudaEventRecord(sp->ev_b, sp->s_rest) != cudaSuccess || cudaStreamWaitEvent(st, sp->ev_b, 0) != cudaSuccess)
-      return PRONY_ERR_CUDA;
+    const int nrest = pl.KC - 1, ng = std::min(kSplitStreams, nrest);
+    for (int gi = 0; gi < ng; ++gi) {
+      const int c_lo = 1 + nrest * gi / ng, c_hi = 1 + nrest * (gi + 1) / ng;  // chunks [c_lo, c_hi)
+      const int r0 = pl.chunk0_w + (c_lo - 1) * pl.chunk_w;
+      const int r1 = std::min(pl.chunk0_w + (c_hi - 1) * pl.chunk_w, g.N);
+      cudaStream_t ss = sp->s_rest[gi];
+      if (cudaStreamWaitEvent(ss, sp->ev_a, 0) != cudaSuccess ||
+          cudaStreamWaitEvent(ss, sp->ev_chunk[std::min(c_hi - 2, kMaxChunkEv - 1)], 0) != cudaSuccess)
+        return PRONY_ERR_CUDA;
+      k_vsum<<<8 * sm_count, 256, 0, ss>>>(r0, r1, g.m, g.m, pl.shape.NP, V, vsum);
+      ProjParams pr = p;
+      pr.chunk_base = c_lo;
+      lrc = launch_main(pr, dim3(grd.x, c_hi - c_lo, grd.z), ss, nullptr);
+      if (lrc != PRONY_OK) return lrc;
+      if (cudaEventRecord(sp->ev_b[gi], ss) != cudaSuccess || cudaStreamWaitEvent(st, sp->ev_b[gi], 0) != cudaSuccess)
+        return PRONY_ERR_CUDA;
+    }
   } else {
     lrc = launch_main(p, grd, st, info);
   }
@@ -1239,8 +1265,8 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   k_finalize<<<(int)std::min<int64_t>((8 * tot + 255) / 256, 4096), 256, 0, st>>>(g.d, g.m, pl.RP, Spart, sigma, S,
                                                                                   g.N, dev_status);
   if (info) {
-    info->launches = (g.shared ? 5 : 4) + (split ? 2 : 0);  // k_prep (+ k_prep_ext), k_project, k_reduce,
-                                                            // k_finalize (+ k_vsum, 2nd k_project)
+    info->launches = (g.shared ? 5 : 4) + (split ? 2 * std::min(kSplitStreams, pl.KC - 1) : 0);  // k_prep
+                      // (+ k_prep_ext), k_project, k_reduce, k_finalize (+ per later chunk group: k_vsum, k_project)
     info->main_grid[0] = (int)grd.x;
     info->main_grid[1] = (int)grd.y;
     info->main_grid[2] = (int)grd.z;
@@ -1567,6 +1593,7 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
     p.m = wcols;
     p.NP = pl.shape.NP;
     p.chunk_w = pl.chunk_w;
+    p.chunk0_w = pl.chunk0_w;
     p.R_tot = pl.R_tot;
     p.KC = pl.KC;
     p.nrb = nrb;

@@ -44,7 +44,8 @@ struct ProjPlan {
   ProjShape shape;
   int yoff[PRONY_MAX_D];
   int R_tot, max_rows;
-  int chunk_w, KC;  // split-K: KC chunks of chunk_w columns of T_l
+  int chunk_w, KC;  // split-K: KC chunks of chunk_w columns of T_l (chunk 0: chunk0_w columns)
+  int chunk0_w;     // width of chunk 0 (= chunk_w, or narrower after project_plan_lead)
   int RP;           // reduce partitions per l (the largest over the j-blocks)
   int nj;           // j-blocks of the warp-specialized reduce (k_reduce_ws)
   int rp_j[4];      // its row partitions per j-block (weighted by the j-block's active m-tiles)
@@ -61,6 +62,7 @@ struct ProjParams {
   double2* Y;
   int* counters;  // [d][nrb] split-K arrival counters (zeroed per call)
   int N, m, NP, chunk_w, R_tot, KC, nrb;
+  int chunk0_w;  // chunk c covers columns [c ? chunk0_w + (c-1) chunk_w : 0, +width) of T_l
   int box;  // grid size (debug index checks)
   int chunk_base;  // first split-K chunk of this launch (blockIdx.y + chunk_base)
   int kb[PRONY_MAX_D], rows[PRONY_MAX_D], yoff[PRONY_MAX_D], shift[PRONY_MAX_D];
@@ -76,20 +78,27 @@ struct RedParams {
   int rp_j[4];  // k_reduce_ws: row partitions of j-block z (CTAs with blockIdx.x >= rp_j[z] write zeros)
 };
 
-// Copy/compute overlap for callers whose V arrives in two parts (prony_pencil_host): when KC > 1 the
-// caller has made V rows [0, chunk_w) resident in stream order on `st` and enqueues the rest on
-// `s_rest` BEFORE calling project_launch; split-K chunk 0 then runs on `st` while chunks 1..KC-1 (and
-// their Vsum rows) run on `s_rest`; `ev_a` / `ev_b` are caller-owned scratch events.
-// ev_prepped (optional): recorded on `st` after the prep kernels, right before k_project is enqueued. A side
-// stream that waits on it (instead of on the call's start) cannot dispatch its CTAs ahead of k_project's:
-// the hardware then serves the earlier-enqueued k_project first and the side kernels fill its last wave.
+// Copy/compute overlap for callers whose V arrives in pieces (prony_pencil_host): when KC > 1 the caller has
+// made V rows [0, chunk0_w) resident in stream order on `st` and enqueued the copy of every later chunk's rows
+// on a copy stream, recording ev_chunk[min(c - 1, kMaxChunkEv - 1)] after chunk c's rows, BEFORE calling
+// project_launch. Chunk 0 of the projection then runs on `st`; chunks 1..KC-1 run in up to kSplitStreams
+// contiguous groups, group i on s_rest[i] as soon as its rows (and their Vsum rows) are in — separate streams,
+// so the groups' CTAs dispatch back to back as in one launch; the fixup counts arrivals across all launches.
+// `ev_a`, `ev_b[i]` are caller-owned scratch events.
+constexpr int kMaxChunkEv = 16;
+constexpr int kSplitStreams = 3;
 struct ProjSplit {
-  cudaStream_t s_rest;
-  cudaEvent_t ev_a, ev_b;
+  cudaStream_t s_rest[kSplitStreams];
+  cudaEvent_t ev_a;
+  cudaEvent_t ev_b[kSplitStreams];
+  const cudaEvent_t* ev_chunk;
 };
 
 ProjShape proj_shape(int m);
 int project_plan(const ProjGeom& g, int sm_count, ProjPlan* pl);
+// host-input pencils: a narrow chunk 0 (about a quarter of a chunk) ahead of the KC uniform chunks, so only its
+// V rows are copied before the first DMMA; no change when the workspace bound leaves no room for one more chunk
+void project_plan_lead(const ProjGeom& g, ProjPlan* pl);
 size_t project_workspace_bytes(int d, int n, int N, int m, int sm_count);
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
                    const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,

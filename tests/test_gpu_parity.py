@@ -446,6 +446,24 @@ def test_pencil_host_shapes(pb, orc, d, n, m, noise):
     assert rel(out["G"], G_or) <= TOL and rel(out["b"], b_or) <= TOL
 
 
+@pytest.mark.parametrize("kc", ["2", "5", "7"])
+def test_pencil_host_chunk_groups(pb, orc, kc, monkeypatch):
+    """The host-input pencil's copy pipeline with the split-K chunk count forced (PRONY_KC, read per call):
+    the narrow lead chunk plus 1..3 launch groups of one or several chunks, each released by its own copy
+    event; S, G, b against the oracle."""
+    monkeypatch.setenv("PRONY_KC", kc)
+    prob = W.make_problem("cfg2")
+    c = prob.cfg
+    out = pb.pencil_host(prob.grid, prob.U, prob.V, prob.sigma, prob.z, c.d, c.n, c.m)
+    assert out["status"] == 0
+    S_or = orc.project(prob.grid, prob.U, prob.V, prob.sigma, c.d, c.n)
+    for l in range(c.d):
+        assert rel(out["S"][l], S_or[l]) <= TOL
+    A_or = orc.vandermonde(prob.z, c.d, c.n)
+    G_or, b_or = orc.ls_products(A_or, prob.grid, c.d, c.n)
+    assert rel(out["G"], G_or) <= TOL and rel(out["b"], b_or) <= TOL
+
+
 def test_end_to_end_recovery_with_oracle_tail(pb, orc):
     """Algorithm 1 with the GPU pencil: S from the device, then the oracle's eig / diagonalization
     (NEXT-1 runs those on the device); t within 1e-8 of planted (noise-free cfg3)."""
