@@ -1042,7 +1042,9 @@ void project_plan_lead(const ProjGeom& g, ProjPlan* pl) {
   if (pl->KC < 2) return;
   const int64_t cap_rows = (int64_t)kYCap * std::max<int64_t>((int64_t)g.d * g.N, ext_rows(g.d, g.n));
   if ((int64_t)(pl->KC + 1) * std::max(pl->R_tot, 1) > cap_rows) return;  // no Y slot for one more chunk
-  const int w0 = (pl->chunk_w / 8 + kBK - 1) / kBK * kBK;
+  const char* eld = getenv("PRONY_LEAD_DIV");  // experiments: lead chunk = chunk_w / div (default 8)
+  const int div = eld && atoi(eld) >= 1 ? atoi(eld) : 8;
+  const int w0 = (pl->chunk_w / div + kBK - 1) / kBK * kBK;
   if (w0 < kBK || w0 >= g.N) return;
   int w = (g.N - w0 + pl->KC - 1) / pl->KC;
   w = (w + kBK - 1) / kBK * kBK;
