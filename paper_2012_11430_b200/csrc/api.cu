@@ -429,9 +429,9 @@ HostTimeline& host_timeline() {
 // chunk 0 of the projection; on the copy stream `s2` the V rows of chunk 1, 2, ... (an event after each);
 // on `s4` the U rows after all of V (first needed by k_reduce); `s3` carries z and, once the prep kernels are
 // done, the LS step. The later chunks of the projection run in groups on the context's launch streams, each
-// as soon as ITS rows are in, so only chunk 0's rows (about 1/24 of V) are copied before the first DMMA and
-// each later chunk's copy hides behind the chunks before it. On return `st` is ordered after everything. The streams / events come from `ctx` (a
-// caller's context) or are created for this call.
+// as soon as ITS rows are in, so only chunk 0's rows (about 1/24 of V) are copied before the first DMMA and each
+// later chunk's copy hides behind the chunks before it. On return `st` is ordered after everything. The streams /
+// events come from `ctx` (a caller's context) or are created for this call.
 int host_pencil(int d, int n, int m, int64_t N, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
                 const double* sigma, const prony_c128* z, int64_t e0, int64_t e1, int64_t c0, int64_t c1, bool solve,
                 double2* S_dev, double2* G_dev, double2* b_dev, double2* c_dev, double* t_dev, int32_t* dst,
@@ -508,9 +508,10 @@ int host_pencil(int d, int n, int m, int64_t N, const prony_c128* grid, const pr
     rc = ls_launch(d, n, m, (int)N, (const double2*)(w + h.z), (const double2*)(w + h.grid), c0, c1, nullptr, G_dev,
                    b_dev, solve ? c_dev : nullptr, solve ? t_dev : nullptr, w + h.inner_ls, dst, sms, s3, nullptr);
   if (tl.on) cudaEventRecord(tl.e[7], s3);
-  // `st` ends after everything the call enqueued on s2..s4 and the launch streams (s2 through s4's U copy, the
-  // launch streams through project_launch's joins; also when the projection had nothing to do and never waited on them): the host buffers may be
-  // released once `st` is synchronized, and a context's streams are idle for the next call once `st` gets here
+  // `st` ends after everything the call enqueued on s2..s4 and the launch streams (s2 through s4's U copy, the launch
+  // streams through project_launch's joins; also when the projection had nothing to do and never waited on them): the
+  // host buffers may be released once `st` is synchronized, and a context's streams are idle for the next call once
+  // `st` gets here
   if (rc == PRONY_OK && !(ok(cudaEventRecord(ev_done, s3)) && ok(cudaStreamWaitEvent(st, ev_done, 0)) &&
                           ok(cudaEventRecord(ev_u, s4)) && ok(cudaStreamWaitEvent(st, ev_u, 0))))
     rc = PRONY_ERR_CUDA;

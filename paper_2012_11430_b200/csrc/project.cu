@@ -255,13 +255,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_project(ProjParams p) {
     const int plane = pt & 31;
     const int32_t* __restrict__ ptab = p.ptab;
     if constexpr (T::ROWOWNER) {
-      // A gather, row-owner form (BM = 96, 48): gather thread pt < GT owns row ra = pt % BM of the tile for the whole CTA (its
-      // P(k_ra) + shift read once from the row table) and columns kc0, kc0 + TPR, ... of every stage; P(h0 + kc)
-      // comes from lane kc (shfl). Per element: one shfl, one subtraction, the two cp.async (immediate smem
-      // offsets). (The round-1/2 form decomposed e = pt + 96 j into (kc, ra) and re-read the row table per
-      // element, ~30 instructions per element: at m = 30 its consumers waited on the full barrier 7.8% of
-      // their samples.) Warp 3 first issues the stage's B rows: one bulk copy per V row (lanes 0..15) and per
-      // Vsum row (lanes 16..31), completing on the same full barrier (expect_tx).
+      // A gather, row-owner form (BM = 96, 48): gather thread pt < GT owns row ra = pt % BM of the tile for the
+      // whole CTA (its P(k_ra) + shift read once from the row table) and columns kc0, kc0 + TPR, ... of every stage;
+      // P(h0 + kc) comes from lane kc (shfl). Per element: one shfl, one subtraction, the two cp.async (immediate
+      // smem offsets). (The round-1/2 form decomposed e = pt + 96 j into (kc, ra) and re-read the row table per
+      // element, ~30 instructions per element: at m = 30 its consumers waited on the full barrier 7.8% of their
+      // samples.) Warp 3 first issues the stage's B rows: one bulk copy per V row (lanes 0..15) and per Vsum row
+      // (lanes 16..31), completing on the same full barrier (expect_tx).
       const double2* __restrict__ grid = p.grid;
       const double* __restrict__ gsum = p.gsum;
       const double2* __restrict__ V = p.V;
