@@ -41,8 +41,8 @@
  *   - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t; 0 = legacy
  *     default stream). Argument validation is synchronous, BEFORE any launch.
  *   - `dev_status` (device int32, caller-owned, nullable) receives numerical failures
- *     found on the device (first error wins); the caller must zero it beforehand and read
- *     it after synchronizing. The return value covers validation and launch errors only.
+ *     found on the device (first error wins); the caller must zero it beforehand (except for
+ *     prony_pencil, which zeroes it itself) and read it after synchronizing. The return value covers validation and launch errors only.
  *
  * Error behaviour (return values):
  *   PRONY_OK                 launched (or nothing to do for an empty range)
@@ -301,7 +301,9 @@ int prony_pencil_host_part_ctx(prony_host_context ctx, int d, int n, int m, cons
  *   grid, U, V, sigma, z   device inputs as prony_project / prony_vandermonde_ls
  *   S, G, b, c, t          device outputs (d x m x m, m x m, m, m, m x d)
  *   workspace    device scratch >= prony_workspace_size(PRONY_WS_PENCIL)
- *   dev_status   as prony_project (zeroed by the caller)
+ *   dev_status   nullable device int32, ZEROED BY THE CALL (in its first kernel, stream-ordered), then as
+ *                prony_project / prony_vandermonde_ls: after `stream` completes it holds this pencil's first
+ *                numerical failure or 0 (the launch path of small pencils saves the caller's separate reset)
  *   info_project, info_ls  nullable prony_exec_info of the two halves (events recorded on their streams)
  * Returns PRONY_OK, a validation error (as prony_project), PRONY_ERR_WORKSPACE or PRONY_ERR_CUDA.
  */

@@ -8,7 +8,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
+#include <vector>
 
 #include "../../include/prony.h"
 #include "common.cuh"
@@ -18,12 +20,40 @@
 
 using namespace prony;
 
+cudaError_t prony::ensure_smem_attr(const void* fn, int bytes) {
+  struct Entry {
+    int dev;
+    const void* fn;
+    int bytes;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  for (Entry& x : done)
+    if (x.dev == dev && x.fn == fn) {
+      if (x.bytes >= bytes) return cudaSuccess;
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (e == cudaSuccess) x.bytes = bytes;
+      return e;
+    }
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.push_back({dev, fn, bytes});
+  return e;
+}
+
 namespace {
 
 int sm_count_current() {
+  constexpr int kMaxDev = 64;
+  static int cached[kMaxDev] = {};  // SM count per device ordinal (0: not queried yet)
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (dev >= 0 && dev < kMaxDev && __atomic_load_n(&cached[dev], __ATOMIC_RELAXED) > 0) return cached[dev];
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  if (dev >= 0 && dev < kMaxDev) __atomic_store_n(&cached[dev], sms, __ATOMIC_RELAXED);
   return sms;
 }
 
@@ -591,7 +621,7 @@ int prony_pencil(prony_host_context ctx, int d, int n, int m, const prony_c128* 
   // take the SMs ahead of k_project's first wave (measured: k_project delayed 0.1 ms per pencil at cfg4); this
   // way k_project is served first and the LS CTAs fill the SMs its last wave leaves idle
   rc = project_launch(g, pl, (const double2*)grid, (const double2*)U, (const double2*)V, sigma, (double2*)S, w,
-                      sms, st, info_project, nullptr, 1, dev_status, nullptr, ev_in);
+                      sms, st, info_project, nullptr, 1, dev_status, nullptr, ev_in, /*reset_status=*/true);
   if (rc == PRONY_OK && cudaStreamWaitEvent(side, ev_in, 0) != cudaSuccess) rc = PRONY_ERR_CUDA;
   if (rc == PRONY_OK)
     rc = ls_launch(d, n, m, (int)N, (const double2*)z, (const double2*)grid, 0, N, nullptr, (double2*)G, (double2*)b,

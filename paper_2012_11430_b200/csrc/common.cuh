@@ -49,4 +49,12 @@ inline int64_t ipow(int64_t b, int e) {
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, size): the call costs microseconds
+// of host time, which small launch-bound pencils paid on every launch (api.cu)
+cudaError_t ensure_smem_attr(const void* fn, int bytes);
+template <typename K>
+cudaError_t ensure_smem_attr(K* fn, size_t bytes) {
+  return ensure_smem_attr(reinterpret_cast<const void*>(fn), (int)bytes);
+}
+
 }  // namespace prony

@@ -569,7 +569,7 @@ int house_qr_launch(int N, int r, double2* X, int ldx, int pivot, double tol, do
   w += align_up((size_t)r * sizeof(double2), 256);
   a.nfin = (double*)w;
   const size_t smem = (size_t)kHqWarps * r * sizeof(double2);
-  if (cudaFuncSetAttribute(k_house_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (ensure_smem_attr(k_house_qr, smem) != cudaSuccess)
     return PRONY_ERR_CUDA;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_house_qr, kHqThreads, smem) != cudaSuccess || per_sm < 1)

@@ -77,9 +77,20 @@ __device__ __forceinline__ void vsum_rows(int r0, int r1, int m, int ldv, int NP
     vsum_rows_t<int64_t>(r0, r1, m, ldv, NP, V, vsum);
 }
 
+__device__ __forceinline__ void prep_ext_rows(int d, int n, int64_t E, int32_t* __restrict__ etab,
+                                              int32_t* __restrict__ umap);
+
+// The staging kernel of a projection: P table, gsum plane, the Vsum rows [0, vrows), and in the same launch
+// (one launch instead of three host API calls for small, launch-bound pencils) the shared-row tables when etab
+// is given, the split-K arrival counters zeroed, and optionally the caller's status word zeroed (prony_pencil).
 __global__ void k_prep(int d, int n, int N, int m, int ldv, int NP, int64_t box, const double2* __restrict__ grid,
                        const double2* __restrict__ V, int32_t* __restrict__ ptab, double* __restrict__ gsum,
-                       double* __restrict__ vsum, int vrows) {
+                       double* __restrict__ vsum, int vrows, int64_t E, int32_t* __restrict__ etab,
+                       int32_t* __restrict__ umap, int* __restrict__ counters, int ncounters,
+                       int32_t* __restrict__ zero_status) {
+  if (etab) prep_ext_rows(d, n, E, etab, umap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ncounters; i += gridDim.x * blockDim.x) counters[i] = 0;
+  if (zero_status && blockIdx.x == 0 && threadIdx.x == 0) *zero_status = 0;
   const int L = 2 * n + 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -111,7 +122,8 @@ __global__ void k_vsum(int r0, int r1, int m, int ldv, int NP, const double2* __
 // Shared-row tables (F8): for e in E = {0..n+1}^d with coordinates c (base n+2, last
 // fastest): etab[e] = sum_i c_i L^(d-1-i), so T_E[e,h] = grid[etab[e] - P(h) + C0]; and for each l,
 // umap[l][e] = index in I_n of k = c - e_l when that k lies in I_n (then T_l[k,:] = T_E[e,:]), else -1.
-__global__ void k_prep_ext(int d, int n, int64_t E, int32_t* __restrict__ etab, int32_t* __restrict__ umap) {
+__device__ __forceinline__ void prep_ext_rows(int d, int n, int64_t E, int32_t* __restrict__ etab,
+                                              int32_t* __restrict__ umap) {
   const int L = 2 * n + 2, Le = n + 2;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E + kPtabPad;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -1061,7 +1073,7 @@ template <int NT, int WN>
 static int launch_project_t(const ProjParams& p, dim3 grid, cudaStream_t st, int mode, prony_exec_info* info) {
   const size_t smem = ProjTile<NT, WN>::SMEM;
   auto kp = mode == 4 ? k_project<NT, WN, 4> : k_project<NT, WN, 3>;
-  if (cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (ensure_smem_attr(kp, smem) != cudaSuccess)
     return PRONY_ERR_CUDA;
   if (info && info->ev_main_begin) cudaEventRecord((cudaEvent_t)info->ev_main_begin, st);
   kp<<<grid, kThreads, smem, st>>>(p);
@@ -1073,7 +1085,7 @@ template <int NT, int WN>
 static int launch_reduce_t(const RedParams& r, dim3 rgrid, cudaStream_t st, int mode) {
   auto kr = mode == 4 ? k_reduce<NT, WN, 4> : k_reduce<NT, WN, 3>;
   const size_t smem = RedTile<NT, WN>::SMEM;
-  if (cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (ensure_smem_attr(kr, smem) != cudaSuccess)
     return PRONY_ERR_CUDA;
   rgrid.z = (r.NP + RedTile<NT, WN>::BJ - 1) / RedTile<NT, WN>::BJ;
   kr<<<rgrid, kReduceThreads, smem, st>>>(r);
@@ -1083,9 +1095,7 @@ static int launch_reduce_t(const RedParams& r, dim3 rgrid, cudaStream_t st, int 
 template <int NT, int WN>
 static int launch_reduce_ws_t(const RedParams& r, dim3 rgrid, cudaStream_t st) {
   const size_t smem = RedWsTile<NT, WN>::SMEM;
-  if (cudaFuncSetAttribute(k_reduce_ws<NT, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return PRONY_ERR_CUDA;
+  if (ensure_smem_attr(k_reduce_ws<NT, WN>, smem) != cudaSuccess) return PRONY_ERR_CUDA;
   k_reduce_ws<NT, WN><<<rgrid, kRwsThreads, smem, st>>>(r);
   return PRONY_OK;
 }
@@ -1093,7 +1103,7 @@ static int launch_reduce_ws_t(const RedParams& r, dim3 rgrid, cudaStream_t st) {
 int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, const double2* U, const double2* V,
                    const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
                    prony_exec_info* info, cudaEvent_t wait_before_reduce, int ell_base, int32_t* dev_status,
-                   const ProjSplit* sp, cudaEvent_t ev_prepped) {
+                   const ProjSplit* sp, cudaEvent_t ev_prepped, bool reset_status) {
   const WsLayout wl = ws_layout(g.d, g.n, g.N, g.m, sm_count);
   char* w = (char*)ws;
   int32_t* ptab = (int32_t*)(w + wl.ptab);
@@ -1116,19 +1126,19 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   }
   if (pl.R_tot == 0) {
     if (cudaMemsetAsync(S, 0, (size_t)g.d * g.m * g.m * sizeof(double2), st) != cudaSuccess) return PRONY_ERR_CUDA;
+    if (reset_status && dev_status && cudaMemsetAsync(dev_status, 0, sizeof(int32_t), st) != cudaSuccess)
+      return PRONY_ERR_CUDA;
     if (ev_prepped && cudaEventRecord(ev_prepped, st) != cudaSuccess) return PRONY_ERR_CUDA;
     return PRONY_OK;
   }
   int64_t box = 1;
   for (int i = 0; i < g.d; ++i) box *= (2 * (int64_t)g.n + 2);
   const int nrb = (pl.max_rows + pl.shape.BM - 1) / pl.shape.BM;
-  if (pl.KC > 1 && cudaMemsetAsync(counters, 0, (size_t)pslots * nrb * sizeof(int), st) != cudaSuccess)
-    return PRONY_ERR_CUDA;
   const bool split = sp && pl.KC > 1;
   const int vrows0 = split ? std::min(pl.chunk0_w, g.N) : g.N;
   k_prep<<<8 * sm_count, 256, 0, st>>>(g.d, g.n, g.N, g.m, g.m, pl.shape.NP, box, grid, V, ptab, gsum, vsum,
-                                       vrows0);
-  if (g.shared) k_prep_ext<<<sm_count, 256, 0, st>>>(g.d, g.n, E, etab, umap);
+                                       vrows0, E, g.shared ? etab : nullptr, umap, counters,
+                                       pl.KC > 1 ? pslots * nrb : 0, reset_status ? dev_status : nullptr);
   if (ev_prepped && cudaEventRecord(ev_prepped, st) != cudaSuccess) return PRONY_ERR_CUDA;
 
   ProjParams p{};
@@ -1267,8 +1277,9 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
   k_finalize<<<(int)std::min<int64_t>((8 * tot + 255) / 256, 4096), 256, 0, st>>>(g.d, g.m, pl.RP, Spart, sigma, S,
                                                                                   g.N, dev_status);
   if (info) {
-    info->launches = (g.shared ? 5 : 4) + (split ? 2 * std::min(kSplitStreams, pl.KC - 1) : 0);  // k_prep
-                      // (+ k_prep_ext), k_project, k_reduce, k_finalize (+ per later chunk group: k_vsum, k_project)
+    info->launches = 4 + (split ? 2 * std::min(kSplitStreams, pl.KC - 1) : 0);  // k_prep
+                      // (with the shared-row tables), k_project, k_reduce, k_finalize (+ per later chunk group: k_vsum,
+                      // k_project)
     info->main_grid[0] = (int)grd.x;
     info->main_grid[1] = (int)grd.y;
     info->main_grid[2] = (int)grd.z;
@@ -1558,7 +1569,7 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
     if (smem > 227 * 1024) q = 0;
     if (q) {
       if (smem > 48 * 1024 &&
-          cudaFuncSetAttribute(k_toeplitz_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+          ensure_smem_attr(k_toeplitz_mv, smem) != cudaSuccess)
         return PRONY_ERR_CUDA;
       k_toeplitz_mv<<<dim3(Mp, S), nth, smem, st>>>(d, n, q, Mp, S, g, shift, X, ldx, Y);
       k_mv_reduce<<<(N + 255) / 256, 256, 0, st>>>(N, S, Y, Yout, ldy);
@@ -1581,7 +1592,8 @@ int toeplitz_apply_launch(int d, int n, int N, const double2* grid, int ell, int
     project_plan(gg, sm_count, &pl);
     const int nrb = (pl.max_rows + pl.shape.BM - 1) / pl.shape.BM;
     if (pl.KC > 1 && cudaMemsetAsync(counters, 0, (size_t)nrb * sizeof(int), st) != cudaSuccess) return PRONY_ERR_CUDA;
-    k_prep<<<8 * sm_count, 256, 0, st>>>(d, n, N, wcols, ldx, pl.shape.NP, box, g, X + c0, ptab, gsum, vsum, N);
+    k_prep<<<8 * sm_count, 256, 0, st>>>(d, n, N, wcols, ldx, pl.shape.NP, box, g, X + c0, ptab, gsum, vsum, N, 0,
+                                         nullptr, nullptr, nullptr, 0, nullptr);
     ProjParams p{};
     p.grid = g;
     p.gsum = gsum;

@@ -104,7 +104,7 @@ int project_launch(const ProjGeom& g, const ProjPlan& pl, const double2* grid, c
                    const double* sigma, double2* S, void* ws, int sm_count, cudaStream_t st,
                    prony_exec_info* info, cudaEvent_t wait_before_reduce = nullptr, int ell_base = 1,
                    int32_t* dev_status = nullptr, const ProjSplit* split = nullptr,
-                   cudaEvent_t ev_prepped = nullptr);
+                   cudaEvent_t ev_prepped = nullptr, bool reset_status = false);
 __global__ void k_combine_grid(int d, int n, int64_t box, const double2* grid, const double2* mu, double2* out);
 
 size_t apply_workspace_bytes(int d, int n, int N);

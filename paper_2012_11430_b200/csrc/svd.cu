@@ -239,7 +239,7 @@ int diagonalize_launch(int d, int m, const double2* S, const double2* mu, double
     return PRONY_ERR_CUDA;
   {
     const size_t hsm = m <= 119 ? (size_t)m * m * sizeof(double2) : 0;  // kHqrSmemMaxM (dense.cu)
-    if (hsm && cudaFuncSetAttribute(k_hqr_vals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm) != cudaSuccess)
+    if (hsm && ensure_smem_attr(k_hqr_vals, hsm) != cudaSuccess)
       return PRONY_ERR_CUDA;
     k_hqr_vals<<<1, 32, hsm, st>>>(m, C, lam, status, 60);  // eigenvalues (C overwritten)
   }

@@ -493,7 +493,7 @@ size_t ls_workspace_bytes(int d, int n, int m, int sm_count) {
 }
 
 static int launch_vls(const VlsParams& p, dim3 grid, size_t smem, cudaStream_t st) {
-  if (cudaFuncSetAttribute(k_vls<kVlsNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (ensure_smem_attr(k_vls<kVlsNT>, smem) != cudaSuccess)
     return PRONY_ERR_CUDA;
   k_vls<kVlsNT><<<grid, kVlsThreads, smem, st>>>(p);
   return PRONY_OK;
@@ -503,7 +503,7 @@ int ls_solve_launch(int d, int m, const double2* G, const double2* b, const doub
                     void* ws, int32_t* status, cudaStream_t st) {
   (void)ws;
   const size_t smem = solve_smem(m);
-  if (cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (ensure_smem_attr(k_solve, smem) != cudaSuccess)
     return PRONY_ERR_CUDA;
   k_solve<<<1, kSolveThreads, smem, st>>>(d, m, G, b, z, c, t, status);
   if (cudaGetLastError() != cudaSuccess) return PRONY_ERR_CUDA;

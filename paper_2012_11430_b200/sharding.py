@@ -209,8 +209,7 @@ class DistributedPencil:
             if self.ctx is None:
                 self.ctx = pb.HostContext()
                 self.ws_pencil = pb.alloc_workspace(pb.WS_PENCIL, d, n, m, self.device)
-            with torch.cuda.stream(main):
-                self.status.zero_()
+            # prony_pencil zeroes the status word in its first kernel (no separate reset launch)
             pb.pencil(grid, U, V, sigma, z, d, n, m, self.outs, self.ws_pencil, context=self.ctx,
                       dev_status=self.status, stream=main, info_p=info_p, info_l=info_l)
             self._note(info_p, info_l, 0)

@@ -653,6 +653,28 @@ def test_pencil_host_part_empty_and_partial(pb, orc):
     assert rel(G, G_or) <= TOL and rel(b, b_or) <= TOL
 
 
+def test_pencil_resets_and_reports_status(pb):
+    """prony_pencil zeroes dev_status itself (first kernel, stream-ordered): a stale nonzero word from an earlier
+    failure is cleared by a good pencil, and a bad sigma (below the scale guard) is reported by the next call."""
+    prob = problem(2, 12, 5, 1777, 0.0, random_uv=True)
+    c0 = prob.cfg
+    d, n, m = c0.d, c0.n, c0.m
+    pencil = pb.sharding.DistributedPencil(d, n, m, torch.device("cuda", 0))
+    args = [dev(getattr(prob, k)) for k in ("grid", "U", "V", "sigma", "z")]
+    pencil.status.fill_(pb.PRONY_ERR_SINGULAR)
+    pencil(*args)
+    torch.cuda.synchronize()
+    assert int(pencil.status.item()) == 0
+    bad_sigma = args[3].clone()
+    bad_sigma[-1] = 0.0
+    pencil(args[0], args[1], args[2], bad_sigma, args[4])
+    torch.cuda.synchronize()
+    assert int(pencil.status.item()) == pb.PRONY_ERR_SINGULAR
+    pencil(*args)
+    torch.cuda.synchronize()
+    assert int(pencil.status.item()) == 0
+
+
 def test_pencil_one_call_and_graph_replay(pb, orc):
     """prony_pencil (one C call: projection on the stream, LS + solve on the context's side stream) through
     sharding.DistributedPencil at N = 1, eager and captured once in a CUDA graph then replayed on new inputs
