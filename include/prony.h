@@ -36,8 +36,9 @@
  *   - Every pointer argument of prony_project / prony_vandermonde_ls is a DEVICE pointer
  *     owned by the caller (e.g. a torch tensor); the library never allocates, frees or
  *     retains memory. Scratch comes only from the caller's `workspace` (device, 256-byte
- *     aligned, size >= prony_workspace_size(...)). No global mutable state: calls are
- *     reentrant and CUDA-graph capturable.
+ *     aligned, size >= prony_workspace_size(...)). No global mutable state beyond
+ *     idempotent, thread-safe memoization of device facts (the SM count per device, each
+ *     kernel's shared-memory opt-in): calls are reentrant and CUDA-graph capturable.
  *   - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t; 0 = legacy
  *     default stream). Argument validation is synchronous, BEFORE any launch.
  *   - `dev_status` (device int32, caller-owned, nullable) receives numerical failures
