@@ -524,11 +524,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--cmul", choices=["3m", "4m"], default=None,
+                    help="complex products of the DMMA engine: 3M (Gauss, default) or 4M (sets PRONY_CMUL)")
     ap.add_argument("--force-dist", action="store_true",
                     help="test hook: run the N > 1 path (process group + collectives) even with one rank")
     ap.add_argument("--units", default="shared", choices=["shared", "l-major", "row-major"],
                     help="prony_unit_order of the projection (shared: one extended product for all l, F8)")
     args = ap.parse_args()
+    if args.cmul:
+        os.environ["PRONY_CMUL"] = args.cmul  # read by the library at each launch (and by torchrun children)
     if args.warmup < 3:
         args.warmup = 3
     cfg = W.CONFIGS[args.cfg]

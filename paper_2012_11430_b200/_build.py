@@ -37,7 +37,7 @@ def build_variant(out_path: str, defines: list[str]) -> str:
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
     r = subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out_path, *objs,
-                        "-lcudart"], capture_output=True, text=True)
+                        "-lcudart", "-ldl"], capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(r.stderr)
     for o in objs:
@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs, "-lcudart"]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs, "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

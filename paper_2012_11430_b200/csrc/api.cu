@@ -12,6 +12,8 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/prony.h"
 #include "common.cuh"
 #include "project.cuh"
@@ -19,6 +21,15 @@
 #include "dense.cuh"
 
 using namespace prony;
+
+// NVTX range over each compute entry point (SURVEY §5 tracing): named ranges on the host timeline of nsys /
+// ncu --nvtx; without an attached tool the push / pop are a few nanoseconds
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 cudaError_t prony::ensure_smem_attr(const void* fn, int bytes) {
   struct Entry {
@@ -218,6 +229,7 @@ int prony_project_ex(int d, int n, int m, const prony_c128* grid, const prony_c1
                      const double* sigma, int64_t unit_begin, int64_t unit_end, int unit_order, prony_c128* S,
                      void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream,
                      prony_exec_info* info) {
+  NvtxRange nvtx_("prony_project_ex");
   int64_t N = 0;
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
@@ -255,6 +267,7 @@ int prony_vandermonde_ls_ex(int d, int n, int m, const prony_c128* z, const pron
                             int64_t col_end, prony_c128* A, prony_c128* G, prony_c128* b, prony_c128* c, double* t,
                             void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream,
                             prony_exec_info* info) {
+  NvtxRange nvtx_("prony_vandermonde_ls_ex");
   int64_t N = 0;
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
@@ -272,6 +285,7 @@ int prony_vandermonde_ls_ex(int d, int n, int m, const prony_c128* z, const pron
 
 int prony_ls_solve(int d, int m, const prony_c128* G, const prony_c128* b, const prony_c128* z, prony_c128* c,
                    double* t, void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream) {
+  NvtxRange nvtx_("prony_ls_solve");
   if (d < 1 || d > PRONY_MAX_D || m < 1) return PRONY_ERR_INVALID;
   if (m > PRONY_MAX_M) return PRONY_ERR_RANGE;
   (void)workspace_bytes;  // the solve keeps its factor in shared memory; no scratch is needed
@@ -285,6 +299,7 @@ int prony_ls_solve(int d, int m, const prony_c128* G, const prony_c128* b, const
 int prony_project_mu(int d, int n, int m, const prony_c128* grid, const prony_c128* U, const prony_c128* V,
                      const double* sigma, const prony_c128* mu, prony_c128* C, void* workspace, size_t workspace_bytes,
                      int32_t* dev_status, prony_stream_t stream) {
+  NvtxRange nvtx_("prony_project_mu");
   int64_t N = 0;
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
@@ -323,6 +338,7 @@ int prony_project_mu(int d, int n, int m, const prony_c128* grid, const prony_c1
 
 int prony_toeplitz_apply(int d, int n, const prony_c128* grid, int ell, int conj, const prony_c128* X, int ldx, int r,
                          prony_c128* Y, int ldy, void* workspace, size_t workspace_bytes, prony_stream_t stream) {
+  NvtxRange nvtx_("prony_toeplitz_apply");
   int64_t N = 0;
   int rc = validate_dnm(d, n, 1, &N);
   if (rc) return rc;
@@ -583,6 +599,7 @@ int prony_pencil(prony_host_context ctx, int d, int n, int m, const prony_c128* 
                  prony_c128* b, prony_c128* c, double* t, void* workspace, size_t workspace_bytes,
                  int32_t* dev_status, prony_stream_t stream, prony_exec_info* info_project,
                  prony_exec_info* info_ls) {
+  NvtxRange nvtx_("prony_pencil");
   int64_t N = 0;
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
@@ -646,6 +663,7 @@ int prony_pencil_host_ctx(prony_host_context ctx, int d, int n, int m, const pro
                           const prony_c128* V, const double* sigma, const prony_c128* z, prony_c128* S, prony_c128* G,
                           prony_c128* b, prony_c128* c, double* t, void* workspace, size_t workspace_bytes,
                           int32_t* status_out, prony_stream_t stream) {
+  NvtxRange nvtx_("prony_pencil_host_ctx");
   int64_t N = 0;
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
@@ -698,6 +716,7 @@ int prony_pencil_host_part_ctx(prony_host_context ctx, int d, int n, int m, cons
                                int64_t unit_begin, int64_t unit_end, int64_t col_begin, int64_t col_end, prony_c128* S,
                                prony_c128* G, prony_c128* b, void* workspace, size_t workspace_bytes,
                                int32_t* dev_status, prony_stream_t stream) {
+  NvtxRange nvtx_("prony_pencil_host_part_ctx");
   int64_t N = 0;
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
@@ -718,6 +737,7 @@ int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t see
                        prony_c128* S, prony_c128* U, prony_c128* V, double* sigma, int32_t* rank_out,
                        double* resid_out, void* workspace, size_t workspace_bytes, int32_t* dev_status,
                        prony_stream_t stream) {
+  NvtxRange nvtx_("prony_build_pencil");
   int64_t N = 0;
   int rc = validate_dnm(d, n, m, &N);
   if (rc) return rc;
@@ -749,6 +769,7 @@ int prony_build_pencil(int d, int n, int m, const prony_c128* grid, uint64_t see
 int prony_lanczos_svd(int d, int n, const prony_c128* grid, int max_rank, double tol, uint64_t seed, int ldo,
                       prony_c128* U, prony_c128* V, double* sigma, int32_t* rank_out, int32_t* steps_out,
                       void* workspace, size_t workspace_bytes, prony_stream_t stream) {
+  NvtxRange nvtx_("prony_lanczos_svd");
   int64_t N = 0;
   int rc = validate_dnm(d, n, 1, &N);
   if (rc) return rc;
@@ -770,6 +791,7 @@ int prony_lanczos_svd(int d, int n, const prony_c128* grid, int max_rank, double
 
 int prony_diagonalize(int d, int m, const prony_c128* S, const prony_c128* mu, prony_c128* z, double* t, prony_c128* W,
                       void* workspace, size_t workspace_bytes, int32_t* dev_status, prony_stream_t stream) {
+  NvtxRange nvtx_("prony_diagonalize");
   if (d < 1 || d > PRONY_MAX_D || m < 1) return PRONY_ERR_INVALID;
   if (m > PRONY_MAX_M) return PRONY_ERR_RANGE;
   if (!S || !mu || !z || !W || !workspace) return PRONY_ERR_INVALID;
