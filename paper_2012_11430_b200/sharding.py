@@ -195,9 +195,11 @@ class DistributedPencil:
         around k_project / k_vls (each already recorded once so its handle exists); ev_comm: optional
         (begin, end) events recorded around the collective of S.
 
-        N > 1: the LS branch (side stream) all-reduces its G, b once they are done AND k_project has finished
-        (so no rank's NCCL kernel spins on SMs its projection needs) and solves for c, t there, alongside the
-        projection stream's k_reduce_ws, k_finalize and all-reduce of S."""
+        N > 1: the LS branch (side stream, released right before k_project, which runs on a HIGHER-priority
+        stream) gets SMs only once k_project's CTA queue is drained — in its last wave — and all-reduces its G, b
+        and solves for c, t there, so the NCCL kernel and the one-CTA solve use the SMs the last wave leaves idle
+        instead of following k_project; the projection stream then runs k_reduce_ws, k_finalize and the
+        all-reduce of S."""
         pb, d, n, m = self.pb, self.d, self.n, self.m
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
         full = not self.collective
@@ -221,7 +223,6 @@ class DistributedPencil:
             self.ev_in.record(hi)
             pb.project(grid, U, V, sigma, d, n, m, self.u0, self.u1, self.order, out=self.S, workspace=self.ws_p,
                        dev_status=self.status, stream=hi, info=info_p)
-        ev_proj_end = pe[1]  # recorded by the library right after k_project
         side.wait_event(self.ev_in)
         side.wait_event(pe[0])  # recorded by the library right before k_project (stale only if it had no rows)
         with torch.cuda.stream(side):
@@ -229,8 +230,7 @@ class DistributedPencil:
                                     out={"G": self.G, "b": self.b, "c": self.c, "t": self.t}, workspace=self.ws_l,
                                     dev_status=self.status, stream=side, info=info_l)
             if not full:
-                side.wait_event(ev_proj_end)
-                self._allreduce(self.buf[d * m * m:])            # G, b
+                self._allreduce(self.buf[d * m * m:])            # G, b (in k_project's last wave)
                 pb.ls_solve(self.G, self.b, z, d, m, dev_status=self.status, stream=side,
                             out={"c": self.c, "t": self.t})
             self.ev_ls.record(side)
