@@ -70,9 +70,10 @@
 extern "C" {
 #endif
 
-#define PRONY_ABI_VERSION 5  /* 2: PRONY_UNITS_SHARED, prony_lanczos_svd, PRONY_WS_LANCZOS; 3: prony_pencil_host_part;
+#define PRONY_ABI_VERSION 6  /* 2: PRONY_UNITS_SHARED, prony_lanczos_svd, PRONY_WS_LANCZOS; 3: prony_pencil_host_part;
                                  4: prony_host_context, prony_pencil_host_ctx, prony_pencil_host_part_ctx;
-                                 5: prony_pencil, PRONY_WS_PENCIL */
+                                 5: prony_pencil, PRONY_WS_PENCIL;
+                                 6: prony_exec_info.ev_wait_u (prony_project_ex) */
 #define PRONY_MAX_D 8
 #define PRONY_MAX_M 128
 
@@ -136,6 +137,9 @@ typedef struct prony_exec_info {
   int32_t split_k;        /* out: column chunks of T_l (prony_project) / column blocks (LS) */
   double main_flops;      /* out: algorithmic FP64 flops of the dominant kernel (8 real flops per
                              complex multiply-add): 8 m N * rows for k_project, 8 m^2 W for k_vls */
+  void* ev_wait_u;        /* in, nullable (prony_project_ex only): cudaEvent_t the stream waits on right
+                             before the reduction, the first kernel that reads U — lets a caller still
+                             copying U (another stream) overlap that copy with the projection */
 } prony_exec_info;
 
 /* ABI version (== PRONY_ABI_VERSION of the built library). */

@@ -39,14 +39,16 @@ class ExecInfo(ctypes.Structure):
     """prony_exec_info (include/prony.h): events around the dominant kernel + launch record."""
     _fields_ = [("ev_main_begin", ctypes.c_void_p), ("ev_main_end", ctypes.c_void_p), ("launches", ctypes.c_int32),
                 ("main_grid", ctypes.c_int32 * 3), ("main_block", ctypes.c_int32), ("split_k", ctypes.c_int32),
-                ("main_flops", ctypes.c_double)]
+                ("main_flops", ctypes.c_double), ("ev_wait_u", ctypes.c_void_p)]
 
 
-def make_exec_info(ev_begin=None, ev_end=None) -> ExecInfo:
-    """ev_*: torch.cuda.Event(enable_timing=True) already created (recorded once)."""
+def make_exec_info(ev_begin=None, ev_end=None, ev_wait_u=None) -> ExecInfo:
+    """ev_*: torch.cuda.Event already created (recorded once). ev_wait_u (prony_project_ex): an event the call's
+    stream waits on before the reduction that first reads U."""
     info = ExecInfo()
     info.ev_main_begin = ev_begin.cuda_event if ev_begin is not None else None
     info.ev_main_end = ev_end.cuda_event if ev_end is not None else None
+    info.ev_wait_u = ev_wait_u.cuda_event if ev_wait_u is not None else None
     return info
 
 

@@ -253,7 +253,8 @@ int prony_project_ex(int d, int n, int m, const prony_c128* grid, const prony_c1
   ProjPlan pl{};
   project_plan(g, sms, &pl);
   return project_launch(g, pl, (const double2*)grid, (const double2*)U, (const double2*)V, sigma, (double2*)S,
-                        workspace, sms, (cudaStream_t)stream, info, nullptr, 1, dev_status);
+                        workspace, sms, (cudaStream_t)stream, info,
+                        info ? (cudaEvent_t)info->ev_wait_u : nullptr, 1, dev_status);
 }
 
 int prony_vandermonde_ls(int d, int n, int m, const prony_c128* z, const prony_c128* grid, int64_t col_begin,

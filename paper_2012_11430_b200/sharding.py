@@ -188,12 +188,13 @@ class DistributedPencil:
         self.ev_pbeg = torch.cuda.Event()
         self.ev_pbeg.record(torch.cuda.current_stream(self.device))
 
-    def __call__(self, grid, U, V, sigma, z, stream=None, ev_project=None, ev_ls=None, ev_comm=None):
+    def __call__(self, grid, U, V, sigma, z, stream=None, ev_project=None, ev_ls=None, ev_comm=None, ev_wait_u=None):
         """Device-resident inputs -> (S, c, t) (views of this object's buffers, valid until the next call).
         Ordered after prior work on `stream` (default: the current stream), which is ordered after all of it
         on return. ev_project / ev_ls: optional (begin, end) timing torch.cuda.Events the library records
         around k_project / k_vls (each already recorded once so its handle exists); ev_comm: optional
-        (begin, end) events recorded around the collective of S.
+        (begin, end) events recorded around the collective of S; ev_wait_u: optional event after which U is complete
+        (a copy still in flight on another stream): only the reduction, the first kernel reading U, waits for it.
 
         N > 1: the LS branch (side stream, released right before k_project, which runs on a HIGHER-priority
         stream) gets SMs only once k_project's CTA queue is drained — in its last wave — and all-reduces its G, b
@@ -204,13 +205,15 @@ class DistributedPencil:
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
         full = not self.collective
         pe = ev_project if ev_project is not None else (self.ev_pbeg, self.ev_proj)
-        info_p = pb.make_exec_info(pe[0], pe[1])
+        info_p = pb.make_exec_info(pe[0], pe[1], ev_wait_u)
         info_l = pb.make_exec_info(*ev_ls) if ev_ls is not None else pb.make_exec_info()
         if full and self.order == UNITS_SHARED:
             # one C call (prony_pencil): the projection on `main`, the LS step on the context's side stream
             if self.ctx is None:
                 self.ctx = pb.HostContext()
                 self.ws_pencil = pb.alloc_workspace(pb.WS_PENCIL, d, n, m, self.device)
+            if ev_wait_u is not None:  # prony_pencil has no U hook: the whole call waits for U
+                main.wait_event(ev_wait_u)
             # prony_pencil zeroes the status word in its first kernel (no separate reset launch)
             pb.pencil(grid, U, V, sigma, z, d, n, m, self.outs, self.ws_pencil, context=self.ctx,
                       dev_status=self.status, stream=main, info_p=info_p, info_l=info_l)
@@ -293,6 +296,9 @@ class DistributedPencil:
             self.dU = torch.zeros((self.N, m), dtype=torch.complex128, device=dev)
             self.dVpad = torch.zeros((chunk * self.world, m), dtype=torch.complex128, device=dev)
             self.dVmine = torch.zeros((chunk, m), dtype=torch.complex128, device=dev)
+            self.su = torch.cuda.Stream(device=dev)  # U rows behind V's slice, overlapped with the projection
+            self.ev_vcopied = torch.cuda.Event()
+            self.ev_ucopied = torch.cuda.Event()
         with torch.cuda.stream(main):
             self.dz.copy_(z_h, non_blocking=True)
             if not scatter_v:
@@ -308,13 +314,22 @@ class DistributedPencil:
                                     self.S, self.G, self.b, workspace=self.ws_h, dev_status=self.status, stream=main,
                                     context=self.hctx)
                 return self._reduce_and_solve(self.dz, main, ev_comm)
-            chunk, (v0, v1), (ulo, uhi) = host_rows(d, n, self.world, self.rank, self.order)
+            if not hasattr(self, "rows_h"):  # a Python scan over the unit range: computed once, not per call
+                self.rows_h = host_rows(d, n, self.world, self.rank, self.order)
+            chunk, (v0, v1), (ulo, uhi) = self.rows_h
             self.dgrid.copy_(grid_h, non_blocking=True)
             self.dsig.copy_(sigma_h, non_blocking=True)
-            if uhi > ulo:
-                self.dU[ulo:uhi].copy_(U_h[ulo:uhi], non_blocking=True)
             if v1 > v0:
                 self.dVmine[:v1 - v0].copy_(V_h[v0:v1], non_blocking=True)
+            self.ev_vcopied.record(main)
+        # the U rows cross the link after V's slice (so they do not slow it down) on their own stream; only the
+        # reduction at the end of the projection waits for them (prony_exec_info.ev_wait_u)
+        self.su.wait_event(self.ev_vcopied)
+        with torch.cuda.stream(self.su):
+            if uhi > ulo:
+                self.dU[ulo:uhi].copy_(U_h[ulo:uhi], non_blocking=True)
+            self.ev_ucopied.record(self.su)
+        with torch.cuda.stream(main):
             allgather_rows(self.dVpad, self.world, self.rank, self.dVmine, collective=self.collective)
             V = self.dVpad[:self.N]
-        return self(self.dgrid, self.dU, V, self.dsig, self.dz, stream=main, ev_comm=ev_comm)
+        return self(self.dgrid, self.dU, V, self.dsig, self.dz, stream=main, ev_comm=ev_comm, ev_wait_u=self.ev_ucopied)

@@ -42,7 +42,7 @@ def test_exported_symbols_are_c_abi(pb):
 
 def test_abi_version_and_status_strings(pb):
     hdr = open(os.path.join(ROOT, "include", "prony.h")).read()
-    assert pb.lib().prony_abi_version() == int(re.search(r"#define PRONY_ABI_VERSION (\d+)", hdr).group(1)) == 5
+    assert pb.lib().prony_abi_version() == int(re.search(r"#define PRONY_ABI_VERSION (\d+)", hdr).group(1)) == 6
     for code in range(0, 9):
         assert len(pb.status_string(code)) > 0
     assert pb.status_string(12345) == "unknown status"
