@@ -249,6 +249,48 @@ def stamped_traffic():
     return j.get("dram_bytes_per_launch"), os.path.relpath(TRAFFIC_PROFILE, ROOT)
 
 
+def other_configs(names, dev, peak, steps=10, warmup=3):
+    """The other BASELINE configs through the same device path on this GPU (parity cases, not bench lines), so
+    the driver's own run records them too: pencils/s, ms per pencil, k_project ms and its fraction of the
+    measured FP64 peak (real 3M flops). Same timing rules: warm-up, L2 flushed before each step, CUDA events."""
+    import torch
+
+    from paper_2012_11430_b200 import sharding
+    out = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for name in names:
+        prob = W.make_problem(W.CONFIGS[name])
+        c = prob.cfg
+        tg = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        args = [tg(x) for x in (prob.grid, prob.U, prob.V, prob.sigma, prob.z)]
+        pencil = sharding.DistributedPencil(c.d, c.n, c.m, dev)
+        for _ in range(warmup):
+            pencil(*args, stream=stream)
+        torch.cuda.synchronize()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+        for e in ev:
+            for x in e:
+                x.record(stream)
+        torch.cuda.synchronize()
+        for i in range(steps):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record(stream)
+            pencil(*args, stream=stream, ev_project=(ev[i][2], ev[i][3]))
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        assert int(pencil.status.item()) == 0, f"{name}: device status {int(pencil.status.item())}"
+        step = sum(e[0].elapsed_time(e[1]) for e in ev) / steps
+        proj = sum(e[2].elapsed_time(e[3]) for e in ev) / steps
+        achieved = 6.0 * (pencil.last_main_flops / 8.0) / (proj * 1e-3) / 1e12
+        out[name] = {"workload": f"d={c.d} n={c.n} N={c.N} m={c.m} noise={c.noise}", "pencils_per_s": 1e3 / step,
+                     "ms_per_step": step, "k_project_ms": proj,
+                     "k_project_frac": achieved / peak if peak else None}
+        del pencil, args
+    del flush
+    return out
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -482,6 +524,8 @@ def run_ours(args, cfg):
             "clocks": clk,
             "e2e": e2e,
         }
+        if world == 1 and not args.no_other_configs and c.name == "cfg4":
+            line["other_configs"] = other_configs([k for k in ("cfg2", "cfg3", "cfg5") if k in W.CONFIGS], dev, peak)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(prob)
         print(json.dumps(line), flush=True)
@@ -523,6 +567,8 @@ def main():
     ap.add_argument("--cfg", default="cfg4", choices=sorted(W.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the cfg2/cfg3/cfg5 device timings attached to the cfg4 line at N = 1")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--cmul", choices=["3m", "4m"], default=None,
                     help="complex products of the DMMA engine: 3M (Gauss, default) or 4M (sets PRONY_CMUL)")
