@@ -1,7 +1,6 @@
 """Host cost of one small pencil (cfg1): the public call path (sharding.DistributedPencil), the binding
 (binding.pencil), and the bare C entry point with pre-marshalled arguments — where the eager launch time
 goes when the GPU work is ~25 us. Wall clock per call, the GPU kept busy ahead (no host waits)."""
-import ctypes
 import json
 import os
 import sys
