@@ -1,7 +1,9 @@
 """Per-rank device time of the N-way sharded pencil, measured rank by rank on ONE B200 (no collective): for
 N in {1, 2, 4, 8}, rank r runs its SHARED unit slab of prony_project and its column range of
-prony_vandermonde_ls (+ the solve, as the side stream does at N > 1). The max over ranks plus an all-reduce
-estimate is the modelled step of an N-GPU run; the driver's scaling run measures the real one."""
+prony_vandermonde_ls (+ the solve), with the streams of sharding.DistributedPencil at N > 1: the projection on a
+high-priority stream, the LS branch on a normal one released right before k_project (so it runs in k_project's
+last wave). The max over ranks plus an all-reduce estimate is the modelled step of an N-GPU run;
+the driver's scaling run measures the real one."""
 import json
 import os
 import statistics
@@ -29,7 +31,7 @@ G = torch.empty((m, m), dtype=torch.complex128, device="cuda")
 b = torch.empty(m, dtype=torch.complex128, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 side = torch.cuda.Stream()
-main = torch.cuda.current_stream()
+main = torch.cuda.Stream(priority=-1)
 out = {"cfg": name}
 for world in (1, 2, 4, 8):
     per_rank = []
@@ -39,11 +41,14 @@ for world in (1, 2, 4, 8):
         ts = []
         for rep in range(6):
             flush.fill_(rep & 0xFF)
-            e0, e1, ep = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0, e1, ep, pb0, pb1 = (torch.cuda.Event(enable_timing=True) for _ in range(5))
+            for x in (pb0, pb1):
+                x.record(main)
             torch.cuda.synchronize()
             e0.record(main)
-            pb.project(grid, U, V, sigma, d, n, m, u0, u1, pb.UNITS_SHARED, out=S, workspace=ws_p, stream=main)
-            side.wait_event(e0)
+            pb.project(grid, U, V, sigma, d, n, m, u0, u1, pb.UNITS_SHARED, out=S, workspace=ws_p, stream=main,
+                       info=pb.make_exec_info(pb0, pb1))
+            side.wait_event(pb0)  # recorded by the library right before k_project
             ls = pb.vandermonde_ls(z, grid, d, n, m, c0, c1, want_solution=False, out={"G": G, "b": b},
                                    workspace=ws_l, stream=side)
             pb.ls_solve(G, b, z, d, m, stream=side)
