@@ -525,7 +525,11 @@ def run_ours(args, cfg):
             "e2e": e2e,
         }
         if world == 1 and not args.no_other_configs and c.name == "cfg4":
-            line["other_configs"] = other_configs([k for k in ("cfg2", "cfg3", "cfg5") if k in W.CONFIGS], dev, peak)
+            try:  # informational: never let it cost the headline line
+                line["other_configs"] = other_configs([k for k in ("cfg2", "cfg3", "cfg5") if k in W.CONFIGS], dev,
+                                                      peak)
+            except Exception as exc:  # noqa: BLE001
+                line["other_configs"] = {"error": f"{type(exc).__name__}: {exc}"}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(prob)
         print(json.dumps(line), flush=True)
