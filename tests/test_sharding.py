@@ -44,11 +44,13 @@ def _worker(rank, world, port, d, n, m, order, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("d,n,m,order", [(3, 4, 6, 1), (3, 4, 6, 0), (2, 9, 5, 1), (2, 9, 5, 2), (3, 4, 6, 2)])
-def test_allreduce_pencil_world2_gloo(tmp_path, oracle_mod, d, n, m, order):
+@pytest.mark.parametrize("d,n,m,order,world", [(3, 4, 6, 1, 2), (3, 4, 6, 0, 2), (2, 9, 5, 1, 2), (2, 9, 5, 2, 2),
+                                               (3, 4, 6, 2, 2), (2, 9, 5, 2, 3)])
+def test_allreduce_pencil_world2_gloo(tmp_path, oracle_mod, d, n, m, order, world):
+    """world 2 (the contract's case) and an uneven world 3 split of the units and columns."""
     import workload as W
     out = str(tmp_path / "res.npz")
-    mp.spawn(_worker, args=(2, _free_port(), d, n, m, order, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), d, n, m, order, out), nprocs=world, join=True)
     res = np.load(out)
     prob = W.make_problem(W.custom_config(d, n, m, 1e-6, 97), with_svd=True)
     S = oracle_mod.project(prob.grid, prob.U, prob.V, prob.sigma, d, n)
