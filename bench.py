@@ -181,8 +181,9 @@ def cpu_baseline(prob, budget_s=16.0):
 def run_reference(args, cfg):
     """Reference arm: the oracle, as it stands, on host cores; each step = a bounded sample of the same kind as
     the cpu_baseline leg (~7 s of CPU work: large enough that the oracle's per-call marshalling of U, V does not
-    inflate the extrapolation; a 3 s sample read ~20% slower than cpu_baseline's 12 s one). A step computes a known fraction of one pencil (the sampled rows and
-    columns), so ms_per_step is the measured time of that sample and value = fraction / step time = pencils/s."""
+    inflate the extrapolation; a 3 s sample read ~20% slower than cpu_baseline's 12 s one). A step computes a
+    known fraction of one pencil (the sampled rows and columns), so ms_per_step is the measured time of that
+    sample and value = fraction / step time = pencils/s."""
     import oracle
     oracle.build()
     prob = W.make_problem(cfg)
