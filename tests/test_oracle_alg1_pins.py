@@ -393,3 +393,39 @@ def test_perturbation_bounds_hoffman_wielandt_and_tail(oracle_mod):
     tail = math.sqrt(float(np.sum(s1[m:] ** 2)))
     assert tail <= eps * nT
     assert s0[m] <= 1e-12 * s0[0]                    # noise-free T has rank m exactly
+
+
+@pytest.mark.parametrize("d,n,m", [(2, 8, 3), (3, 4, 4)])
+def test_pencil_forward_error_eq_deltaSl(oracle_mod, d, n, m):
+    """PAPER.md:413-418 (eq_deltaSl): with samples f(1 + delta_k), |delta_k| <= eps, the pencil S~_l built from the
+    noisy T's rank-m SVD, compared with S_l of the noise-free T in the gauge of P:332-334 (each column of U scaled
+    by the phase that makes U(:,i)^* U~(:,i) real positive, the same scalars on V), obeys the first-order bound
+    ||S~_l - S_l||_F <= eps ||T_l||_F / sigma~_m (1 + (1 + 4 sqrt2 + (2 + g) sqrt(2m)) ||T||_F / delta_min),
+    delta_i = min{min_{j != i} |sigma_i - sigma~_j|, sigma_i}, with g = 8 (SPEC's default for the
+    paper's unnamed constant) — all from the oracle's own Jacobi SVDs; and the error is linear in eps."""
+    rng = np.random.default_rng(11 + d)
+    t = W.planted_nodes(d, m, n, rng)
+    c = W.planted_coeffs(m, rng)
+    g0 = W.sample_grid(t, c, n)
+    U0, s0, V0, _ = oracle_mod.jacobi_svd(oracle_mod.T_dense(g0, d, n, 0))
+    U, V, sig = U0[:, :m], V0[:, :m], s0[:m]
+    nT = oracle_mod.T_fro(g0, d, n)
+    nTl = [np.linalg.norm(oracle_mod.T_dense(g0, d, n, ell)) for ell in range(1, d + 1)]
+    worst = []
+    for eps in (1e-8, 1e-6):
+        g1 = W.sample_grid(t, c, n, eps, 5, noise_model="disk")
+        U1f, s1, V1f, _ = oracle_mod.jacobi_svd(oracle_mod.T_dense(g1, d, n, 0))
+        U1, V1, sig1 = U1f[:, :m], V1f[:, :m], s1[:m]
+        ph = np.exp(1j * np.angle(np.sum(U.conj() * U1, axis=0)))  # gauge of P:332-334
+        S0 = oracle_mod.project(g0, U * ph, V * ph, sig, d, n)
+        S1 = oracle_mod.project(g1, U1, V1, sig1, d, n)
+        delta_min = min(min(np.min(np.abs(np.delete(s1, i) - sig[i])), sig[i]) for i in range(m))
+        k = (1 + 4 * math.sqrt(2) + 10 * math.sqrt(2 * m)) * nT / delta_min
+        ratios = []
+        for ell in range(d):
+            err = np.linalg.norm(S1[ell] - S0[ell])
+            bound = eps * nTl[ell] / sig1[-1] * (1 + k)
+            assert err <= bound, (eps, ell, err, bound)
+            ratios.append(err / (eps * nTl[ell] / sig1[-1]))
+        worst.append(max(np.linalg.norm(S1[ell] - S0[ell]) for ell in range(d)))
+    assert 50.0 < worst[1] / worst[0] < 200.0  # first order: 100x the noise, 100x the error
