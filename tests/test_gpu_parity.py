@@ -446,12 +446,13 @@ def test_pencil_host_shapes(pb, orc, d, n, m, noise):
     assert rel(out["G"], G_or) <= TOL and rel(out["b"], b_or) <= TOL
 
 
-@pytest.mark.parametrize("kc", ["2", "5", "7"])
-def test_pencil_host_chunk_groups(pb, orc, kc, monkeypatch):
+@pytest.mark.parametrize("kc,cmul", [("2", "3m"), ("5", "3m"), ("7", "3m"), ("5", "4m")])
+def test_pencil_host_chunk_groups(pb, orc, kc, cmul, monkeypatch):
     """The host-input pencil's copy pipeline with the split-K chunk count forced (PRONY_KC, read per call):
     the narrow lead chunk plus 1..3 launch groups of one or several chunks, each released by its own copy
-    event; S, G, b against the oracle."""
+    event (3M and 4M complex products); S, G, b against the oracle."""
     monkeypatch.setenv("PRONY_KC", kc)
+    monkeypatch.setenv("PRONY_CMUL", cmul)
     prob = W.make_problem("cfg2")
     c = prob.cfg
     out = pb.pencil_host(prob.grid, prob.U, prob.V, prob.sigma, prob.z, c.d, c.n, c.m)
